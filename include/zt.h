@@ -1,0 +1,129 @@
+/*
+ * zt.h — C ABI of the B200-native isospectral time-step hot path
+ * (Zeitlin–Euler on the sphere, arXiv 2206.05466).
+ *
+ * One shared library (paper_2206_05466_b200/libzt.so, sm_100a).  Every entry
+ * point takes plain device pointers and sizes, enqueues on the caller's
+ * cudaStream_t (passed as void*), never allocates inside a step call (the
+ * workspace is caller-owned), and returns a zt_status code; details of the
+ * last failure on the calling thread are in zt_last_error().
+ *
+ * Matrices are complex128, row-major, interleaved (re, im) doubles, with a
+ * leading dimension counted in complex elements — i.e. numpy/torch
+ * complex128 C-order memory, zero-copy.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/zeitlin/):
+ *   zt_op_create        laplacian.py:179-219, 319-322  LaplacianOperator / build_operator
+ *   zt_stream_solve     laplacian.py:370-431 (+272-316) solve_stream (check=False body)
+ *   zt_apply_laplacian  laplacian.py:341-367            apply_laplacian
+ *   zt_residuals        laplacian.py:75-104             skewness_residual / trace_residual
+ *   zt_fixed_point      integrator.py:96-138            fixed_point_solve
+ *   zt_midpoint_step    integrator.py:141-171           midpoint_step_info
+ *   zt_zgemm            integrator.py:127-128, 155-156  the numpy `@` products (OpenBLAS zgemm)
+ *   zt_commutator /     integrator.py:127-129           (a - a^H) and the sandwich update
+ *   zt_sandwich
+ */
+#ifndef ZT_H_
+#define ZT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ZT_OK = 0,
+  ZT_EINVAL = 1,      /* bad argument (maps to ValueError) */
+  ZT_ESTRUCTURE = 2,  /* input not skew-Hermitian / traceless (StructureError) */
+  ZT_ENOCONV = 3,     /* fixed point did not reach tol (FixedPointError) */
+  ZT_ELINALG = 4,     /* tridiagonal factorisation failed (LinAlgError) */
+  ZT_ECUDA = 5,       /* CUDA runtime error */
+  ZT_ENCCL = 6,       /* collective failure */
+  ZT_ENOMEM = 7       /* workspace too small / allocation failed */
+} zt_status;
+
+typedef struct zt_operator* zt_op_t;
+
+int zt_version(void);
+const char* zt_strerror(int status);
+const char* zt_last_error(void);
+
+/* Per-N Laplacian operator on `device` (laplacian.py:179-219).  Builds the
+ * per-chunk LDL^T carry tables on the GPU; immutable afterwards and
+ * shareable across streams.  n >= 2. */
+int zt_op_create(int n, int device, zt_op_t* op);
+int zt_op_destroy(zt_op_t op);
+int zt_op_n(zt_op_t op);
+/* Copies the reference-layout factor tables (sheared N x N, laplacian.py:
+ * 213-215) to host arrays (test hook; either pointer may be NULL). */
+int zt_op_factors(zt_op_t op, double* linv_host, double* dinv_host);
+
+/* P = lap^{-1} W for `batch` matrices (laplacian.py:370-431, check=False).
+ * Reads only the lower triangle + diagonal of W; writes the full P (lower
+ * from the solve, strict upper by skew reflection, laplacian.py:306-316).
+ * W and P must not alias.  Strides between batch entries in complex elems. */
+int zt_stream_solve(zt_op_t op, const double* w, int64_t ldw, int64_t stride_w, double* p,
+                    int64_t ldp, int64_t stride_p, int batch, void* stream);
+
+/* Same with caller-owned carry workspace of zt_solve_workspace_bytes(n,
+ * batch) bytes (no allocation; graph-capturable). */
+size_t zt_solve_workspace_bytes(int n, int batch);
+int zt_stream_solve_ws(zt_op_t op, const double* w, int64_t ldw, int64_t stride_w, double* p,
+                       int64_t ldp, int64_t stride_p, int batch, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Y = sign * stencil(W) over diagonals (laplacian.py:341-367), sign = +-1;
+ * lower triangle of W read only; bit-identical to the reference. */
+int zt_apply_laplacian(zt_op_t op, const double* w, int64_t ldw, int64_t stride_w, double* y,
+                       int64_t ldy, int64_t stride_y, int sign, int batch, void* stream);
+
+/* out_dev[0] = ||W + W^H||_F / ||W||_F, out_dev[1] = |tr W| / ||W||_F,
+ * out_dev[2] = ||W||_F (device doubles; 0,0,0 for the zero matrix). */
+int zt_residuals(int n, const double* w, int64_t ldw, double* out_dev, void* stream);
+size_t zt_resid_workspace_bytes(int n);
+int zt_residuals_ws(int n, const double* w, int64_t ldw, double* out_dev, void* workspace,
+                    void* stream);
+
+/* C = A @ B (complex128, n x n, all row-major).  `algo` 0 = 3M (Gauss)
+ * DMMA, 1 = 4M DMMA.  Used by the GEMM op benchmark and casimirs. */
+int zt_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+             int64_t ldc, int algo, void* stream);
+
+/* Workspace for zt_fixed_point / zt_midpoint_step at size n (bytes). */
+size_t zt_step_workspace_bytes(int n);
+
+/* Fixed-point solve for W~ (integrator.py:96-138).  wt receives W~;
+ * *iterations / *residual report the loop; returns ZT_ENOCONV (with both
+ * filled) when max_iter is exhausted, ZT_ESTRUCTURE when W_n fails the
+ * 1e-10 skew/trace gate (laplacian.py:107-116).  Synchronises the stream
+ * once per iteration (4-byte residual read-back). */
+int zt_fixed_point(zt_op_t op, const double* wn, double* wt, double h, double tol, int max_iter,
+                   void* workspace, size_t workspace_bytes, int* iterations, double* residual,
+                   void* stream);
+
+/* One midpoint step (integrator.py:141-171): w_next = W_{n+1} from w_n with
+ * h_eff = h * comm_scale.  If consistency != NULL it receives
+ * max|W~ - (h/2)(a-a^H) - (h^2/4) a P~ - W_n| (integrator.py:160-163).
+ * w_next must not alias w_n. */
+int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff, double tol,
+                     int max_iter, void* workspace, size_t workspace_bytes, int* iterations,
+                     double* residual, double* consistency, void* stream);
+
+/* Config-3 ops (integrator.py:127-129): commutator C = P W - W P = a - a^H
+ * with a = P W; sandwich S = W - (h/2)(a - a^H) - (h^2/4) a P
+ * = (I - hP/2) W (I + hP/2).  `work` holds n*n complex (a). */
+int zt_commutator(int n, const double* p, const double* w, double* c, double* work, void* stream);
+int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work,
+                void* stream);
+
+/* Number of kernels this library launched since load (device-side work
+ * evidence for the bench's gpu_launches claim). */
+int64_t zt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZT_H_ */

@@ -1,0 +1,42 @@
+"""B200-native isospectral time-step hot path (arXiv 2206.05466).
+
+Drop-in for the reference package's step / stream-solve API
+(/root/reference/pkg/src/zeitlin/__init__.py:27-48): the same names, backed
+by hand-written sm_100a kernels in ``libzt.so`` (C ABI: include/zt.h).
+"""
+
+from .diagnostics import hamiltonian
+from .integrator import (
+    FixedPointError,
+    StepInfo,
+    StepperState,
+    casimirs,
+    casimirs_from_spectrum,
+    commutator_scale,
+    default_time_step,
+    fixed_point_solve,
+    midpoint_step,
+    midpoint_step_info,
+)
+from .laplacian import (
+    LaplacianBlock,
+    LaplacianOperator,
+    StructureError,
+    apply_laplacian,
+    build_block,
+    build_operator,
+    skewness_residual,
+    solve_stream,
+    solve_stream_batched,
+    spectral_norm,
+    trace_residual,
+    validate_vorticity,
+)
+
+__all__ = [
+    "FixedPointError", "StepInfo", "StepperState", "casimirs", "casimirs_from_spectrum",
+    "commutator_scale", "default_time_step", "fixed_point_solve", "midpoint_step",
+    "midpoint_step_info", "LaplacianBlock", "LaplacianOperator", "StructureError",
+    "apply_laplacian", "build_block", "build_operator", "skewness_residual", "solve_stream",
+    "solve_stream_batched", "spectral_norm", "trace_residual", "validate_vorticity", "hamiltonian",
+]

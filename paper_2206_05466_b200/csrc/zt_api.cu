@@ -1,0 +1,295 @@
+// C ABI (include/zt.h) and the device-resident fixed-point / midpoint step
+// driver (integrator.py:96-171) for sm_100a.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "zt_common.cuh"
+
+
+
+namespace zt {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const std::string& msg) { t_err = msg; }
+int fail(int status, const std::string& msg) {
+  t_err = msg;
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  t_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return ZT_ECUDA;
+}
+
+// implemented in zt_solve.cu / zt_gemm.cu
+int op_create(int n, int device, zt_operator** out);
+int op_destroy(zt_operator* op);
+int op_factors(zt_operator* op, double* linv_h, double* dinv_h);
+size_t solve_workspace_bytes(int n, int batch);
+int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
+                 int64_t sp, int batch, void* ws, size_t ws_bytes, cudaStream_t st);
+int apply_laplacian(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* y,
+                    int64_t ldy, int64_t sy, int sign, int batch, cudaStream_t st);
+size_t resid_workspace_bytes(int n);
+int residuals(int n, const double* w, int64_t ldw, double* out, void* ws, cudaStream_t st);
+int zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+          int algo, cudaStream_t st);
+int zgemm_update(int n, const double* amat, const double* p, const double* base, const double* xprev,
+                 const double* wn, double* out, int64_t ld, double hh, double qq,
+                 unsigned long long* resid, unsigned long long* cons, int algo, cudaStream_t st);
+int skew_diff(int n, const double* a, double* c, cudaStream_t st);
+
+static int g_algo = 0;  // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
+
+// ---- step workspace layout -------------------------------------------------
+struct StepWS {
+  double* p;     // n x n complex: stream matrix
+  double* a;     // n x n complex: a = P X
+  void* solve;   // solve carries
+  size_t solve_bytes;
+  void* resid;   // residual partials
+  unsigned long long* flags;  // [0] residual bits, [1] consistency bits
+  double* val;   // [0..2] validation residuals
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t ws_layout(int n, char* base, StepWS* w) {
+  const size_t mat = align_up((size_t)n * n * 16);
+  const size_t sb = align_up(solve_workspace_bytes(n, 1));
+  const size_t rb = align_up(resid_workspace_bytes(n));
+  size_t off = 0;
+  if (w) {
+    w->p = reinterpret_cast<double*>(base + off);
+    w->a = reinterpret_cast<double*>(base + off + mat);
+    w->solve = base + off + 2 * mat;
+    w->solve_bytes = sb;
+    w->resid = base + off + 2 * mat + sb;
+    w->flags = reinterpret_cast<unsigned long long*>(base + off + 2 * mat + sb + rb);
+    w->val = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 64);
+  }
+  return 2 * mat + sb + rb + 256;
+}
+
+// small pinned host mailbox for the per-iteration read-back
+struct Mailbox {
+  unsigned long long* h = nullptr;
+  Mailbox() {
+    if (cudaHostAlloc(&h, 64 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) h = nullptr;
+  }
+};
+static thread_local Mailbox t_mail;
+
+static double bits_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+// One update: P = lap^-1 X; a = P X; out = base + hh (a - a^H) + qq a P.
+static int update(zt_operator* op, const double* x, const double* base, const double* xprev,
+                  const double* wn, double* out, double hh, double qq, StepWS& w,
+                  unsigned long long* resid, unsigned long long* cons, cudaStream_t st) {
+  const int n = op->n;
+  int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
+  if (rc) return rc;
+  rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
+  if (rc) return rc;
+  return zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, g_algo, st);
+}
+
+static int fixed_point_impl(zt_operator* op, const double* wn, double* x, double h, double tol,
+                            int max_iter, StepWS& w, int* iterations, double* residual,
+                            cudaStream_t st) {
+  const int n = op->n;
+  if (!(h >= 0.0)) return fail(ZT_EINVAL, "time-step must be nonnegative, got " + std::to_string(h));
+  if (!(tol > 0.0)) return fail(ZT_EINVAL, "tolerance must be positive, got " + std::to_string(tol));
+  if (max_iter < 1) return fail(ZT_EINVAL, "max_iter must be at least 1, got " + std::to_string(max_iter));
+  if (!t_mail.h) return fail(ZT_ENOMEM, "pinned mailbox allocation failed");
+  // input gate (integrator.py:121 -> laplacian.py:107-116), checked at the
+  // first read-back; the loop is enqueued behind it without a sync.
+  int rc = residuals(n, wn, n, w.val, w.resid, st);
+  if (rc) return rc;
+  ZT_CUDA_CHECK(cudaMemcpyAsync(x, wn, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, st));
+  const double hh = 0.5 * h, qq = 0.25 * h * h;
+  double r = INFINITY;
+  for (int k = 1; k <= max_iter; ++k) {
+    ZT_CUDA_CHECK(cudaMemsetAsync(w.flags, 0, sizeof(unsigned long long), st));
+    // in place: X <- W_n + (h/2)(a - a^H) + (h^2/4) a P, residual vs old X
+    rc = update(op, x, wn, x, nullptr, x, hh, qq, w, w.flags, nullptr, st);
+    if (rc) return rc;
+    ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h, w.flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (k == 1) ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h + 1, w.val, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    ZT_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (k == 1) {
+      const double sk = bits_to_double(t_mail.h[1]), tr = bits_to_double(t_mail.h[2]);
+      char buf[160];
+      if (sk > 1e-10) {  // NaN passes, as `r > tol` in the reference
+        snprintf(buf, sizeof buf, "matrix is not skew-Hermitian: residual %.3e > 1.0e-10", sk);
+        return fail(ZT_ESTRUCTURE, buf);
+      }
+      if (tr > 1e-10) {
+        snprintf(buf, sizeof buf, "matrix is not traceless: residual %.3e > 1.0e-10", tr);
+        return fail(ZT_ESTRUCTURE, buf);
+      }
+    }
+    r = bits_to_double(t_mail.h[0]);
+    *iterations = k;
+    *residual = r;
+    if (r <= tol) return ZT_OK;
+  }
+  char buf[200];
+  snprintf(buf, sizeof buf,
+           "fixed-point iteration did not reach tol=%.1e in %d iterations (last residual %.3e)", tol,
+           max_iter, r);
+  return fail(ZT_ENOCONV, buf);
+}
+
+}  // namespace zt
+
+using namespace zt;
+
+extern "C" {
+
+int zt_version(void) { return 1; }
+
+const char* zt_strerror(int s) {
+  switch (s) {
+    case ZT_OK: return "ok";
+    case ZT_EINVAL: return "invalid argument";
+    case ZT_ESTRUCTURE: return "structure violation";
+    case ZT_ENOCONV: return "fixed point did not converge";
+    case ZT_ELINALG: return "factorisation failed";
+    case ZT_ECUDA: return "CUDA error";
+    case ZT_ENCCL: return "collective error";
+    case ZT_ENOMEM: return "out of memory / workspace too small";
+    default: return "unknown status";
+  }
+}
+
+const char* zt_last_error(void) { return t_err.c_str(); }
+
+int64_t zt_launch_count(void) { return g_launches.load(); }
+
+int zt_op_create(int n, int device, zt_op_t* op) {
+  if (!op) return fail(ZT_EINVAL, "null output");
+  if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : 0;
+  return op_create(n, device, op);
+}
+int zt_op_destroy(zt_op_t op) { return op_destroy(op); }
+int zt_op_n(zt_op_t op) { return op ? op->n : -1; }
+int zt_op_factors(zt_op_t op, double* linv, double* dinv) { return op_factors(op, linv, dinv); }
+
+size_t zt_solve_workspace_bytes(int n, int batch) { return solve_workspace_bytes(n, batch); }
+
+int zt_stream_solve_ws(zt_op_t op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
+                       int64_t sp, int batch, void* ws, size_t ws_bytes, void* stream) {
+  if (!op || !w || !p || batch < 1) return fail(ZT_EINVAL, "zt_stream_solve: bad argument");
+  return stream_solve(op, w, ldw, sw, p, ldp, sp, batch, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int zt_stream_solve(zt_op_t op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
+                    int64_t sp, int batch, void* stream) {
+  // convenience form: allocates its carry workspace with stream-ordered
+  // cudaMallocAsync (pool-backed, no device sync)
+  if (!op || !w || !p || batch < 1) return fail(ZT_EINVAL, "zt_stream_solve: bad argument");
+  const size_t b = solve_workspace_bytes(op->n, batch);
+  void* ws = nullptr;
+  ZT_CUDA_CHECK(cudaMallocAsync(&ws, b, (cudaStream_t)stream));
+  int rc = stream_solve(op, w, ldw, sw, p, ldp, sp, batch, ws, b, (cudaStream_t)stream);
+  cudaFreeAsync(ws, (cudaStream_t)stream);
+  return rc;
+}
+
+int zt_apply_laplacian(zt_op_t op, const double* w, int64_t ldw, int64_t sw, double* y, int64_t ldy,
+                       int64_t sy, int sign, int batch, void* stream) {
+  if (!op || !w || !y || batch < 1) return fail(ZT_EINVAL, "zt_apply_laplacian: bad argument");
+  return apply_laplacian(op, w, ldw, sw, y, ldy, sy, sign, batch, (cudaStream_t)stream);
+}
+
+size_t zt_resid_workspace_bytes(int n) { return resid_workspace_bytes(n); }
+
+int zt_residuals_ws(int n, const double* w, int64_t ldw, double* out, void* ws, void* stream) {
+  if (n < 1 || !w || !out) return fail(ZT_EINVAL, "zt_residuals: bad argument");
+  return residuals(n, w, ldw, out, ws, (cudaStream_t)stream);
+}
+
+int zt_residuals(int n, const double* w, int64_t ldw, double* out, void* stream) {
+  if (n < 1 || !w || !out) return fail(ZT_EINVAL, "zt_residuals: bad argument");
+  const size_t b = resid_workspace_bytes(n);
+  void* ws = nullptr;
+  ZT_CUDA_CHECK(cudaMallocAsync(&ws, b, (cudaStream_t)stream));
+  int rc = residuals(n, w, ldw, out, ws, (cudaStream_t)stream);
+  cudaFreeAsync(ws, (cudaStream_t)stream);
+  return rc;
+}
+
+int zt_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+             int algo, void* stream) {
+  if (n < 1 || !a || !b || !c) return fail(ZT_EINVAL, "zt_zgemm: bad argument");
+  return zgemm(n, a, lda, b, ldb, c, ldc, algo, (cudaStream_t)stream);
+}
+
+size_t zt_step_workspace_bytes(int n) { return ws_layout(n, nullptr, nullptr); }
+
+int zt_fixed_point(zt_op_t op, const double* wn, double* wt, double h, double tol, int max_iter,
+                   void* workspace, size_t workspace_bytes, int* iterations, double* residual,
+                   void* stream) {
+  if (!op || !wn || !wt || !workspace || !iterations || !residual)
+    return fail(ZT_EINVAL, "zt_fixed_point: bad argument");
+  if (workspace_bytes < zt_step_workspace_bytes(op->n)) return fail(ZT_ENOMEM, "step workspace too small");
+  StepWS w;
+  ws_layout(op->n, reinterpret_cast<char*>(workspace), &w);
+  return fixed_point_impl(op, wn, wt, h, tol, max_iter, w, iterations, residual, (cudaStream_t)stream);
+}
+
+int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff, double tol,
+                     int max_iter, void* workspace, size_t workspace_bytes, int* iterations,
+                     double* residual, double* consistency, void* stream) {
+  if (!op || !wn || !w_next || !workspace || !iterations || !residual)
+    return fail(ZT_EINVAL, "zt_midpoint_step: bad argument");
+  if (wn == w_next) return fail(ZT_EINVAL, "zt_midpoint_step: w_next must not alias w_n");
+  if (workspace_bytes < zt_step_workspace_bytes(op->n)) return fail(ZT_ENOMEM, "step workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  StepWS w;
+  ws_layout(op->n, reinterpret_cast<char*>(workspace), &w);
+  int rc = fixed_point_impl(op, wn, w_next, h_eff, tol, max_iter, w, iterations, residual, st);
+  if (rc) return rc;
+  // final update (integrator.py:154-158): W_{n+1} = W~ + (h/2)(a - a^H) - (h^2/4) a P~
+  const double hh = 0.5 * h_eff, q = 0.25 * h_eff * h_eff;
+  if (consistency) ZT_CUDA_CHECK(cudaMemsetAsync(w.flags + 1, 0, sizeof(unsigned long long), st));
+  rc = update(op, w_next, w_next, nullptr, consistency ? wn : nullptr, w_next, hh, -q, w, nullptr,
+              consistency ? w.flags + 1 : nullptr, st);
+  if (rc) return rc;
+  if (consistency) {
+    ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h + 4, w.flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    ZT_CUDA_CHECK(cudaStreamSynchronize(st));
+    *consistency = bits_to_double(t_mail.h[4]);
+  }
+  return ZT_OK;
+}
+
+int zt_commutator(int n, const double* p, const double* w, double* c, double* work, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
+  if (rc) return rc;
+  return skew_diff(n, work, c, st);
+}
+
+int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work, void* stream) {
+  // S = W - (h/2)(a - a^H) - (h^2/4) a P  with a = P W
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
+  if (rc) return rc;
+  return zgemm_update(n, work, p, w, nullptr, nullptr, s, n, -0.5 * h, -0.25 * h * h, nullptr, nullptr,
+                      g_algo, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// Shared helpers for the sm_100a isospectral hot path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/zt.h"
+
+// Per-N operator (opaque to C callers): closed-form sqrt table, deflated
+// m = 0 factors, and per-(chunk, diagonal) pivots / carry gains.
+struct zt_operator {
+  int n = 0, device = 0, C = 0;
+  double* sqB = nullptr;
+  double* L0 = nullptr;
+  double* dinv0 = nullptr;
+  double* d0 = nullptr;
+  double* lin = nullptr;
+  double* G = nullptr;
+  double* H = nullptr;
+  double* K = nullptr;
+  void* block = nullptr;  // single allocation holding every table
+};
+
+namespace zt {
+
+extern std::atomic<int64_t> g_launches;
+
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define ZT_CUDA_CHECK(expr)                                   \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::zt::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define ZT_LAUNCHED() ::zt::g_launches.fetch_add(1, std::memory_order_relaxed)
+
+// complex128 as double2 (re, im) — matches numpy/torch interleaved layout
+struct cplx {
+  double re, im;
+};
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 ld2_plain(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// Separately rounded real*complex and complex ops (no FMA contraction) so
+// sweeps and stencils follow the reference's numpy/numba rounding exactly.
+__device__ __forceinline__ double2 rmul(double a, double2 z) {
+  return make_double2(__dmul_rn(a, z.x), __dmul_rn(a, z.y));
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+
+// Closed-form block entries (laplacian.py:129-137).  All quantities are
+// exact in binary64 for n < 2^26: diag is a half-integer combination.
+__device__ __forceinline__ double block_diag(int n, int m, int k) {
+  const double s = (n - 1) * 0.5;
+  const double kd = (double)k;
+  return 2.0 * (s * (2.0 * kd + 1.0 + (double)m) - kd * (kd + (double)m));
+}
+
+// Max of a non-negative double via integer atomics on the bit pattern.
+// fabs() clears the sign so NaN (0x7ff8...) orders above +inf: a NaN
+// residual propagates to "not converged" as in the reference.
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, double v) {
+  atomicMax(addr, (unsigned long long)__double_as_longlong(fabs(v)));
+}
+
+}  // namespace zt

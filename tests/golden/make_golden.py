@@ -1,0 +1,130 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Run in the build container only (it imports the read-only reference from
+/root/reference/pkg/src); the outputs are committed as small .npz fixtures so
+the GPU box, which has no /root/reference, can check against them:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Contents (all complex128 C-order unless noted):
+  solve_small.npz   per N in SOLVE_NS: W (random_admissible, seed 1000+N),
+                    P = solve_stream(W), A = apply_laplacian(W) (sign -1),
+                    plus the reference operator's factor tables at N=17
+  cfg1.npz          BASELINE cfg 1: N=128, W0 = random_admissible(128,
+                    default_rng(0), 1/128), h=0.01, 10 steps: W1, W10,
+                    iterations per step, fixed-point residual traces of step 1,
+                    casimirs(w,3) and hamiltonian at every step
+  cfg4_n64.npz      cfg 4 recipe at N=64 (smooth W0, h=0.005), 20 steps: W20,
+                    per-step iterations, C2/C3/H series
+  known.npz         known answers: pinv-oracle P at N=5, casimirs of
+                    i*diag(1,-1,0,0), blocks N=2 m=0 / N=3 m=1
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+from conftest import casimir_laplacian_dense, random_admissible  # noqa: E402
+from zeitlin import diagnostics, integrator, laplacian  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+SOLVE_NS = (2, 3, 5, 8, 17, 40, 64, 97)
+
+
+def solve_small():
+    d = {}
+    for n in SOLVE_NS:
+        w = random_admissible(n, np.random.default_rng(1000 + n), 1.0 / n)
+        d[f"W_{n}"] = w
+        d[f"P_{n}"] = laplacian.solve_stream(w)
+        d[f"A_{n}"] = laplacian.apply_laplacian(w)
+        d[f"Ap_{n}"] = laplacian.apply_laplacian(w, sign=1)
+    op = laplacian.build_operator(17)
+    d["linv_17"] = op._solve_linv
+    d["dinv_17"] = op._solve_dinv
+    d["sdiag_17"] = op._stencil_diag
+    d["soff_17"] = op._stencil_off
+    np.savez_compressed(os.path.join(OUT, "solve_small.npz"), **d)
+
+
+def run_steps(w0, h, steps, keep=()):
+    st = integrator.StepperState(w=w0.copy(), h=h)
+    iters, c, hh, kept = [], [], [], {}
+    c.append(integrator.casimirs(st.w, 3))
+    hh.append(diagnostics.hamiltonian(st.w))
+    for s in range(1, steps + 1):
+        st, info = integrator.midpoint_step_info(st)
+        iters.append(info.iterations)
+        c.append(integrator.casimirs(st.w, 3))
+        hh.append(diagnostics.hamiltonian(st.w))
+        if s in keep:
+            kept[s] = st.w.copy()
+    return st, np.array(iters), np.array(c), np.array(hh), kept
+
+
+def fp_trace(w0, h):
+    """Residuals of every fixed-point iterate, by re-running with max_iter=k."""
+    res = []
+    for k in range(1, 11):
+        try:
+            integrator.fixed_point_solve(w0, h, max_iter=k)
+            break
+        except integrator.FixedPointError as e:
+            res.append(e.residual)
+    return np.array(res)
+
+
+def cfg1():
+    n = 128
+    w0 = random_admissible(n, np.random.default_rng(0), 1.0 / n)
+    st, iters, c, hh, kept = run_steps(w0, 0.01, 10, keep=(1,))
+    np.savez_compressed(
+        os.path.join(OUT, "cfg1.npz"),
+        W0=w0, W1=kept[1], W10=st.w, iters=iters, casimirs=c, H=hh,
+        fp_residuals_step1=fp_trace(w0, 0.01),
+    )
+
+
+def cfg4_n64():
+    n = 64
+    r = random_admissible(n, np.random.default_rng(0), 1.0 / n)
+    w0 = laplacian.solve_stream(r)
+    w0 /= np.linalg.norm(w0)
+    st, iters, c, hh, _ = run_steps(w0, 0.005, 20)
+    np.savez_compressed(
+        os.path.join(OUT, "cfg4_n64.npz"), W0=w0, W20=st.w, iters=iters, casimirs=c, H=hh
+    )
+
+
+def known():
+    n = 5
+    w = random_admissible(n, np.random.default_rng(5), 1.0)
+    basis = np.eye(n * n, dtype=complex).reshape(n * n, n, n)
+    op_dense = np.stack([casimir_laplacian_dense(e).ravel() for e in basis], axis=1)
+    p_pinv = (np.linalg.pinv(op_dense) @ w.ravel()).reshape(n, n)
+    wd = 1j * np.diag([1.0, -1.0, 0.0, 0.0]).astype(complex)
+    b20 = laplacian.build_block(2, 0)
+    b31 = laplacian.build_block(3, 1)
+    np.savez_compressed(
+        os.path.join(OUT, "known.npz"),
+        W5=w, P5_pinv=p_pinv, P5_ref=laplacian.solve_stream(w),
+        casimir_diag=integrator.casimirs(wd, 4),
+        b20_diag=b20.diag, b20_off=b20.offdiag, b31_diag=b31.diag, b31_off=b31.offdiag,
+    )
+
+
+if __name__ == "__main__":
+    solve_small()
+    cfg1()
+    cfg4_n64()
+    known()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -1,0 +1,95 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+The goldens come from tests/golden/make_golden.py (runs the reference
+``zeitlin`` package from /root/reference).  These checks make the oracle a
+trusted checker for the GPU parity tests.
+"""
+
+import numpy as np
+import pytest
+from conftest import relf
+
+from oracle import zeitlin_oracle as zo
+
+SOLVE_NS = (2, 3, 5, 8, 17, 40, 64, 97)
+
+
+@pytest.mark.parametrize("n", SOLVE_NS)
+def test_solve_and_apply_match_reference(n, golden):
+    g = golden("solve_small.npz")
+    w = g[f"W_{n}"]
+    assert relf(zo.solve_stream(w), g[f"P_{n}"]) <= 1e-14
+    # the stencil is evaluated in the reference's exact operation order
+    np.testing.assert_array_equal(zo.apply_laplacian(w), g[f"A_{n}"])
+    np.testing.assert_array_equal(zo.apply_laplacian(w, sign=1), g[f"Ap_{n}"])
+
+
+def test_operator_tables_bit_identical(golden):
+    g = golden("solve_small.npz")
+    op = zo.OracleOperator(17)
+    np.testing.assert_array_equal(op.linv, g["linv_17"])
+    np.testing.assert_array_equal(op.dinv, g["dinv_17"])
+    np.testing.assert_array_equal(op.stencil_diag, g["sdiag_17"])
+    np.testing.assert_array_equal(op.stencil_off, g["soff_17"])
+
+
+def test_known_answers(golden):
+    k = golden("known.npz")
+    assert np.max(np.abs(zo.solve_stream(k["W5"]) - k["P5_pinv"])) <= 1e-11
+    np.testing.assert_allclose(k["casimir_diag"], [0.0, -2.0, 0.0, 2.0], atol=1e-15)
+    wd = 1j * np.diag([1.0, -1.0, 0.0, 0.0]).astype(complex)
+    np.testing.assert_allclose(zo.casimirs(wd, 4), k["casimir_diag"], atol=1e-15)
+    d, o = zo.block_entries(2, 0)
+    np.testing.assert_array_equal(d, k["b20_diag"])
+    np.testing.assert_array_equal(o, k["b20_off"])
+    d, o = zo.block_entries(3, 1)
+    np.testing.assert_array_equal(d, k["b31_diag"])
+    np.testing.assert_array_equal(o, k["b31_off"])  # sqrt(2)*sqrt(2), 1 ulp off -2
+
+
+def test_cfg1_steps_match_reference(golden):
+    g = golden("cfg1.npz")
+    w = g["W0"]
+    w0 = zo.random_admissible(128, np.random.default_rng(0), 1.0 / 128)
+    np.testing.assert_array_equal(w, w0)  # generator reproducible here
+    iters = []
+    for s in range(10):
+        w, k, _ = zo.midpoint_step(w, 0.01)
+        iters.append(k)
+        if s == 0:
+            assert relf(w, g["W1"]) <= 1e-14
+    assert iters == list(g["iters"])
+    assert relf(w, g["W10"]) <= 1e-13
+    np.testing.assert_allclose(zo.casimirs(w, 3), g["casimirs"][-1], rtol=1e-12, atol=1e-15)
+    assert abs(zo.hamiltonian(w) - g["H"][-1]) <= 1e-14 * abs(g["H"][-1])
+
+
+def test_cfg4_recipe_n64_matches_reference(golden):
+    g = golden("cfg4_n64.npz")
+    w = zo.smooth_initial(64)
+    assert relf(w, g["W0"]) <= 1e-14
+    iters = []
+    for _ in range(20):
+        w, k, _ = zo.midpoint_step(w, 0.005)
+        iters.append(k)
+    assert iters == list(g["iters"])
+    assert relf(w, g["W20"]) <= 1e-12
+
+
+def test_fixed_point_residual_trace(golden):
+    g = golden("cfg1.npz")
+    tr = []
+    zo.fixed_point_solve(g["W0"], 0.01, trace=tr)
+    ref = g["fp_residuals_step1"]
+    np.testing.assert_allclose(tr[: len(ref)], ref, rtol=1e-6)
+
+
+def test_oracle_errors():
+    w = zo.random_admissible(8, np.random.default_rng(3))
+    with pytest.raises(zo.OracleStructureError):
+        zo.solve_stream(w + 1e-3j * np.eye(8))
+    with pytest.raises(ValueError, match="does not match"):
+        zo.apply_laplacian(w, op=zo.build_operator(6))
+    with pytest.raises(zo.OracleFixedPointError) as e:
+        zo.fixed_point_solve(w / 4, 0.05, tol=1e-14, max_iter=1)
+    assert e.value.iterations == 1 and e.value.residual > 1e-14

@@ -1,0 +1,123 @@
+"""GPU parity of the isospectral step (fixed point + final update) and the
+complex128 DMMA GEMM against the oracle and the reference goldens."""
+
+import numpy as np
+import pytest
+from conftest import relf
+
+from oracle import zeitlin_oracle as zo
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def zt():
+    import paper_2206_05466_b200 as m
+
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+@pytest.mark.parametrize("n", (1, 2, 3, 8, 17, 63, 64, 65, 100, 128, 256, 333))
+@pytest.mark.parametrize("algo", (0, 1))
+def test_zgemm_vs_numpy(zt, n, algo):
+    rng = np.random.default_rng(n)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    b = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    c = zt.integrator.zgemm(dev(a), dev(b), algo=algo).cpu().numpy()
+    assert relf(c, a @ b) <= 1e-14
+
+
+def test_cfg1_ten_steps_match_reference(zt, golden):
+    g = golden("cfg1.npz")
+    st = zt.StepperState(w=dev(g["W0"]), h=0.01)
+    iters = []
+    for s in range(10):
+        st, info = zt.midpoint_step_info(st)
+        iters.append(info.iterations)
+        if s == 0:
+            assert relf(st.w.cpu().numpy(), g["W1"]) <= 1e-12
+    assert iters == list(g["iters"])
+    w = st.w.cpu().numpy()
+    assert relf(w, g["W10"]) <= 1e-10
+    c = zt.casimirs(st.w, 3)
+    c0 = g["casimirs"][0]
+    # drift no larger than the reference's (with a round-off floor)
+    ref_drift = np.abs(g["casimirs"][-1] - c0)
+    assert np.all(np.abs(c[1:] - c0[1:]) <= np.maximum(ref_drift[1:], 1e-13 * np.abs(c0[1:])))
+    h = zt.hamiltonian(st.w)
+    assert abs(h - g["H"][0]) <= max(abs(g["H"][-1] - g["H"][0]), 1e-13 * abs(g["H"][0]))
+
+
+def test_cfg4_recipe_n64(zt, golden):
+    g = golden("cfg4_n64.npz")
+    st = zt.StepperState(w=dev(g["W0"]), h=0.005)
+    iters = []
+    for _ in range(20):
+        st, info = zt.midpoint_step_info(st)
+        iters.append(info.iterations)
+    assert iters == list(g["iters"])
+    assert relf(st.w.cpu().numpy(), g["W20"]) <= 1e-10
+
+
+def test_zero_step_is_exact(zt):
+    w = zo.random_admissible(8, np.random.default_rng(0))
+    wt, it = zt.fixed_point_solve(w, h=0.0)
+    assert it == 1
+    np.testing.assert_array_equal(wt, w)
+
+
+def test_errors(zt):
+    w = zo.random_admissible(8, np.random.default_rng(1))
+    with pytest.raises(zt.StructureError):
+        zt.fixed_point_solve(w + 0.01 * np.eye(8), h=1e-3)
+    with pytest.raises(ValueError):
+        zt.fixed_point_solve(w, h=-1.0)
+    with pytest.raises(ValueError):
+        zt.fixed_point_solve(w, h=1e-3, tol=0.0)
+    with pytest.raises(ValueError):
+        zt.fixed_point_solve(w, h=1e-3, max_iter=0)
+    w16 = zo.random_admissible(16, np.random.default_rng(2))
+    w16 /= np.max(np.abs(np.linalg.eigvalsh(1j * w16)))
+    with pytest.raises(zt.FixedPointError) as e:
+        zt.fixed_point_solve(w16, h=0.05, tol=1e-14, max_iter=1)
+    assert e.value.residual > 1e-14 and e.value.iterations == 1
+
+
+def test_zero_state_and_bookkeeping(zt):
+    st = zt.StepperState(w=np.zeros((6, 6), dtype=complex), h=1e-2)
+    out = zt.midpoint_step(st)
+    assert np.all(out.w == 0.0)
+    assert out.step_index == 1 and abs(out.time - 1e-2) < 1e-15
+
+
+def test_consistency_and_comm_scale(zt):
+    w = zo.smooth_initial(12)
+    st = zt.StepperState(w=w, h=1e-3, tol=1e-13)
+    _, info = zt.midpoint_step_info(st, check_consistency=True)
+    assert info.consistency_error <= 1e-12
+    a = zt.midpoint_step(zt.StepperState(w=w.copy(), h=1e-3, comm_scale=4.0)).w
+    b = zt.midpoint_step(zt.StepperState(w=w.copy(), h=4e-3, comm_scale=1.0)).w
+    np.testing.assert_allclose(a, b, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", (200, 512))
+def test_step_vs_oracle_midsize(zt, n):
+    w = zo.smooth_initial(n)
+    ref = w
+    x = dev(w)
+    for _ in range(3):
+        ref, kr, _ = zo.midpoint_step(ref, 0.005)
+        x, k, _, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, zt.build_operator(n))
+        assert k == kr
+    assert relf(x.cpu().numpy(), ref) <= 1e-12
+
+
+def test_casimirs_match_oracle(zt):
+    w = zo.random_admissible(16, np.random.default_rng(3))
+    for k in (2, 5, 9):
+        np.testing.assert_allclose(zt.casimirs(dev(w), k), zo.casimirs(w, k), rtol=1e-12, atol=1e-12)
