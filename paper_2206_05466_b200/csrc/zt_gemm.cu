@@ -8,9 +8,12 @@
 //  * sm_100a has no tcgen05 kind::f64, so FP64 MMA is the warp-level
 //    mma.sync m8n8k4 (SASS DMMA.8x8x4, 64 FMA/clk/SM measured = 37 TF at
 //    1.965 GHz).  The kernel is warp-specialised Blackwell style anyway:
-//    one producer warp streams operand rows with cp.async.bulk (TMA engine,
-//    UBLKCP) into padded, bank-conflict-free shared-memory stages guarded
-//    by mbarriers (full/empty ring); 8 consumer warps issue DMMA.
+//    one producer thread streams operand tiles with 2D TMA
+//    (cp.async.bulk.tensor, 128B swizzle, OOB zero fill) into a ring of
+//    shared-memory stages guarded by mbarriers (full/empty); 8 consumer
+//    warps issue DMMA.  Fragment k-indices are permuted (DMMA k-slot kk of
+//    k4-step s reads 16B chunk 2kk+(s&1) of the 128B swizzle row) so every
+//    LDS.128 fragment load is bank-conflict free under the swizzle.
 //  * complex products use the 3M (Gauss) form by default:
 //      T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi); Cr = T1-T2, Ci = T3-T1-T2
 //    — 3 real MMAs per complex MMA instead of 4 (25% fewer DMMA), operand
@@ -23,7 +26,11 @@
 //    reduces max|new - X| (fixed-point residual, integrator.py:129) and
 //    optionally max|recon - W_n| (consistency, integrator.py:160-163) with
 //    one atomic per CTA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdio.h>
+
+#include <string>
 
 #include "zt_common.cuh"
 
@@ -31,19 +38,25 @@ namespace zt {
 
 constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int STAGES = 4;
-constexpr int ASTR = BK + 4;  // complex elems per A row in smem (pad -> conflict-free frags)
-constexpr int BSTR = BN + 2;  // complex elems per B row in smem
-constexpr int A_STAGE = BM * ASTR;  // complex elems
-constexpr int B_STAGE = BK * BSTR;
+// TMA boxes: 128B-wide (8 complex) swizzled rows
+constexpr int A_BOXES = BK / 8;            // A stage = A_BOXES boxes of [BM rows][8 complex]
+constexpr int B_BOXES = BN / 8;            // B stage = B_BOXES boxes of [BK rows][8 complex]
+constexpr int A_BOX_BYTES = BM * 128;
+constexpr int B_BOX_BYTES = BK * 128;
+constexpr int A_STAGE_BYTES = A_BOXES * A_BOX_BYTES;
+constexpr int B_STAGE_BYTES = B_BOXES * B_BOX_BYTES;
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int CONSUMER_WARPS = 8;
 constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
-constexpr int GEMM_SMEM = STAGES * (A_STAGE + B_STAGE) * 16 + 2 * STAGES * 8 + 64;
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024 + 64;
 
 enum { ALGO_3M = 0, ALGO_4M = 1 };
 enum { EPI_STORE = 0, EPI_UPDATE = 1 };
 
 struct GemmArgs {
   int n;
+  CUtensorMap tma_a;  // 2D map of A (and "a" operand) as doubles, box 16 x BM
+  CUtensorMap tma_b;  // 2D map of B, box 16 x BK
   const double* a;  // row-major n x n complex, lda
   int64_t lda;
   const double* b;
@@ -94,6 +107,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -128,11 +154,12 @@ __device__ __forceinline__ void tile_of(int t, bool lower, int T, int& I, int& J
 
 // ---- kernel ---------------------------------------------------------------
 template <int ALGO, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(GemmArgs g) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  double2* As = reinterpret_cast<double2*>(smem);
-  double2* Bs = As + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_STAGE);
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant__ GemmArgs g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128B swizzle needs 1024B-aligned boxes
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
 
@@ -146,7 +173,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(GemmArgs g) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], CONSUMER_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -154,38 +181,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(GemmArgs g) {
   __syncthreads();
 
   if (warp == CONSUMER_WARPS) {
-    // ===== producer warp: cp.async.bulk rows into the ring =====
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      const uint32_t ph = (kt / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      const int k0 = kt * BK;
-      const int kv = min(BK, n - k0);  // valid k in this stage
-      double2* as = As + s * A_STAGE;
-      double2* bs = Bs + s * B_STAGE;
-      // bytes: A rows (valid rows x kv), B rows (kv rows x valid cols)
-      const int mv = min(BM, n - row0), nv = min(BN, n - col0);
-      if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(mv * kv + kv * nv) * 16u);
-      __syncwarp();
-      for (int r = lane; r < BM; r += 32) {
-        double2* dst = as + r * ASTR;
-        if (r < mv) {
-          bulk_g2s(dst, g.a + ((size_t)(row0 + r) * g.lda + k0) * 2, kv * 16, &full[s]);
-          for (int q = kv; q < BK; ++q) dst[q] = make_double2(0.0, 0.0);
-        } else {
-          for (int q = 0; q < BK; ++q) dst[q] = make_double2(0.0, 0.0);
-        }
+    // ===== producer: one thread issues 2D TMA boxes into the ring =====
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_b) : "memory");
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (kt / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int j = 0; j < A_BOXES; ++j)
+          tma_2d(st + j * A_BOX_BYTES, &g.tma_a, 2 * (k0 + 8 * j), row0, &full[s]);
+#pragma unroll
+        for (int q = 0; q < B_BOXES; ++q)
+          tma_2d(st + A_STAGE_BYTES + q * B_BOX_BYTES, &g.tma_b, 2 * (col0 + 8 * q), k0, &full[s]);
       }
-      for (int r = lane; r < BK; r += 32) {
-        double2* dst = bs + r * BSTR;
-        if (r < kv) {
-          bulk_g2s(dst, g.b + ((size_t)(k0 + r) * g.ldb + col0) * 2, nv * 16, &full[s]);
-          for (int q = nv; q < BN; ++q) dst[q] = make_double2(0.0, 0.0);
-        } else {
-          for (int q = 0; q < BN; ++q) dst[q] = make_double2(0.0, 0.0);
-        }
-      }
-      mbar_arrive(&full[s]);
     }
     return;
   }
@@ -202,18 +215,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(GemmArgs g) {
       for (int j = 0; j < 2; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
   const int fr = lane >> 2, fk = lane & 3;
+  // A fragment row r = wm*32 + i*8 + fr (r & 7 == fr); B fragment column
+  // n = wn*16 + j*8 + fr lives in box (wn*2 + j), in-box column fr.
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;
     mbar_wait(&full[s], (kt / STAGES) & 1);
-    const double2* as = As + s * A_STAGE + (wm * 32 + fr) * ASTR + fk;
-    const double2* bs = Bs + s * B_STAGE + fk * BSTR + wn * 16 + fr;
+    const unsigned char* st = smem + s * STAGE_BYTES;
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int jb = ks >> 1, par = ks & 1;
+      const int c = 2 * fk + par;           // 16B chunk inside the 128B row
+      const int kr = 8 * jb + c;            // k row of the B stage
       double2 af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * ASTR + kk * 4];
+      for (int i = 0; i < 4; ++i) {
+        const int r = wm * 32 + i * 8 + fr;
+        af[i] = *reinterpret_cast<const double2*>(st + jb * A_BOX_BYTES + r * 128 + ((c ^ fr) << 4));
+      }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = bs[kk * 4 * BSTR + j * 8];
+      for (int j = 0; j < 2; ++j) {
+        bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * 2 + j) * B_BOX_BYTES +
+                                                   kr * 128 + ((fr ^ (kr & 7)) << 4));
+      }
       if (ALGO == ALGO_3M) {
         double bsum[2];
 #pragma unroll
@@ -360,10 +383,36 @@ __global__ void k_skew_diff(int n, const double* __restrict__ a, double* __restr
   }
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int make_map(CUtensorMap* map, const double* base, int n, int64_t ld, int box_rows) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    ZT_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(ZT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ld < n) return fail(ZT_EINVAL, "zgemm: operand must be 16B aligned with ld >= n");
+  cuuint64_t dims[2] = {(cuuint64_t)2 * n, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 16};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ZT_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return ZT_OK;
+}
+
 static bool g_attr[16][4];
 
 template <int ALGO, int EPI>
-static int launch(const GemmArgs& g, int ntiles, cudaStream_t st) {
+static int launch(GemmArgs& g, int ntiles, cudaStream_t st) {
+  int rc = make_map(&g.tma_a, g.a, g.n, g.lda, BM);
+  if (rc) return rc;
+  rc = make_map(&g.tma_b, g.b, g.n, g.ldb, BK);
+  if (rc) return rc;
   int dev;
   cudaGetDevice(&dev);
   const int slot = ALGO * 2 + EPI;

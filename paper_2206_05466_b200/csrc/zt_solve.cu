@@ -326,25 +326,35 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 3) k_solve_tiles(SolveArgs A
     }
     return;
   }
-  // forward sweep (laplacian.py:280-287) with on-the-fly factors
-  double d = A.d0[(size_t)c * n + m];
+  // factor chain first (independent of the W loads still in flight):
+  // dpttrf order L = e/d, d' = diag - L*e, dinv = 1/d (laplacian.py:208-215)
+  {
+    double d = A.d0[(size_t)c * n + m];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      if (r >= r0 && r <= rl) {
+        const int i = i0 + r;
+        const int k = i - m;
+        const double di = __drcp_rn(d);
+        double L = 0.0;
+        if (k < len - 1) {
+          const double e = __dmul_rn(-A.sqB[i], A.sqB[k]);
+          L = __ddiv_rn(e, d);
+          d = __dsub_rn(block_diag(n, m, k + 1), __dmul_rn(L, e));
+        }
+        sm[r * 32 + lane] = make_double2(L, di);
+      }
+    }
+  }
+  // forward sweep (laplacian.py:280-287)
   double Lprev = A.lin[(size_t)c * n + m];
   double2 y = FINAL ? A.yend[cm] : make_double2(0.0, 0.0);
 #pragma unroll
   for (int r = 0; r < TR; ++r) {
     if (r >= r0 && r <= rl) {
-      const int i = i0 + r;
-      const int k = i - m;
+      const int k = i0 + r - m;
       y = (k == 0) ? v[r] : csub(v[r], rmul(Lprev, y));
-      const double di = __drcp_rn(d);
-      double L = 0.0;
-      if (k < len - 1) {
-        const double e = __dmul_rn(-A.sqB[i], A.sqB[k]);
-        L = __ddiv_rn(e, d);
-        d = __dsub_rn(block_diag(n, m, k + 1), __dmul_rn(L, e));
-      }
-      Lprev = L;
-      sm[r * 32 + lane] = make_double2(L, di);
+      Lprev = sm[r * 32 + lane].x;
       v[r] = y;
     }
   }
@@ -385,7 +395,8 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 3) k_solve_tiles(SolveArgs A
   }
 }
 
-// pass 2: chain the chunk carries, one thread per diagonal
+// pass 2: chain the chunk carries, one thread per diagonal; loads are
+// batched 8 chunks ahead so the serial chain is not latency bound
 __global__ void k_solve_carry(int n, int C, const double* __restrict__ G,
                               const double* __restrict__ H, const double* __restrict__ K,
                               double2* yend, double2* xst) {
@@ -393,22 +404,51 @@ __global__ void k_solve_carry(int n, int C, const double* __restrict__ G,
   if (m < 1 || m >= n) return;
   const size_t base = (size_t)blockIdx.y * C * n;
   const int cs = m / TR;
+  constexpr int PF = 8;
   double2 y = make_double2(0.0, 0.0);
-  for (int c = cs; c < C; ++c) {
-    const size_t o = (size_t)c * n + m;
-    const double2 t = yend[base + o];
-    yend[base + o] = y;
-    const double gg = G[o];
-    y = make_double2(t.x + gg * y.x, t.y + gg * y.y);
+  for (int c0 = cs; c0 < C; c0 += PF) {
+    double2 t[PF];
+    double gg[PF];
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int c = c0 + q;
+      if (c < C) {
+        t[q] = yend[base + (size_t)c * n + m];
+        gg[q] = G[(size_t)c * n + m];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int c = c0 + q;
+      if (c < C) {
+        yend[base + (size_t)c * n + m] = y;
+        y = make_double2(t[q].x + gg[q] * y.x, t[q].y + gg[q] * y.y);
+      }
+    }
   }
   double2 x = make_double2(0.0, 0.0);
-  for (int c = C - 1; c >= cs; --c) {
-    const size_t o = (size_t)c * n + m;
-    const double2 t = xst[base + o];
-    const double2 yi = yend[base + o];
-    xst[base + o] = x;
-    const double hh = H[o], kk = K[o];
-    x = make_double2(t.x + hh * x.x + kk * yi.x, t.y + hh * x.y + kk * yi.y);
+  for (int c0 = C - 1; c0 >= cs; c0 -= PF) {
+    double2 t[PF], yi[PF];
+    double hh[PF], kk[PF];
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int c = c0 - q;
+      if (c >= cs) {
+        const size_t o = (size_t)c * n + m;
+        t[q] = xst[base + o];
+        yi[q] = yend[base + o];
+        hh[q] = H[o];
+        kk[q] = K[o];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int c = c0 - q;
+      if (c >= cs) {
+        xst[base + (size_t)c * n + m] = x;
+        x = make_double2(t[q].x + hh[q] * x.x + kk[q] * yi[q].x, t[q].y + hh[q] * x.y + kk[q] * yi[q].y);
+      }
+    }
   }
 }
 
