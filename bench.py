@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Driver benchmark: isospectral midpoint time-steps/sec at N=2048 (cfg 4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one full isospectral implicit-midpoint step (fixed point to
+tol=1e-12 + final update) of the BASELINE.json cfg-4 workload: N=2048
+complex128, smooth initial vorticity W0 = lap^{-1}(random_admissible(2048,
+default_rng(0), 1/2048)) normalised to unit Frobenius norm, h=0.005.
+
+ours:       device-resident steps through the C ABI (zt_midpoint_step);
+            `value` = steps/s with W resident in HBM; `e2e` = the same through
+            the public Python API with the step's W copied from pinned host
+            memory and the result copied back every step; `roofline` for the
+            dominant kernel (3M DMMA ZGEMM, GEMM-1 a = P X) from CUDA events
+            around every launch in the timed region; `cpu_baseline` = the CPU
+            oracle port on this host's cores (rank 0, N=1 only).
+reference:  the CPU oracle port (restating the reference's numpy/OpenBLAS
+            path; the reference itself is Python and is not on the GPU box)
+            timed on all host cores, same config/metric.
+Multi-GPU (torchrun): each rank runs an independent replica ("replicas");
+`value` = total steps/s over ranks, time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 2048
+H = 0.005
+TOL = 1e-12
+MAX_ITER = 10
+METRIC = "isospectral time-steps/sec at N=2048 complex128"
+WORKLOAD = "cfg4: full isospectral midpoint step on 1 GPU (N=2048, h=0.005, tol=1e-12)"
+REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def cfg4_initial_numpy(n=N, seed=0):
+    """random_admissible (tests/conftest.py:9-14 of the reference) draw."""
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    w = 0.5 * (a - a.conj().T)
+    w -= (np.trace(w) / n) * np.eye(n)
+    return w / n
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (baseline / reference arm)
+# ---------------------------------------------------------------------------
+def oracle_steps(steps, warmup, n=N):
+    """Time the CPU oracle's midpoint step (numpy/OpenBLAS on all host cores)."""
+    from threadpoolctl import threadpool_info, threadpool_limits
+
+    from oracle import zeitlin_oracle as zo
+
+    cores = host_cores()
+    with threadpool_limits(limits=cores):
+        op = zo.build_operator(n)
+        w = zo.solve_stream(cfg4_initial_numpy(n), op)
+        w /= np.linalg.norm(w)
+        times, iters = [], []
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            w, k, _ = zo.midpoint_step(w, H, TOL, MAX_ITER, op=op)
+            dt = time.perf_counter() - t0
+            if s >= warmup:
+                times.append(dt)
+                iters.append(k)
+        blas = [f"{d.get('internal_api')} {d.get('version')} x{d.get('num_threads')}" for d in threadpool_info()]
+    return times, iters, cores, blas
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, iters, cores, blas = oracle_steps(args.steps, args.warmup)
+    total = sum(times)
+    value = len(times) / total
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N": N, "h": H, "iterations_per_step": iters},
+        "cpu_baseline": {
+            "value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} full cfg-4 steps at N=2048 (after {args.warmup} warm-up); "
+                      f"oracle/zeitlin_oracle.py restating integrator.py:96-171 + laplacian.py:272-316; "
+                      f"BLAS: {'; '.join(blas)}; sweeps are numpy row loops",
+        },
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.samples = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:  # pragma: no cover
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [v for k, v in REASONS.items() if mask & k and k != 0x1], "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def load_fp64_peak():
+    """Measured DMMA peak (profiles/r01_fp64_peaks.jsonl, our microbenchmark);
+    MEASURED_PEAKS.json carries no FP64 figure."""
+    path = os.path.join(ROOT, "profiles", "r01_fp64_peaks.jsonl")
+    best = None
+    try:
+        for line in open(path):
+            d = json.loads(line)
+            if str(d.get("bench", "")).startswith("dmma"):
+                best = max(best or 0.0, d["tflops"])
+    except OSError:
+        pass
+    return best or 37.2, ("measured: DMMA.8x8x4 issue-rate microbenchmark, profiles/r01_fp64_peaks.jsonl"
+                          if best else "nominal 148 SM x 128 flop/clk x 1.965 GHz")
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2206_05466_b200 as zt
+    from paper_2206_05466_b200 import _lib
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+
+    lib = _lib.lib
+    op = zt.build_operator(N, dev)
+    r = torch.from_numpy(cfg4_initial_numpy()).to(dev)
+    w0 = zt.solve_stream(r, op)
+    w0 = w0 / torch.linalg.norm(w0)
+    x = w0.clone()
+    out = torch.empty_like(x)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    iters = []
+    for _ in range(args.warmup):
+        y, k, _, _ = midpoint_step_raw(x, H, TOL, MAX_ITER, op, out=out)
+        x, out = y, x
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = lib.zt_launch_count()
+    lib.zt_profile_read(None, None, 1)
+    lib.zt_profile_enable(1)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            y, k, _, _ = midpoint_step_raw(x, H, TOL, MAX_ITER, op, out=out)
+            x, out = y, x
+            iters.append(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    lib.zt_profile_enable(0)
+    launches = lib.zt_launch_count() - launches0
+    import ctypes
+
+    pms = (ctypes.c_double * 3)()
+    pcnt = (ctypes.c_int64 * 3)()
+    lib.zt_profile_read(ctypes.cast(pms, ctypes.c_void_p), ctypes.cast(pcnt, ctypes.c_void_p), 1)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API, host buffers every step ----
+    host_in = torch.empty((N, N), dtype=torch.complex128, pin_memory=True)
+    host_in.copy_(w0.cpu())
+    host_out = torch.empty_like(host_in).pin_memory()
+    st = zt.StepperState(w=None, h=H, tol=TOL, max_iter=MAX_ITER)
+    e2e_steps = max(1, min(args.steps, 10))
+    torch.cuda.synchronize()
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        wdev = host_in.to(dev, non_blocking=True)
+        st.w = wdev
+        st, _info = zt.midpoint_step_info(st)
+        host_out.copy_(st.w, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        host_in, host_out = host_out, host_in
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ems = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([ems], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = world * e2e_steps / (ems / 1e3)
+
+    # ---- roofline of the dominant kernel (GEMM-1: a = P X, 3M DMMA) ----
+    peak, peak_src = load_fp64_peak()
+    g1_ms = pms[1] / max(1, pcnt[1])
+    g2_ms = pms[2] / max(1, pcnt[2])
+    sv_ms = pms[0] / max(1, pcnt[0])
+    alg = 8.0 * N**3
+    achieved = alg / (g1_ms * 1e-3) / 1e12
+    roofline = {
+        "bound": "tensor", "kernel": "k_zgemm<3M,STORE> (GEMM-1 a = P X)",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "traffic": TRAFFIC_GEMM1,
+        "peak_source": peak_src,
+        "algorithmic_flop_per_launch": alg,
+        "executed_dmma_flop_per_launch": 6.0 * N**3,
+        "executed_frac": (6.0 * N**3) / (g1_ms * 1e-3) / 1e12 / peak,
+        "avg_launch_ms": g1_ms,
+        "note": "3M (Gauss) complex product: 6N^3 DMMA flop executed for the 8N^3 algorithmic flop, "
+                "so achieved/peak may exceed 1",
+        "gemm2_avg_ms": g2_ms, "gemm2_alg_flop": alg,
+        "solve_avg_ms": sv_ms, "solve_alg_bytes": 24.0 * N * N,
+        "solve_GBps_alg": 24.0 * N * N / (sv_ms * 1e-3) / 1e9 if sv_ms > 0 else None,
+        "step_share": {"gemm1": pms[1] / ms, "gemm2": pms[2] / ms, "solve": pms[0] / ms},
+        "step_alg_flop": 16.0 * N**3 * (statistics.mean(iters) + 1),
+        "step_TFLOPs_alg": 16.0 * N**3 * (statistics.mean(iters) + 1) / (ms_per_step * 1e-3) / 1e12,
+    }
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": WORKLOAD, "N": N, "h": H, "tol": TOL, "max_iter": MAX_ITER,
+            "init": "W0 = lap^-1(random_admissible(2048, default_rng(0), 1/2048)) / ||.||_F",
+            "iterations_per_step": sorted(set(iters)),
+            "parallelism": "replicas" if world > 1 else "single",
+            "gemm": "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages",
+            "l2": "no flush: per-step working set W_n, W~, P, a = 256 MB > 126 MB L2",
+        },
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 16 * N * N,
+                "d2h_bytes_per_step": 16 * N * N, "steps": e2e_steps,
+                "api": "paper_2206_05466_b200.midpoint_step_info(StepperState(w=cuda tensor)) "
+                       "with pinned-host W copied in and out each step"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, citers, cores, blas = oracle_steps(args.cpu_steps, 1)
+        line["cpu_baseline"] = {
+            "value": len(times) / sum(times), "unit": "steps/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} full cfg-4 steps at N=2048 after 1 warm-up "
+                      f"(iterations {citers}); oracle/zeitlin_oracle.py numpy/OpenBLAS; "
+                      f"BLAS: {'; '.join(blas)}",
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum per GEMM-1 launch at N=2048 from
+# the committed `ncu --set full` capture (profiles/r01_ncu_summary.md); None
+# until captured for the current kernel.
+TRAFFIC_GEMM1 = 367.78e6  # 314.66 MB read + 53.13 MB write (profiles/r01_ncu_summary.md)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

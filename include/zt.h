@@ -119,6 +119,13 @@ int zt_commutator(int n, const double* p, const double* w, double* c, double* wo
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work,
                 void* stream);
 
+/* Per-kernel device timing for the roofline report: when enabled, CUDA
+ * events bracket the stream solve, GEMM-1 (a = P X) and GEMM-2 (update) of
+ * every update inside zt_midpoint_step; zt_profile_read returns the summed
+ * milliseconds and launch counts [solve, gemm1, gemm2]. */
+int zt_profile_enable(int on);
+int zt_profile_read(double* ms3, int64_t* counts3, int reset);
+
 /* Number of kernels this library launched since load (device-side work
  * evidence for the bench's gpu_launches claim). */
 int64_t zt_launch_count(void);

@@ -93,16 +93,61 @@ static double bits_to_double(unsigned long long b) {
   return d;
 }
 
+// ---- optional per-kernel device timing (bench.py roofline) -----------------
+// When enabled, events bracket the solve / GEMM-1 / GEMM-2 of every update on
+// the launching stream; durations are accumulated after the call's syncs.
+static bool g_prof = false;
+struct ProfSlot {
+  cudaEvent_t ev[4];
+};
+static std::vector<ProfSlot> g_slots;
+static size_t g_used = 0;
+static double g_prof_ms[3] = {0, 0, 0};
+static int64_t g_prof_cnt[3] = {0, 0, 0};
+
+static void prof_mark(int which, cudaStream_t st) {
+  if (!g_prof) return;
+  if (which == 0) {
+    if (g_used == g_slots.size()) {
+      ProfSlot s;
+      for (auto& e : s.ev) cudaEventCreate(&e);
+      g_slots.push_back(s);
+    }
+    ++g_used;
+  }
+  cudaEventRecord(g_slots[g_used - 1].ev[which], st);
+}
+
+static void prof_collect() {
+  if (!g_prof) return;
+  for (size_t i = 0; i < g_used; ++i) {
+    cudaEventSynchronize(g_slots[i].ev[3]);
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, g_slots[i].ev[k], g_slots[i].ev[k + 1]) == cudaSuccess) {
+        g_prof_ms[k] += ms;
+        g_prof_cnt[k] += 1;
+      }
+    }
+  }
+  g_used = 0;
+}
+
 // One update: P = lap^-1 X; a = P X; out = base + hh (a - a^H) + qq a P.
 static int update(zt_operator* op, const double* x, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, StepWS& w,
                   unsigned long long* resid, unsigned long long* cons, cudaStream_t st) {
   const int n = op->n;
+  prof_mark(0, st);
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
+  prof_mark(1, st);
   rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
   if (rc) return rc;
-  return zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, g_algo, st);
+  prof_mark(2, st);
+  rc = zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, g_algo, st);
+  prof_mark(3, st);
+  return rc;
 }
 
 static int fixed_point_impl(zt_operator* op, const double* wn, double* x, double h, double tol,
@@ -177,6 +222,24 @@ const char* zt_strerror(int s) {
 const char* zt_last_error(void) { return t_err.c_str(); }
 
 int64_t zt_launch_count(void) { return g_launches.load(); }
+
+int zt_profile_enable(int on) {
+  g_prof = on != 0;
+  g_used = 0;
+  return ZT_OK;
+}
+
+int zt_profile_read(double* ms, int64_t* counts, int reset) {
+  for (int k = 0; k < 3; ++k) {
+    if (ms) ms[k] = g_prof_ms[k];
+    if (counts) counts[k] = g_prof_cnt[k];
+    if (reset) {
+      g_prof_ms[k] = 0;
+      g_prof_cnt[k] = 0;
+    }
+  }
+  return ZT_OK;
+}
 
 int zt_op_create(int n, int device, zt_op_t* op) {
   if (!op) return fail(ZT_EINVAL, "null output");
@@ -268,6 +331,7 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
   rc = update(op, w_next, w_next, nullptr, consistency ? wn : nullptr, w_next, hh, -q, w, nullptr,
               consistency ? w.flags + 1 : nullptr, st);
   if (rc) return rc;
+  prof_collect();
   if (consistency) {
     ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h + 4, w.flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     ZT_CUDA_CHECK(cudaStreamSynchronize(st));

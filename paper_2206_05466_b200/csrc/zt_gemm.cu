@@ -50,7 +50,7 @@ constexpr int CONSUMER_WARPS = 8;
 constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024 + 64;
 
-enum { ALGO_3M = 0, ALGO_4M = 1 };
+enum { ALGO_3M = 0, ALGO_4M = 1, ALGO_3M_NOSUM = 2 /* timing experiment only: wrong results */ };
 enum { EPI_STORE = 0, EPI_UPDATE = 1 };
 
 struct GemmArgs {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
 
   // ===== consumer warps: 2 (M) x 4 (N), warp tile 32 x 16 complex =====
   const int wm = warp >> 2, wn = warp & 3;
-  constexpr int NACC = (ALGO == ALGO_3M) ? 3 : 2;
+  constexpr int NACC = (ALGO != ALGO_4M) ? 3 : 2;
   double acc[NACC][4][2][2];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
@@ -237,13 +237,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
         bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * 2 + j) * B_BOX_BYTES +
                                                    kr * 128 + ((fr ^ (kr & 7)) << 4));
       }
-      if (ALGO == ALGO_3M) {
+      if (ALGO != ALGO_4M) {
         double bsum[2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) bsum[j] = bf[j].x + bf[j].y;
+        for (int j = 0; j < 2; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const double asum = af[i].x + af[i].y;
+          const double asum = (ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         double cr, ci;
-        if (ALGO == ALGO_3M) {
+        if (ALGO != ALGO_4M) {
           cr = acc[0][i][j][e] - acc[1][i][j][e];
           ci = acc[2][i][j][e] - acc[0][i][j][e] - acc[1][i][j][e];
         } else {
@@ -405,7 +405,7 @@ static int make_map(CUtensorMap* map, const double* base, int n, int64_t ld, int
   return ZT_OK;
 }
 
-static bool g_attr[16][4];
+static bool g_attr[16][8];
 
 template <int ALGO, int EPI>
 static int launch(GemmArgs& g, int ntiles, cudaStream_t st) {
@@ -439,6 +439,7 @@ int zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, dou
   g.ldc = ldc;
   const int T = (n + BM - 1) / BM;
   if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, T * T, st);
+  if (algo == ALGO_3M_NOSUM) return launch<ALGO_3M_NOSUM, EPI_STORE>(g, T * T, st);
   return launch<ALGO_3M, EPI_STORE>(g, T * T, st);
 }
 
