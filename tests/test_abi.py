@@ -54,7 +54,7 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in sass  # FP64 tensor-pipe MMA in the GEMM
-    assert "UBLKCP" in sass  # cp.async.bulk (TMA engine) operand staging
+    assert "UTMALDG" in sass  # 2D TMA (cp.async.bulk.tensor) operand staging
 
 
 def test_no_cpu_fallback_in_product_path():
