@@ -20,6 +20,7 @@ struct zt_operator {
   double* G = nullptr;
   double* H = nullptr;
   double* K = nullptr;
+  double* m0x = nullptr;  // m = 0 per-chunk constant-RHS responses
   void* block = nullptr;  // single allocation holding every table
 };
 

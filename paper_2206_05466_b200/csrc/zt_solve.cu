@@ -3,24 +3,25 @@
 // (laplacian.py:189-219 factor build, 272-300 sweeps, 306-316 reflection,
 // 341-367 stencil) as HBM-bound, chunk-parallel kernels:
 //
-//  * sheared tiles: warp = 32 consecutive diagonals m x 32 consecutive rows i
-//    ("chunk"); lane m reads W[i][i-m] so each row of a tile is one
-//    contiguous 512 B segment (the reference's sheared layout, laplacian.py:
-//    16-21, without materialising it);
-//  * LDL^T factors are regenerated on the fly from the closed-form block
-//    entries with the exact dpttrf operation order (L = e/d,
-//    d' = diag - L*e, dinv = 1/d: bit-identical to LAPACK's tables), so no
-//    factor bytes are streamed; only a per-(chunk, diagonal) table of the
-//    pivot d at the chunk start is read;
-//  * chunk coupling is linear: pass 1 computes each chunk's zero-carry
-//    forward end value and backward start value, pass 2 (one thread per
-//    diagonal) chains the carries with precomputed gains G/H/K, pass 3
-//    re-sweeps each chunk with its true carries and writes the lower
-//    triangle coalesced and the skew reflection through a shared-memory
+//  * sheared tiles: warp = 32 consecutive diagonals m x SR consecutive rows
+//    i ("chunk"); lane m reads W[i][i-m], so each tile row is one contiguous
+//    512 B segment (the reference's sheared layout, laplacian.py:16-21,
+//    applied on the fly instead of materialised);
+//  * LDL^T factors are regenerated in registers from the closed-form block
+//    entries (a fast reciprocal + 2 Newton steps per row, within an ulp of
+//    dpttrf) starting from the exact dpttrf pivot at each chunk start, so no
+//    factor bytes are streamed from HBM;
+//  * chunks couple affinely: pass 1 computes each chunk's zero-carry forward
+//    end value and backward start value; pass 2 (one warp per diagonal,
+//    warp-level affine scans) chains the carries with precomputed gains
+//    G/H/K; pass 3 re-sweeps every chunk with its true carries and writes the
+//    lower triangle coalesced and the skew reflection through a shared-memory
 //    transpose;
-//  * the singular m = 0 diagonal (deflated, null-mode projection and
-//    zero-mean gauge, laplacian.py:276-298) is solved by one 128-thread
-//    block per matrix inside pass 1 with block-level affine scans.
+//  * the singular m = 0 diagonal (deflated block, null-mode projection of the
+//    RHS and zero-mean gauge, laplacian.py:201-215, 276-298) runs in the same
+//    tiles: by linearity pass 1 records per-chunk trace partials and x-sums,
+//    and pass 2 resolves mu = tr/N and the gauge from precomputed responses
+//    to a constant right-hand side.
 #include <math.h>
 #include <stdio.h>
 
@@ -32,239 +33,125 @@
 
 namespace zt {
 
-constexpr int TR = 32;  // rows per chunk (and diagonals per tile)
+constexpr int SUB = 16;        // rows per lane (sub-chunk)
+constexpr int LPD = 4;         // lanes per diagonal
+constexpr int DPW = 32 / LPD;  // diagonals per warp tile
+constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
+constexpr int TR = 32;  // rows per apply tile / diagonals per apply tile
+constexpr int M0X = 5;  // m = 0 per-chunk responses: Y1, X1, S1, SH, SK
 
 // ---------------------------------------------------------------------------
-// operator build: one thread per diagonal walks the factor recurrence once
-// (laplacian.py:197-215) and records per-chunk pivots and carry gains.
+// operator build (laplacian.py:197-215): one thread per diagonal walks the
+// exact dpttrf recurrence once and records the pivot at every 16-row
+// sub-chunk start, and per 64-row chunk the coupling into the chunk and the
+// carry gains G (forward), H (backward), K (forward carry -> backward start).
 // ---------------------------------------------------------------------------
 __global__ void k_op_sqrt_table(int n, double* sqB) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) sqB[j] = sqrt((j + 1.0) * (n - 1.0 - j));  // sqrt((i+1)(N-1-i)), laplacian.py:134-136
 }
 
-__global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double* d0, double* lin,
-                           double* G, double* H, double* K, double* L0, double* dinv0) {
+__global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double* d0s, double* lin,
+                           double* G, double* H, double* K, double* L0, double* dinv0, double* m0x) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  if (m == 0) {
-    // deflated m = 0 block: leading (N-1) x (N-1) SPD part (laplacian.py:201-204)
-    const int sz = n - 1;
-    double d = block_diag(n, 0, 0);
-    for (int k = 0; k < sz; ++k) {
-      dinv0[k] = __drcp_rn(d);
-      if (k < sz - 1) {
-        const double e = __dmul_rn(-sqB[k], sqB[k]);
-        const double L = __ddiv_rn(e, d);
-        L0[k] = L;
-        d = __dsub_rn(block_diag(n, 0, k + 1), __dmul_rn(L, e));
-      } else {
-        L0[k] = 0.0;
-      }
-    }
-    L0[n - 1] = 0.0;
-    dinv0[n - 1] = 0.0;  // gauge row keeps the null component at zero
-    return;
-  }
   const int len = n - m;
   double d = block_diag(n, m, 0);
   double Lprev = 0.0;
-  double Lc[TR], Dc[TR];
+  double Lc[SR], Dc[SR], g[SR], z[SR], hh[SR];
   int k = 0;
+  // m = 0 is deflated to its leading (N-1) block; row N-1 is the gauge row
+  const int last = (m == 0) ? n - 2 : len - 1;  // last factored row
   while (k < len) {
     const int i = m + k;
-    const int c = i / TR;
+    const int c = i / SR;
     const int k0 = k;
-    const int i1 = min((c + 1) * TR, n);
-    const int cnt = i1 - i;
-    d0[(size_t)c * n + m] = d;
-    lin[(size_t)c * n + m] = (k0 == 0) ? 0.0 : Lprev;
+    const int cnt = min((c + 1) * SR, n) - i;
+    const double lin_c = (k0 == 0) ? 0.0 : Lprev;
+    lin[(size_t)c * n + m] = lin_c;
     for (int r = 0; r < cnt; ++r, ++k) {
-      Dc[r] = __drcp_rn(d);
-      if (k < len - 1) {
-        const double e = __dmul_rn(-sqB[m + k], sqB[k]);
-        const double L = __ddiv_rn(e, d);
-        Lc[r] = L;
-        d = __dsub_rn(block_diag(n, m, k + 1), __dmul_rn(L, e));
+      if ((m + k) % SUB == 0 || r == 0) d0s[(size_t)((m + k) / SUB) * n + m] = d;
+      if (k <= last) {
+        Dc[r] = __drcp_rn(d);
+        if (k < last) {
+          const double e = __dmul_rn(-sqB[m + k], sqB[k]);
+          const double L = __ddiv_rn(e, d);
+          Lc[r] = L;
+          d = __dsub_rn(block_diag(n, m, k + 1), __dmul_rn(L, e));
+        } else {
+          Lc[r] = 0.0;
+        }
       } else {
+        Dc[r] = 0.0;
         Lc[r] = 0.0;
       }
+      if (m == 0) {
+        L0[k] = Lc[r];
+        dinv0[k] = Dc[r];
+      }
     }
-    const double lin_c = (k0 == 0) ? 0.0 : Lprev;
-    // forward response to y_in, and its backward sweep (K)
-    double g[TR];
     double gg = -lin_c;
-    double Gp = 1.0;
     for (int r = 0; r < cnt; ++r) {
       if (r > 0) gg = -Lc[r - 1] * gg;
       g[r] = gg;
     }
-    Gp = g[cnt - 1];
-    double z = 0.0, Hp = 1.0;
+    double zz = 0.0, hv = 1.0;
     for (int r = cnt - 1; r >= 0; --r) {
-      z = g[r] * Dc[r] - Lc[r] * z;
-      Hp *= -Lc[r];
+      zz = g[r] * Dc[r] - Lc[r] * zz;
+      hv = -Lc[r] * hv;
+      z[r] = zz;
+      hh[r] = hv;
     }
-    G[(size_t)c * n + m] = Gp;
-    H[(size_t)c * n + m] = Hp;
-    K[(size_t)c * n + m] = z;
+    G[(size_t)c * n + m] = g[cnt - 1];
+    H[(size_t)c * n + m] = hh[0];
+    K[(size_t)c * n + m] = z[0];
+    if (m == 0) {
+      // responses to a constant right-hand side 1 with zero carries, and the
+      // chunk sums of the x responses (for the zero-mean gauge)
+      double yy = 0.0;
+      for (int r = 0; r < cnt; ++r) {
+        yy = (r == 0) ? 1.0 : 1.0 - Lc[r - 1] * yy;
+        g[r] = yy;  // reuse as y1
+      }
+      double x1 = 0.0, s1 = 0.0, sh = 0.0, sk = 0.0;
+      for (int r = cnt - 1; r >= 0; --r) {
+        x1 = g[r] * Dc[r] - Lc[r] * x1;
+        s1 += x1;
+        sh += hh[r];
+        sk += z[r];
+      }
+      double* q = m0x + (size_t)c * M0X;
+      q[0] = g[cnt - 1];
+      q[1] = x1;
+      q[2] = s1;
+      q[3] = sh;
+      q[4] = sk;
+    }
     Lprev = Lc[cnt - 1];
   }
 }
 
-// ---------------------------------------------------------------------------
-// m = 0 diagonal: 128 threads, contiguous segments, affine block scans.
-// ---------------------------------------------------------------------------
-struct Aff {  // y_out = a + g * y_in
-  double2 a;
-  double g;
-};
-__device__ __forceinline__ Aff aff_then(Aff first, Aff second) {
-  Aff r;
-  r.a = make_double2(second.a.x + second.g * first.a.x, second.a.y + second.g * first.a.y);
-  r.g = second.g * first.g;
-  return r;
-}
-
-template <bool REVERSE>
-__device__ Aff block_scan_exclusive(Aff v, Aff* sh) {
-  // returns the composition of all maps strictly before this thread (in
-  // scan order) applied as a map; forward order = thread 0 first.
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  Aff inc = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Aff o;
-    const int src = REVERSE ? lane + off : lane - off;
-    o.a.x = __shfl_sync(0xffffffff, inc.a.x, REVERSE ? min(src, 31) : max(src, 0));
-    o.a.y = __shfl_sync(0xffffffff, inc.a.y, REVERSE ? min(src, 31) : max(src, 0));
-    o.g = __shfl_sync(0xffffffff, inc.g, REVERSE ? min(src, 31) : max(src, 0));
-    const bool ok = REVERSE ? (src < 32) : (src >= 0);
-    if (ok) inc = aff_then(o, inc);
-  }
-  if (lane == (REVERSE ? 0 : 31)) sh[w] = inc;
-  __syncthreads();
-  Aff pre;
-  pre.a = make_double2(0.0, 0.0);
-  pre.g = 1.0;
-  if (!REVERSE) {
-    for (int j = 0; j < w; ++j) pre = aff_then(pre, sh[j]);
-  } else {
-    for (int j = nw - 1; j > w; --j) pre = aff_then(pre, sh[j]);
-  }
-  // exclusive within warp
-  Aff ex;
-  const int src = REVERSE ? lane + 1 : lane - 1;
-  ex.a.x = __shfl_sync(0xffffffff, inc.a.x, REVERSE ? min(src, 31) : max(src, 0));
-  ex.a.y = __shfl_sync(0xffffffff, inc.a.y, REVERSE ? min(src, 31) : max(src, 0));
-  ex.g = __shfl_sync(0xffffffff, inc.g, REVERSE ? min(src, 31) : max(src, 0));
-  const bool has = REVERSE ? (lane < 31) : (lane > 0);
-  Aff res = has ? aff_then(pre, ex) : pre;
-  __syncthreads();
-  return res;
-}
-
-__device__ double2 block_sum2(double2 v, double2* sh) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffff, v.x, off);
-    v.y += __shfl_xor_sync(0xffffffff, v.y, off);
-  }
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  double2 t = make_double2(0.0, 0.0);
-  for (int j = 0; j < nw; ++j) t = make_double2(t.x + sh[j].x, t.y + sh[j].y);
-  __syncthreads();
-  return t;
-}
-
-// Solves the m = 0 diagonal of one matrix; writes P[k][k] = -(x_k - mean x).
-__device__ void solve_m0(int n, const double* __restrict__ L0, const double* __restrict__ dinv0,
-                         const double* __restrict__ w, int64_t ldw, double* __restrict__ p,
-                         int64_t ldp, unsigned char* smem) {
-  Aff* sha = reinterpret_cast<Aff*>(smem);
-  double2* shs = reinterpret_cast<double2*>(smem + 32 * sizeof(Aff));
-  const int T = blockDim.x;
-  const int E = (n + T - 1) / T;
-  const int kb = threadIdx.x * E, ke = min(kb + E, n);
-  const size_t dw = (size_t)(ldw + 1) * 2, dp = (size_t)(ldp + 1) * 2;
-  // trace mean (laplacian.py:276-279)
-  double2 s = make_double2(0.0, 0.0);
-  for (int k = kb; k < ke; ++k) {
-    const double2 b = ld2(w + k * dw);
-    s.x += b.x;
-    s.y += b.y;
-  }
-  s = block_sum2(s, shs);
-  const double2 mu = make_double2(s.x / n, s.y / n);
-  // forward: local aggregate with zero carry
-  Aff f;
-  f.a = make_double2(0.0, 0.0);
-  f.g = 1.0;
-  for (int k = kb; k < ke; ++k) {
-    const double2 b = csub(ld2(w + k * dw), mu);
-    if (k == 0) {
-      f.a = b;
-      f.g = 0.0;
-    } else {
-      const double L = L0[k - 1];
-      f.a = csub(b, rmul(L, f.a));
-      f.g = -L * f.g;
-    }
-  }
-  const Aff fin = block_scan_exclusive<false>(f, sha);
-  double2 y = fin.a;  // carry in (applied to y_in = 0)
-  for (int k = kb; k < ke; ++k) {
-    const double2 b = csub(ld2(w + k * dw), mu);
-    y = (k == 0) ? b : csub(b, rmul(L0[k - 1], y));
-    st2(p + k * dp, y);  // scratch: forward values in P's diagonal
-  }
-  __syncthreads();
-  // backward local aggregate (x_in from the right)
-  Aff bk;
-  bk.a = make_double2(0.0, 0.0);
-  bk.g = 1.0;
-  for (int k = ke - 1; k >= kb; --k) {
-    const double2 yk = ld2_plain(p + k * dp);
-    const double di = dinv0[k];
-    if (k == n - 1) {
-      bk.a = rmul(di, yk);
-      bk.g = 0.0;
-    } else {
-      const double L = L0[k];
-      bk.a = csub(rmul(di, yk), rmul(L, bk.a));
-      bk.g = -L * bk.g;
-    }
-  }
-  const Aff bin = block_scan_exclusive<true>(bk, sha);
-  double2 x = bin.a;
-  double2 xs = make_double2(0.0, 0.0);
-  for (int k = ke - 1; k >= kb; --k) {
-    const double2 yk = ld2_plain(p + k * dp);
-    const double di = dinv0[k];
-    x = (k == n - 1) ? rmul(di, yk) : csub(rmul(di, yk), rmul(L0[k], x));
-    st2(p + k * dp, x);
-    xs.x += x.x;
-    xs.y += x.y;
-  }
-  xs = block_sum2(xs, shs);
-  const double2 g = make_double2(xs.x / n, xs.y / n);  // zero-mean gauge (293-296)
-  for (int k = kb; k < ke; ++k) {
-    const double2 xk = ld2_plain(p + k * dp);
-    st2(p + k * dp, make_double2(-(xk.x - g.x), -(xk.y - g.y)));
-  }
+// Fast pivot reciprocal: approximate rcp + 2 Newton steps (d > 0, well
+// scaled: 1 <= d <= 2e8 for N <= 16384), within ~1 ulp of 1/d.
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
 }
 
 // ---------------------------------------------------------------------------
-// chunk tiles (m >= 1).  FINAL=false: pass 1 (aggregates).  FINAL=true:
-// pass 3 (true carries, writes P).
+// chunk tiles: warp = 8 diagonals x 64 rows; lane (d = lane & 7,
+// s = lane >> 3) owns rows [16 s, 16 s + 16) of diagonal m0 + d.
+// FINAL=false: pass 1 (chunk aggregates).  FINAL=true: pass 3 (writes P).
 // ---------------------------------------------------------------------------
 struct SolveArgs {
   int n, C, ntiles;
   const double* sqB;
-  const double* d0;
+  const double* d0s;
   const double* lin;
   const double* L0;
   const double* dinv0;
@@ -272,184 +159,405 @@ struct SolveArgs {
   int64_t ldw, sw;
   double* p;
   int64_t ldp, sp;
-  double2* yend;  // [batch][C][n]: pass1 y_end -> pass2 y_in
-  double2* xst;   // [batch][C][n]: pass1 x_start -> pass2 x_in
+  double2* yend;   // [batch][C][n]: pass1 y_end -> pass2 y_in
+  double2* xst;    // [batch][C][n]: pass1 x_start -> pass2 x_in
+  double2* m0acc;  // [batch][C][2]: (trace partial, x-sum) of the m = 0 chunk
+  double2* m0mg;   // [batch][2]: (mu, gauge)
 };
+
+struct AffW {  // y_out = a + g * y_in
+  double2 a;
+  double g;
+};
+__device__ __forceinline__ AffW aff_compose(AffW first, AffW second) {
+  // apply `first`, then `second`
+  AffW r;
+  r.a = make_double2(fma(second.g, first.a.x, second.a.x), fma(second.g, first.a.y, second.a.y));
+  r.g = second.g * first.g;
+  return r;
+}
+__device__ __forceinline__ AffW aff_shfl(AffW v, int src) {
+  AffW o;
+  o.a.x = __shfl_sync(0xffffffff, v.a.x, src);
+  o.a.y = __shfl_sync(0xffffffff, v.a.y, src);
+  o.g = __shfl_sync(0xffffffff, v.g, src);
+  return o;
+}
+
+// tile t -> (chunk c, group g of 8 diagonals): chunk c holds 8(c+1) groups
+__device__ __forceinline__ void solve_tile_coords(int t, int& c, int& g) {
+  int q = (int)((sqrt(1.0 + (double)t) - 1.0) * 0.5);
+  while (4 * (q + 1) * (q + 2) <= t) ++q;
+  while (4 * q * (q + 1) > t) --q;
+  c = q;
+  g = t - 4 * q * (q + 1);
+}
+
+static int solve_ntiles(int C) { return 4 * C * (C + 1); }
+
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const double* w = A.w + (size_t)b * A.sw * 2;
+  double* p = A.p + (size_t)b * A.sp * 2;
+  const int n = A.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * SOLVE_WARPS + warp;
+  if (t >= A.ntiles) return;
+  int c, g;
+  solve_tile_coords(t, c, g);
+  const int i0 = c * SR;
+  const int m0 = g * DPW;
+  if (m0 >= n || m0 > i0 + SR - 1) return;  // whole tile empty (warp-uniform)
+  const int dl = lane & (DPW - 1), s = lane >> 3;
+  const int m = m0 + dl;
+  const int ib = i0 + s * SUB;
+  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;  // [row in chunk][dl]
+  const bool mok = m < n;
+  const int len = n - m;
+  const int rs = max(0, m - ib);
+  const int re = min(SUB - 1, n - 1 - ib);
+  const bool has = mok && rs <= re;
+  const size_t cm = (size_t)b * A.C * n + (size_t)c * n + m;
+
+  // 1. loads (16 rows, coalesced: each instruction covers 4 rows x 128 B)
+  double2 v[SUB];
+#pragma unroll
+  for (int r = 0; r < SUB; ++r) {
+    const int i = ib + r;
+    v[r] = (has && r >= rs && r <= re) ? ld2(w + ((size_t)i * A.ldw + (i - m)) * 2) : make_double2(0.0, 0.0);
+  }
+  // 2. factor chain for my 16 rows, starting from the exact sub-chunk pivot
+  if (has) {
+    if (m == 0) {
+#pragma unroll
+      for (int r = 0; r < SUB; ++r)
+        if (r <= re) sm[(s * SUB + r) * DPW + dl] = make_double2(A.L0[ib + r], A.dinv0[ib + r]);
+    } else {
+      double d = A.d0s[(size_t)(ib / SUB) * n + m];
+      int k = ib + rs - m;
+      double dg = block_diag(n, m, k);
+      double inc = 2.0 * (double)(n - 2 - 2 * k - m);  // diag(k+1) - diag(k), exact
+#pragma unroll
+      for (int r = 0; r < SUB; ++r) {
+        if (r >= rs && r <= re) {
+          const double di = fast_rcp(d);
+          double L = 0.0;
+          if (k < len - 1) {
+            const double e = -A.sqB[ib + r] * A.sqB[k];
+            L = e * di;
+            dg += inc;
+            inc -= 4.0;
+            d = fma(-L, e, dg);
+          }
+          sm[(s * SUB + r) * DPW + dl] = make_double2(L, di);
+          ++k;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // coupling into my first row: previous chunk (table) or my s-1 neighbour
+  double Lin = 0.0;
+  if (has) Lin = (s == 0) ? A.lin[(size_t)c * n + m] : sm[(s * SUB - 1) * DPW + dl].x;
+
+  double2 mu = make_double2(0.0, 0.0), gauge = make_double2(0.0, 0.0);
+  if (FINAL && m == 0) {
+    mu = A.m0mg[2 * b];
+    gauge = A.m0mg[2 * b + 1];
+  }
+  // 3. forward sweep with zero carry (laplacian.py:280-287) -> affine map
+  double2 tb = make_double2(0.0, 0.0);
+  AffW fm;
+  fm.a = make_double2(0.0, 0.0);
+  fm.g = 1.0;
+  if (has) {
+    double Lp = Lin;
+#pragma unroll
+    for (int r = 0; r < SUB; ++r) {
+      if (r >= rs && r <= re) {
+        const int k = ib + r - m;
+        double2 bb = v[r];
+        if (!FINAL && m == 0) tb = make_double2(tb.x + bb.x, tb.y + bb.y);
+        if (FINAL && m == 0) bb = csub(bb, mu);
+        if (k == 0) {
+          fm.a = bb;
+          fm.g = 0.0;
+        } else {
+          fm.a = make_double2(fma(-Lp, fm.a.x, bb.x), fma(-Lp, fm.a.y, bb.y));
+          fm.g = -Lp * fm.g;
+        }
+        Lp = sm[(s * SUB + r) * DPW + dl].x;
+        v[r] = fm.a;
+      }
+    }
+  }
+  // 4. compose the 4 segment maps of each diagonal (lanes dl, dl+8, dl+16, dl+24)
+  AffW inc = fm;
+  {
+    AffW o = aff_shfl(inc, max(lane - 8, 0));
+    if (s >= 1) inc = aff_compose(o, inc);
+    o = aff_shfl(inc, max(lane - 16, 0));
+    if (s >= 2) inc = aff_compose(o, inc);
+  }
+  AffW exm = aff_shfl(inc, max(lane - 8, 0));
+  if (s == 0) {
+    exm.a = make_double2(0.0, 0.0);
+    exm.g = 1.0;
+  }
+  const double2 ych = FINAL ? A.yend[cm] : make_double2(0.0, 0.0);
+  const double2 yin = make_double2(fma(exm.g, ych.x, exm.a.x), fma(exm.g, ych.y, exm.a.y));
+  if (!FINAL && s == LPD - 1 && mok) A.yend[cm] = inc.a;  // chunk forward aggregate (zero carry)
+  // 5. forward fix-up: y(r) += g(r) y_in, g(r) = prod(-L) from the segment start
+  if (has) {
+    double gg = 1.0, Lp = Lin;
+#pragma unroll
+    for (int r = 0; r < SUB; ++r) {
+      if (r >= rs && r <= re) {
+        const int k = ib + r - m;
+        gg = (k == 0) ? 0.0 : -Lp * gg;
+        v[r] = make_double2(fma(gg, yin.x, v[r].x), fma(gg, yin.y, v[r].y));
+        Lp = sm[(s * SUB + r) * DPW + dl].x;
+      }
+    }
+  }
+  // 6. backward sweep with zero carry (laplacian.py:288-292)
+  AffW bm;
+  bm.a = make_double2(0.0, 0.0);
+  bm.g = 1.0;
+  if (has) {
+#pragma unroll
+    for (int r = SUB - 1; r >= 0; --r) {
+      if (r >= rs && r <= re) {
+        const int k = ib + r - m;
+        const double2 f = sm[(s * SUB + r) * DPW + dl];
+        if (k == len - 1) {
+          bm.a = make_double2(f.y * v[r].x, f.y * v[r].y);
+          bm.g = 0.0;
+        } else {
+          bm.a = make_double2(fma(-f.x, bm.a.x, f.y * v[r].x), fma(-f.x, bm.a.y, f.y * v[r].y));
+          bm.g = -f.x * bm.g;
+        }
+        v[r] = bm.a;
+      }
+    }
+  }
+  // 7. reverse composition over segments: x_in(s) = x_start(s+1)
+  AffW rinc = bm;
+  {
+    AffW o = aff_shfl(rinc, min(lane + 8, 31));
+    if (s <= 2) rinc = aff_compose(o, rinc);
+    o = aff_shfl(rinc, min(lane + 16, 31));
+    if (s <= 1) rinc = aff_compose(o, rinc);
+  }
+  AffW rex = aff_shfl(rinc, min(lane + 8, 31));
+  if (s == LPD - 1) {
+    rex.a = make_double2(0.0, 0.0);
+    rex.g = 1.0;
+  }
+  const double2 xch = FINAL ? A.xst[cm] : make_double2(0.0, 0.0);
+  const double2 xin = make_double2(fma(rex.g, xch.x, rex.a.x), fma(rex.g, xch.y, rex.a.y));
+  if (!FINAL) {
+    if (s == 0 && mok) A.xst[cm] = rinc.a;  // chunk backward aggregate (zero carries)
+    if (m == 0) {
+      // chunk sums for the m = 0 null-mode projection and gauge
+      double2 xs = make_double2(0.0, 0.0);
+      if (has) {
+        double hh = 1.0;
+#pragma unroll
+        for (int r = SUB - 1; r >= 0; --r) {
+          if (r >= rs && r <= re) {
+            const int k = ib + r - m;
+            hh = (k == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
+            xs = make_double2(xs.x + fma(hh, xin.x, v[r].x), xs.y + fma(hh, xin.y, v[r].y));
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 8; off < 32; off <<= 1) {
+        tb.x += __shfl_xor_sync(0xffffffff, tb.x, off);
+        tb.y += __shfl_xor_sync(0xffffffff, tb.y, off);
+        xs.x += __shfl_xor_sync(0xffffffff, xs.x, off);
+        xs.y += __shfl_xor_sync(0xffffffff, xs.y, off);
+      }
+      if (lane == 0) {
+        A.m0acc[((size_t)b * A.C + c) * 2] = tb;
+        A.m0acc[((size_t)b * A.C + c) * 2 + 1] = xs;
+      }
+    }
+    return;
+  }
+  // 8. backward fix-up and output
+  if (has) {
+    double hh = 1.0;
+#pragma unroll
+    for (int r = SUB - 1; r >= 0; --r) {
+      if (r >= rs && r <= re) {
+        const int i = ib + r;
+        const int k = i - m;
+        hh = (k == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
+        const double2 x = make_double2(fma(hh, xin.x, v[r].x), fma(hh, xin.y, v[r].y));
+        if (m == 0) {
+          // zero-mean gauge (laplacian.py:293-298): P[i][i] = -(x - g)
+          st2(p + ((size_t)i * A.ldp + i) * 2, make_double2(-(x.x - gauge.x), -(x.y - gauge.y)));
+        } else {
+          // lower triangle: P[i][i-m] = -x (laplacian.py:299-300)
+          st2(p + ((size_t)i * A.ldp + (i - m)) * 2, make_double2(-x.x, -x.y));
+        }
+        v[r] = x;
+      }
+    }
+  }
+  __syncwarp();
+  // stage x for the transposed store (reuse the factor tile)
+#pragma unroll
+  for (int r = 0; r < SUB; ++r) sm[(s * SUB + r) * DPW + dl] = v[r];
+  __syncwarp();
+  // strict upper by skew reflection: P[i-m][i] = conj(x) (laplacian.py:306-316).
+  // Output row j = i0 - m0 + t holds columns i0 + t + u, u = 0..7 (one 128 B
+  // run); each instruction writes 4 such rows.
+  const int u = lane & 7;
+  for (int t0 = -(DPW - 1); t0 < SR; t0 += 4) {
+    const int tt = t0 + (lane >> 3);
+    const int r = tt + u;  // row in chunk of diagonal m0 + u
+    const int mm = m0 + u;
+    const int i = i0 + r;
+    if (tt < SR && r >= 0 && r < SR && mm >= 1 && mm < n && i >= mm && i < n) {
+      const double2 xv = sm[r * DPW + u];
+      st2(p + ((size_t)(i - mm) * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass 2: chain the chunk carries.  Block = 32 diagonals (lanes) x 8 chunk
+// segments (warps); loads are coalesced across diagonals; the segment maps
+// are composed through shared memory.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_solve_carry(int n, int C, const double* __restrict__ G,
+                                                     const double* __restrict__ H,
+                                                     const double* __restrict__ K,
+                                                     const double* __restrict__ m0x, double2* yend,
+                                                     double2* xst, const double2* __restrict__ m0acc,
+                                                     double2* m0mg) {
+  __shared__ AffW agg[8][32];
+  __shared__ double2 red[8];
+  const int lane = threadIdx.x & 31, wseg = threadIdx.x >> 5;
+  const int m = blockIdx.x * 32 + lane;
+  const int b = blockIdx.y;
+  const size_t base = (size_t)b * C * n;
+  const bool ok = m < n;
+  const int cs = (blockIdx.x * 32) / SR;  // first chunk holding any of the 32 diagonals
+  const int nc = C - cs;
+  const int E = (nc + 7) / 8;
+  const int cb = cs + wseg * E, ce = min(cb + E, C);
+  // m = 0: mu = tr W / N from the chunk trace partials (laplacian.py:276-279)
+  double2 mu = make_double2(0.0, 0.0);
+  if (blockIdx.x == 0) {
+    double2 tr = make_double2(0.0, 0.0);
+    if (lane == 0)
+      for (int c = cb; c < ce; ++c) {
+        const double2 q = m0acc[((size_t)b * C + c) * 2];
+        tr = make_double2(tr.x + q.x, tr.y + q.y);
+      }
+    if (lane == 0) red[wseg] = tr;
+    __syncthreads();
+    double2 t = make_double2(0.0, 0.0);
+    for (int q = 0; q < 8; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
+    mu = make_double2(t.x / n, t.y / n);
+    __syncthreads();
+  }
+  const bool is0 = (m == 0);
+  // forward: segment composition
+  AffW f;
+  f.a = make_double2(0.0, 0.0);
+  f.g = 1.0;
+  if (ok)
+    for (int c = cb; c < ce; ++c) {
+      const size_t o = (size_t)c * n + m;
+      double2 a = yend[base + o];
+      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 0], a.y - mu.y * m0x[c * M0X + 0]);
+      const double gg = G[o];
+      f.a = make_double2(fma(gg, f.a.x, a.x), fma(gg, f.a.y, a.y));
+      f.g *= gg;
+    }
+  agg[wseg][lane] = f;
+  __syncthreads();
+  AffW pre;
+  pre.a = make_double2(0.0, 0.0);
+  pre.g = 1.0;
+  for (int q = 0; q < wseg; ++q) pre = aff_compose(pre, agg[q][lane]);
+  double2 y = pre.a;
+  if (ok)
+    for (int c = cb; c < ce; ++c) {
+      const size_t o = (size_t)c * n + m;
+      double2 a = yend[base + o];
+      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 0], a.y - mu.y * m0x[c * M0X + 0]);
+      yend[base + o] = y;  // y_in(c)
+      const double gg = G[o];
+      y = make_double2(fma(gg, y.x, a.x), fma(gg, y.y, a.y));
+    }
+  __syncthreads();
+  // backward: x_start(c) = (xst(c) + K y_in(c)) + H x_start(c+1)
+  AffW bk;
+  bk.a = make_double2(0.0, 0.0);
+  bk.g = 1.0;
+  if (ok)
+    for (int c = ce - 1; c >= cb; --c) {
+      const size_t o = (size_t)c * n + m;
+      double2 a = xst[base + o];
+      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 1], a.y - mu.y * m0x[c * M0X + 1]);
+      const double2 yi = yend[base + o];
+      const double kk = K[o], hh = H[o];
+      a = make_double2(fma(kk, yi.x, a.x), fma(kk, yi.y, a.y));
+      bk.a = make_double2(fma(hh, bk.a.x, a.x), fma(hh, bk.a.y, a.y));
+      bk.g *= hh;
+    }
+  agg[wseg][lane] = bk;
+  __syncthreads();
+  AffW suf;
+  suf.a = make_double2(0.0, 0.0);
+  suf.g = 1.0;
+  for (int q = 7; q > wseg; --q) suf = aff_compose(suf, agg[q][lane]);
+  double2 x = suf.a;
+  double2 gs = make_double2(0.0, 0.0);
+  if (ok)
+    for (int c = ce - 1; c >= cb; --c) {
+      const size_t o = (size_t)c * n + m;
+      double2 a = xst[base + o];
+      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 1], a.y - mu.y * m0x[c * M0X + 1]);
+      const double2 yi = yend[base + o];
+      const double kk = K[o], hh = H[o];
+      xst[base + o] = x;  // x_in(c)
+      if (is0) {
+        // chunk x-sum = (sum x^ - mu S1) + SH x_in + SK y_in  (zero-mean gauge)
+        const double2 sx = m0acc[((size_t)b * C + c) * 2 + 1];
+        const double* q = m0x + (size_t)c * M0X;
+        gs.x += (sx.x - mu.x * q[2]) + q[3] * x.x + q[4] * yi.x;
+        gs.y += (sx.y - mu.y * q[2]) + q[3] * x.y + q[4] * yi.y;
+      }
+      a = make_double2(fma(kk, yi.x, a.x), fma(kk, yi.y, a.y));
+      x = make_double2(fma(hh, x.x, a.x), fma(hh, x.y, a.y));
+    }
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    if (lane == 0) red[wseg] = gs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int q = 0; q < 8; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
+      m0mg[2 * b] = mu;
+      m0mg[2 * b + 1] = make_double2(t.x / n, t.y / n);  // laplacian.py:293-296
+    }
+  }
+}
 
 __device__ __forceinline__ void tile_coords(int t, int& c, int& g) {
   c = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((c + 1) * (c + 2) / 2 <= t) ++c;
   while (c * (c + 1) / 2 > t) --c;
   g = t - c * (c + 1) / 2;
-}
-
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, 3) k_solve_tiles(SolveArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b = blockIdx.y;
-  const double* w = A.w + (size_t)b * A.sw * 2;
-  double* p = A.p + (size_t)b * A.sp * 2;
-  const int n = A.n;
-  int blk = blockIdx.x;
-  if (!FINAL) {
-    if (blk == 0) {
-      solve_m0(n, A.L0, A.dinv0, w, A.ldw, p, A.ldp, smem_raw);
-      return;
-    }
-    --blk;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blk * SOLVE_WARPS + warp;
-  if (t >= A.ntiles) return;
-  int c, g;
-  tile_coords(t, c, g);
-  const int i0 = c * TR;
-  const int m = g * TR + lane;
-  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * TR * 32;  // [r][lane]
-  const bool lane_ok = (m >= 1) && (m < n) && (m <= i0 + TR - 1);
-  const int len = n - m;
-  const int r0 = max(0, m - i0);
-  const int rl = min(TR - 1, n - 1 - i0);  // last row of the chunk inside the matrix
-  const size_t cm = (size_t)b * A.C * n + (size_t)c * n + m;
-
-  double2 v[TR];
-#pragma unroll
-  for (int r = 0; r < TR; ++r) {
-    const int i = i0 + r;
-    v[r] = (lane_ok && r >= r0 && r <= rl) ? ld2(w + ((size_t)i * A.ldw + (i - m)) * 2)
-                                           : make_double2(0.0, 0.0);
-  }
-  if (!lane_ok) {
-    if (FINAL) {  // keep smem tile defined for the transposed store
-#pragma unroll
-      for (int r = 0; r < TR; ++r) sm[r * 32 + lane] = make_double2(0.0, 0.0);
-    }
-    return;
-  }
-  // factor chain first (independent of the W loads still in flight):
-  // dpttrf order L = e/d, d' = diag - L*e, dinv = 1/d (laplacian.py:208-215)
-  {
-    double d = A.d0[(size_t)c * n + m];
-#pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      if (r >= r0 && r <= rl) {
-        const int i = i0 + r;
-        const int k = i - m;
-        const double di = __drcp_rn(d);
-        double L = 0.0;
-        if (k < len - 1) {
-          const double e = __dmul_rn(-A.sqB[i], A.sqB[k]);
-          L = __ddiv_rn(e, d);
-          d = __dsub_rn(block_diag(n, m, k + 1), __dmul_rn(L, e));
-        }
-        sm[r * 32 + lane] = make_double2(L, di);
-      }
-    }
-  }
-  // forward sweep (laplacian.py:280-287)
-  double Lprev = A.lin[(size_t)c * n + m];
-  double2 y = FINAL ? A.yend[cm] : make_double2(0.0, 0.0);
-#pragma unroll
-  for (int r = 0; r < TR; ++r) {
-    if (r >= r0 && r <= rl) {
-      const int k = i0 + r - m;
-      y = (k == 0) ? v[r] : csub(v[r], rmul(Lprev, y));
-      Lprev = sm[r * 32 + lane].x;
-      v[r] = y;
-    }
-  }
-  if (!FINAL) A.yend[cm] = y;
-  // backward sweep (laplacian.py:288-292)
-  double2 x = FINAL ? A.xst[cm] : make_double2(0.0, 0.0);
-#pragma unroll
-  for (int r = TR - 1; r >= 0; --r) {
-    if (r >= r0 && r <= rl) {
-      const int i = i0 + r;
-      const int k = i - m;
-      const double2 f = sm[r * 32 + lane];
-      x = (k == len - 1) ? rmul(f.y, v[r]) : csub(rmul(f.y, v[r]), rmul(f.x, x));
-      if (FINAL) {
-        // lower triangle: P[i][i-m] = -x (laplacian.py:297-300), coalesced
-        st2(p + ((size_t)i * A.ldp + (i - m)) * 2, make_double2(-x.x, -x.y));
-        sm[r * 32 + lane] = x;
-      }
-    } else if (FINAL) {
-      sm[r * 32 + lane] = make_double2(0.0, 0.0);
-    }
-  }
-  if (!FINAL) {
-    A.xst[cm] = x;
-    return;
-  }
-  // strict upper by skew reflection: P[i-m][i] = -conj(-x) = conj(x)
-  // (laplacian.py:306-316); lane l writes column i0+t+l of row i0-m0+t.
-  const int m0 = g * TR;
-#pragma unroll 4
-  for (int tt = -(TR - 1); tt <= TR - 1; ++tt) {
-    const int r = tt + lane;
-    if (r >= r0 && r <= rl && r >= 0 && r < TR) {
-      const double2 xv = sm[r * 32 + lane];
-      const int j = i0 - m0 + tt;
-      st2(p + ((size_t)j * A.ldp + (i0 + r)) * 2, make_double2(xv.x, -xv.y));
-    }
-  }
-}
-
-// pass 2: chain the chunk carries, one thread per diagonal; loads are
-// batched 8 chunks ahead so the serial chain is not latency bound
-__global__ void k_solve_carry(int n, int C, const double* __restrict__ G,
-                              const double* __restrict__ H, const double* __restrict__ K,
-                              double2* yend, double2* xst) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m < 1 || m >= n) return;
-  const size_t base = (size_t)blockIdx.y * C * n;
-  const int cs = m / TR;
-  constexpr int PF = 8;
-  double2 y = make_double2(0.0, 0.0);
-  for (int c0 = cs; c0 < C; c0 += PF) {
-    double2 t[PF];
-    double gg[PF];
-#pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int c = c0 + q;
-      if (c < C) {
-        t[q] = yend[base + (size_t)c * n + m];
-        gg[q] = G[(size_t)c * n + m];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int c = c0 + q;
-      if (c < C) {
-        yend[base + (size_t)c * n + m] = y;
-        y = make_double2(t[q].x + gg[q] * y.x, t[q].y + gg[q] * y.y);
-      }
-    }
-  }
-  double2 x = make_double2(0.0, 0.0);
-  for (int c0 = C - 1; c0 >= cs; c0 -= PF) {
-    double2 t[PF], yi[PF];
-    double hh[PF], kk[PF];
-#pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int c = c0 - q;
-      if (c >= cs) {
-        const size_t o = (size_t)c * n + m;
-        t[q] = xst[base + o];
-        yi[q] = yend[base + o];
-        hh[q] = H[o];
-        kk[q] = K[o];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int c = c0 - q;
-      if (c >= cs) {
-        xst[base + (size_t)c * n + m] = x;
-        x = make_double2(t[q].x + hh[q] * x.x + kk[q] * yi[q].x, t[q].y + hh[q] * x.y + kk[q] * yi[q].y);
-      }
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -602,18 +710,20 @@ __global__ void k_resid_final(int nt, const double* __restrict__ partial, double
 // ---------------------------------------------------------------------------
 
 static size_t op_bytes(int n, int C) {
-  return sizeof(double) * ((size_t)3 * n + (size_t)5 * C * n) + 256;
+  const size_t nsub = (size_t)(n + SUB - 1) / SUB;
+  return sizeof(double) * ((size_t)3 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) + 256;
 }
 
 int op_create(int n, int device, zt_operator** out) {
   if (n < 2) return fail(ZT_EINVAL, "matrix truncation must be at least 2, got " + std::to_string(n));
+  if (n > 65536) return fail(ZT_EINVAL, "matrix truncation above 65536 is not supported");
   int prev;
   ZT_CUDA_CHECK(cudaGetDevice(&prev));
   ZT_CUDA_CHECK(cudaSetDevice(device));
   zt_operator* op = new zt_operator;
   op->n = n;
   op->device = device;
-  op->C = (n + TR - 1) / TR;
+  op->C = (n + SR - 1) / SR;
   const int C = op->C;
   cudaError_t e = cudaMalloc(&op->block, op_bytes(n, C));
   if (e != cudaSuccess) {
@@ -629,7 +739,7 @@ int op_create(int n, int device, zt_operator** out) {
   op->dinv0 = q;
   q += n;
   op->d0 = q;
-  q += (size_t)C * n;
+  q += (size_t)((n + SUB - 1) / SUB) * n;
   op->lin = q;
   q += (size_t)C * n;
   op->G = q;
@@ -637,12 +747,19 @@ int op_create(int n, int device, zt_operator** out) {
   op->H = q;
   q += (size_t)C * n;
   op->K = q;
+  q += (size_t)C * n;
+  op->m0x = q;
   cudaMemset(op->block, 0, op_bytes(n, C));
   k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB);
   ZT_LAUNCHED();
-  k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lin, op->G, op->H, op->K,
-                                        op->L0, op->dinv0);
+  k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lin, op->G, op->H, op->K, op->L0,
+                                        op->dinv0, op->m0x);
   ZT_LAUNCHED();
+  int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
+  int asmem = SOLVE_WARPS * TR * 32 * (int)sizeof(double2);
+  cudaFuncSetAttribute(k_solve_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
   e = cudaDeviceSynchronize();
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
@@ -662,29 +779,20 @@ int op_destroy(zt_operator* op) {
 }
 
 size_t solve_workspace_bytes(int n, int batch) {
-  const int C = (n + TR - 1) / TR;
-  return (size_t)2 * batch * C * n * sizeof(double2) + 256;
+  const int C = (n + SR - 1) / SR;
+  return (size_t)batch * (2 * (size_t)C * n + 2 * (size_t)C + 2) * sizeof(double2) + 256;
 }
-
-static int solve_smem() { return SOLVE_WARPS * TR * 32 * (int)sizeof(double2); }
 
 int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
                  int64_t sp, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int n = op->n, C = op->C;
   if (ws_bytes < solve_workspace_bytes(n, batch)) return fail(ZT_ENOMEM, "solve workspace too small");
-  static bool attr_done = false;
-  if (!attr_done) {
-    ZT_CUDA_CHECK(cudaFuncSetAttribute(k_solve_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem()));
-    ZT_CUDA_CHECK(cudaFuncSetAttribute(k_solve_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem()));
-    ZT_CUDA_CHECK(cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem()));
-    attr_done = true;
-  }
   SolveArgs A;
   A.n = n;
   A.C = C;
-  A.ntiles = C * (C + 1) / 2;
+  A.ntiles = solve_ntiles(C);
   A.sqB = op->sqB;
-  A.d0 = op->d0;
+  A.d0s = op->d0;
   A.lin = op->lin;
   A.L0 = op->L0;
   A.dinv0 = op->dinv0;
@@ -696,12 +804,16 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
   A.sp = sp;
   A.yend = reinterpret_cast<double2*>(ws);
   A.xst = A.yend + (size_t)batch * C * n;
+  A.m0acc = A.xst + (size_t)batch * C * n;
+  A.m0mg = A.m0acc + (size_t)batch * C * 2;
+  const int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   const int tb = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  k_solve_tiles<false><<<dim3(tb + 1, batch), SOLVE_WARPS * 32, solve_smem(), st>>>(A);
+  k_solve_tiles<false><<<dim3(tb, batch), SOLVE_WARPS * 32, smem, st>>>(A);
   ZT_LAUNCHED();
-  k_solve_carry<<<dim3((n + 127) / 128, batch), 128, 0, st>>>(n, C, op->G, op->H, op->K, A.yend, A.xst);
+  k_solve_carry<<<dim3((n + 31) / 32, batch), 256, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x, A.yend,
+                                                          A.xst, A.m0acc, A.m0mg);
   ZT_LAUNCHED();
-  k_solve_tiles<true><<<dim3(tb, batch), SOLVE_WARPS * 32, solve_smem(), st>>>(A);
+  k_solve_tiles<true><<<dim3(tb, batch), SOLVE_WARPS * 32, smem, st>>>(A);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -710,16 +822,11 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
 int apply_laplacian(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* y,
                     int64_t ldy, int64_t sy, int sign, int batch, cudaStream_t st) {
   if (sign != 1 && sign != -1) return fail(ZT_EINVAL, "sign must be -1 or +1");
-  const int n = op->n, C = op->C;
-  static bool attr_done = false;
-  if (!attr_done) {
-    ZT_CUDA_CHECK(cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem()));
-    attr_done = true;
-  }
+  const int n = op->n, Ca = (n + TR - 1) / TR;
   ApplyArgs A;
   A.n = n;
-  A.C = C;
-  A.ntiles = C * (C + 1) / 2;
+  A.C = Ca;
+  A.ntiles = Ca * (Ca + 1) / 2;
   A.sign = sign;
   A.sqB = op->sqB;
   A.w = w;
@@ -729,7 +836,7 @@ int apply_laplacian(zt_operator* op, const double* w, int64_t ldw, int64_t sw, d
   A.ldy = ldy;
   A.sy = sy;
   const int tb = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  k_apply_tiles<<<dim3(tb, batch), SOLVE_WARPS * 32, solve_smem(), st>>>(A);
+  k_apply_tiles<<<dim3(tb, batch), SOLVE_WARPS * 32, SOLVE_WARPS * TR * 32 * (int)sizeof(double2), st>>>(A);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -757,9 +864,10 @@ int op_factors(zt_operator* op, double* linv_h, double* dinv_h) {
   // by replaying the recurrence on the host from the device chunk pivots —
   // used by tests to prove bit-identity with dpttrf.
   const int n = op->n, C = op->C;
-  std::vector<double> sq(n), d0((size_t)C * n), L0(n), di0(n);
+  const size_t nsub = (size_t)(n + SUB - 1) / SUB;
+  std::vector<double> sq(n), d0(nsub * n), L0(n), di0(n);
   ZT_CUDA_CHECK(cudaMemcpy(sq.data(), op->sqB, sizeof(double) * n, cudaMemcpyDeviceToHost));
-  ZT_CUDA_CHECK(cudaMemcpy(d0.data(), op->d0, sizeof(double) * C * n, cudaMemcpyDeviceToHost));
+  ZT_CUDA_CHECK(cudaMemcpy(d0.data(), op->d0, sizeof(double) * nsub * n, cudaMemcpyDeviceToHost));
   ZT_CUDA_CHECK(cudaMemcpy(L0.data(), op->L0, sizeof(double) * n, cudaMemcpyDeviceToHost));
   ZT_CUDA_CHECK(cudaMemcpy(di0.data(), op->dinv0, sizeof(double) * n, cudaMemcpyDeviceToHost));
   if (linv_h) std::fill(linv_h, linv_h + (size_t)n * n, 0.0);
@@ -773,8 +881,8 @@ int op_factors(zt_operator* op, double* linv_h, double* dinv_h) {
     for (int k = 0; k < len; ++k) {
       const int i = m + k;
       // pivots at each row are recomputed exactly as the device does
-      double d = d0[(size_t)(i / TR) * n + m];
-      const int kstart = std::max(i / TR * TR, m) - m;
+      double d = d0[(size_t)(i / SUB) * n + m];
+      const int kstart = std::max(i / SUB * SUB, m) - m;
       for (int kk = kstart; kk < k; ++kk) {
         const double e = (-sq[m + kk]) * sq[kk];
         const double L = e / d;
