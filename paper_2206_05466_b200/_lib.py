@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzt.so")
+LIB_PATH = os.environ.get("ZT_LIB_PATH") or os.path.join(_HERE, "libzt.so")
 
 ZT_OK, ZT_EINVAL, ZT_ESTRUCTURE, ZT_ENOCONV, ZT_ELINALG, ZT_ECUDA, ZT_ENCCL, ZT_ENOMEM = range(8)
 

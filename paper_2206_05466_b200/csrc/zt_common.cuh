@@ -21,6 +21,8 @@ struct zt_operator {
   double* H = nullptr;
   double* K = nullptr;
   double* m0x = nullptr;  // m = 0 per-chunk constant-RHS responses
+  int2* gen_tiles = nullptr;  // (chunk, group) of the boundary tiles
+  int ngen = 0;
   void* block = nullptr;  // single allocation holding every table
 };
 

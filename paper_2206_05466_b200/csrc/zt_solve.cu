@@ -38,6 +38,9 @@ constexpr int LPD = 4;         // lanes per diagonal
 constexpr int DPW = 32 / LPD;  // diagonals per warp tile
 constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
+#ifndef SOLVE_FAST_MINB
+#define SOLVE_FAST_MINB 4
+#endif
 constexpr int TR = 32;  // rows per apply tile / diagonals per apply tile
 constexpr int M0X = 5;  // m = 0 per-chunk responses: Y1, X1, S1, SH, SK
 
@@ -195,42 +198,37 @@ __device__ __forceinline__ void solve_tile_coords(int t, int& c, int& g) {
 
 static int solve_ntiles(int C) { return 4 * C * (C + 1); }
 
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b = blockIdx.y;
-  const double* w = A.w + (size_t)b * A.sw * 2;
-  double* p = A.p + (size_t)b * A.sp * 2;
+// Per-lane body.  FAST: every lane owns 16 interior rows of its diagonal
+// (k >= 1 at the first row, the diagonal's last row not inside, m != 0), so
+// all boundary predicates vanish and addresses advance by a constant stride.
+template <bool FINAL, bool FAST>
+__device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __restrict__ w,
+                                          double* __restrict__ p, int b, int c, int m0, int lane,
+                                          double2* sm) {
   const int n = A.n;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * SOLVE_WARPS + warp;
-  if (t >= A.ntiles) return;
-  int c, g;
-  solve_tile_coords(t, c, g);
   const int i0 = c * SR;
-  const int m0 = g * DPW;
-  if (m0 >= n || m0 > i0 + SR - 1) return;  // whole tile empty (warp-uniform)
   const int dl = lane & (DPW - 1), s = lane >> 3;
   const int m = m0 + dl;
   const int ib = i0 + s * SUB;
-  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;  // [row in chunk][dl]
   const bool mok = m < n;
   const int len = n - m;
-  const int rs = max(0, m - ib);
-  const int re = min(SUB - 1, n - 1 - ib);
-  const bool has = mok && rs <= re;
+  const int rs = FAST ? 0 : max(0, m - ib);
+  const int re = FAST ? SUB - 1 : min(SUB - 1, n - 1 - ib);
+  const bool has = FAST || (mok && rs <= re);
   const size_t cm = (size_t)b * A.C * n + (size_t)c * n + m;
+  const int64_t wstride = (A.ldw + 1) * 2;  // doubles between W[i][i-m] and W[i+1][i+1-m]
+  const double* wp = w + ((int64_t)ib * A.ldw + (ib - m)) * 2;
+#define ROW_OK(r) (FAST || ((r) >= rs && (r) <= re))
 
-  // 1. loads (16 rows, coalesced: each instruction covers 4 rows x 128 B)
+  // 1. loads (16 rows; each instruction covers 4 rows x 128 B)
   double2 v[SUB];
 #pragma unroll
-  for (int r = 0; r < SUB; ++r) {
-    const int i = ib + r;
-    v[r] = (has && r >= rs && r <= re) ? ld2(w + ((size_t)i * A.ldw + (i - m)) * 2) : make_double2(0.0, 0.0);
-  }
-  // 2. factor chain for my 16 rows, starting from the exact sub-chunk pivot
+  for (int r = 0; r < SUB; ++r)
+    v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
+
+  // 2. factor chain from the exact sub-chunk pivot (dpttrf order, fast rcp)
   if (has) {
-    if (m == 0) {
+    if (!FAST && m == 0) {
 #pragma unroll
       for (int r = 0; r < SUB; ++r)
         if (r <= re) sm[(s * SUB + r) * DPW + dl] = make_double2(A.L0[ib + r], A.dinv0[ib + r]);
@@ -239,20 +237,21 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
       int k = ib + rs - m;
       double dg = block_diag(n, m, k);
       double inc = 2.0 * (double)(n - 2 - 2 * k - m);  // diag(k+1) - diag(k), exact
+      const double* sqi = A.sqB + ib + rs;
+      const double* sqk = A.sqB + k;
 #pragma unroll
       for (int r = 0; r < SUB; ++r) {
-        if (r >= rs && r <= re) {
+        if (ROW_OK(r)) {
           const double di = fast_rcp(d);
           double L = 0.0;
-          if (k < len - 1) {
-            const double e = -A.sqB[ib + r] * A.sqB[k];
+          if (FAST || k + (r - rs) < len - 1) {
+            const double e = -sqi[r - rs] * sqk[r - rs];
             L = e * di;
             dg += inc;
             inc -= 4.0;
             d = fma(-L, e, dg);
           }
           sm[(s * SUB + r) * DPW + dl] = make_double2(L, di);
-          ++k;
         }
       }
     }
@@ -263,7 +262,7 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
   if (has) Lin = (s == 0) ? A.lin[(size_t)c * n + m] : sm[(s * SUB - 1) * DPW + dl].x;
 
   double2 mu = make_double2(0.0, 0.0), gauge = make_double2(0.0, 0.0);
-  if (FINAL && m == 0) {
+  if (!FAST && FINAL && m == 0) {
     mu = A.m0mg[2 * b];
     gauge = A.m0mg[2 * b + 1];
   }
@@ -276,12 +275,11 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
     double Lp = Lin;
 #pragma unroll
     for (int r = 0; r < SUB; ++r) {
-      if (r >= rs && r <= re) {
-        const int k = ib + r - m;
+      if (ROW_OK(r)) {
         double2 bb = v[r];
-        if (!FINAL && m == 0) tb = make_double2(tb.x + bb.x, tb.y + bb.y);
-        if (FINAL && m == 0) bb = csub(bb, mu);
-        if (k == 0) {
+        if (!FAST && !FINAL && m == 0) tb = make_double2(tb.x + bb.x, tb.y + bb.y);
+        if (!FAST && FINAL && m == 0) bb = csub(bb, mu);
+        if (!FAST && ib + r - m == 0) {
           fm.a = bb;
           fm.g = 0.0;
         } else {
@@ -306,7 +304,7 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
     exm.a = make_double2(0.0, 0.0);
     exm.g = 1.0;
   }
-  const double2 ych = FINAL ? A.yend[cm] : make_double2(0.0, 0.0);
+  const double2 ych = (FINAL && mok) ? A.yend[cm] : make_double2(0.0, 0.0);
   const double2 yin = make_double2(fma(exm.g, ych.x, exm.a.x), fma(exm.g, ych.y, exm.a.y));
   if (!FINAL && s == LPD - 1 && mok) A.yend[cm] = inc.a;  // chunk forward aggregate (zero carry)
   // 5. forward fix-up: y(r) += g(r) y_in, g(r) = prod(-L) from the segment start
@@ -314,9 +312,8 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
     double gg = 1.0, Lp = Lin;
 #pragma unroll
     for (int r = 0; r < SUB; ++r) {
-      if (r >= rs && r <= re) {
-        const int k = ib + r - m;
-        gg = (k == 0) ? 0.0 : -Lp * gg;
+      if (ROW_OK(r)) {
+        gg = (!FAST && ib + r - m == 0) ? 0.0 : -Lp * gg;
         v[r] = make_double2(fma(gg, yin.x, v[r].x), fma(gg, yin.y, v[r].y));
         Lp = sm[(s * SUB + r) * DPW + dl].x;
       }
@@ -329,10 +326,9 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
   if (has) {
 #pragma unroll
     for (int r = SUB - 1; r >= 0; --r) {
-      if (r >= rs && r <= re) {
-        const int k = ib + r - m;
+      if (ROW_OK(r)) {
         const double2 f = sm[(s * SUB + r) * DPW + dl];
-        if (k == len - 1) {
+        if (!FAST && ib + r - m == len - 1) {
           bm.a = make_double2(f.y * v[r].x, f.y * v[r].y);
           bm.g = 0.0;
         } else {
@@ -356,20 +352,19 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
     rex.a = make_double2(0.0, 0.0);
     rex.g = 1.0;
   }
-  const double2 xch = FINAL ? A.xst[cm] : make_double2(0.0, 0.0);
+  const double2 xch = (FINAL && mok) ? A.xst[cm] : make_double2(0.0, 0.0);
   const double2 xin = make_double2(fma(rex.g, xch.x, rex.a.x), fma(rex.g, xch.y, rex.a.y));
   if (!FINAL) {
     if (s == 0 && mok) A.xst[cm] = rinc.a;  // chunk backward aggregate (zero carries)
-    if (m == 0) {
-      // chunk sums for the m = 0 null-mode projection and gauge
+    if (!FAST && m0 == 0) {
+      // chunk sums for the m = 0 null-mode projection and gauge (lanes dl == 0)
       double2 xs = make_double2(0.0, 0.0);
-      if (has) {
+      if (has && m == 0) {
         double hh = 1.0;
 #pragma unroll
         for (int r = SUB - 1; r >= 0; --r) {
           if (r >= rs && r <= re) {
-            const int k = ib + r - m;
-            hh = (k == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
+            hh = (ib + r - m == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
             xs = make_double2(xs.x + fma(hh, xin.x, v[r].x), xs.y + fma(hh, xin.y, v[r].y));
           }
         }
@@ -389,26 +384,27 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
     return;
   }
   // 8. backward fix-up and output
+  const int64_t pstride = (A.ldp + 1) * 2;
+  double* pp = p + ((int64_t)ib * A.ldp + (ib - m)) * 2;
   if (has) {
     double hh = 1.0;
 #pragma unroll
     for (int r = SUB - 1; r >= 0; --r) {
-      if (r >= rs && r <= re) {
-        const int i = ib + r;
-        const int k = i - m;
-        hh = (k == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
+      if (ROW_OK(r)) {
+        hh = (!FAST && ib + r - m == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
         const double2 x = make_double2(fma(hh, xin.x, v[r].x), fma(hh, xin.y, v[r].y));
-        if (m == 0) {
+        if (!FAST && m == 0) {
           // zero-mean gauge (laplacian.py:293-298): P[i][i] = -(x - g)
-          st2(p + ((size_t)i * A.ldp + i) * 2, make_double2(-(x.x - gauge.x), -(x.y - gauge.y)));
+          st2(pp + r * pstride, make_double2(-(x.x - gauge.x), -(x.y - gauge.y)));
         } else {
           // lower triangle: P[i][i-m] = -x (laplacian.py:299-300)
-          st2(p + ((size_t)i * A.ldp + (i - m)) * 2, make_double2(-x.x, -x.y));
+          st2(pp + r * pstride, make_double2(-x.x, -x.y));
         }
         v[r] = x;
       }
     }
   }
+#undef ROW_OK
   __syncwarp();
   // stage x for the transposed store (reuse the factor tile)
 #pragma unroll
@@ -418,16 +414,63 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_tiles(SolveArgs A
   // Output row j = i0 - m0 + t holds columns i0 + t + u, u = 0..7 (one 128 B
   // run); each instruction writes 4 such rows.
   const int u = lane & 7;
+  const int mm = m0 + u;
+  const bool uok = mm >= 1 && mm < n;
   for (int t0 = -(DPW - 1); t0 < SR; t0 += 4) {
     const int tt = t0 + (lane >> 3);
     const int r = tt + u;  // row in chunk of diagonal m0 + u
-    const int mm = m0 + u;
     const int i = i0 + r;
-    if (tt < SR && r >= 0 && r < SR && mm >= 1 && mm < n && i >= mm && i < n) {
+    if (uok && tt < SR && r >= 0 && r < SR && i >= mm && i < n) {
       const double2 xv = sm[r * DPW + u];
       st2(p + ((size_t)(i - mm) * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
     }
   }
+}
+
+// Interior tiles: chunks c < Cf (the chunk ends before row n-2), groups
+// g = 1 .. 8c-1 (all 8 diagonals start before the chunk).  Count per chunk
+// 8c-1, prefix (c-1)(4c-1).
+__device__ __forceinline__ void fast_tile_coords(int t, int& c, int& g) {
+  int q = (int)(sqrt((double)t * 0.25)) + 1;
+  while (q > 1 && (q - 1) * (4 * q - 1) > t) --q;
+  while (q * (4 * q + 3) <= t) ++q;
+  c = q;
+  g = 1 + t - (q - 1) * (4 * q - 1);
+}
+
+static int fast_chunks(int n) {
+  // chunks whose rows i0 .. i0+63 all satisfy i < n-1
+  int cf = 0;
+  while ((cf + 1) * SR < n - 1) ++cf;
+  return cf;
+}
+static int fast_ntiles(int cf) { return cf >= 1 ? (cf - 1) * (4 * cf - 1) : 0; }
+
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_FAST_MINB) k_solve_fast(SolveArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // independent of the generic launch of the same pass: let it start now
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * SOLVE_WARPS + warp;
+  if (t >= A.ntiles) return;
+  int c, g;
+  fast_tile_coords(t, c, g);
+  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
+  tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane, sm);
+}
+
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_generic(SolveArgs A, const int2* __restrict__ tiles, int count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * SOLVE_WARPS + warp;
+  if (t >= count) return;
+  const int2 cg = tiles[t];
+  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
+  tile_body<FINAL, false>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, cg.x, cg.y * DPW, lane, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -709,9 +752,24 @@ __global__ void k_resid_final(int nt, const double* __restrict__ partial, double
 // host side
 // ---------------------------------------------------------------------------
 
+static std::vector<int2> generic_tiles(int n) {
+  const int C = (n + SR - 1) / SR, Gt = (n + DPW - 1) / DPW, cf = fast_chunks(n);
+  std::vector<int2> v;
+  for (int c = 0; c < C; ++c) {
+    const int gmax = std::min(Gt - 1, (c * SR + SR - 1) / DPW);
+    for (int g = 0; g <= gmax; ++g) {
+      const bool fast = (c < cf) && g >= 1 && g <= 8 * c - 1;
+      if (!fast) v.push_back(make_int2(c, g));
+    }
+  }
+  return v;
+}
+
 static size_t op_bytes(int n, int C) {
   const size_t nsub = (size_t)(n + SUB - 1) / SUB;
-  return sizeof(double) * ((size_t)3 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) + 256;
+  const size_t ngen = generic_tiles(n).size();
+  return sizeof(double) * ((size_t)3 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
+         sizeof(int2) * ngen + 512;
 }
 
 int op_create(int n, int device, zt_operator** out) {
@@ -749,7 +807,14 @@ int op_create(int n, int device, zt_operator** out) {
   op->K = q;
   q += (size_t)C * n;
   op->m0x = q;
+  q += (size_t)M0X * C;
   cudaMemset(op->block, 0, op_bytes(n, C));
+  {
+    std::vector<int2> gt = generic_tiles(n);
+    op->gen_tiles = reinterpret_cast<int2*>(reinterpret_cast<uintptr_t>(q + 1) & ~(uintptr_t)7);
+    op->ngen = (int)gt.size();
+    cudaMemcpy(op->gen_tiles, gt.data(), sizeof(int2) * gt.size(), cudaMemcpyHostToDevice);
+  }
   k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB);
   ZT_LAUNCHED();
   k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lin, op->G, op->H, op->K, op->L0,
@@ -757,8 +822,10 @@ int op_create(int n, int device, zt_operator** out) {
   ZT_LAUNCHED();
   int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   int asmem = SOLVE_WARPS * TR * 32 * (int)sizeof(double2);
-  cudaFuncSetAttribute(k_solve_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
   e = cudaDeviceSynchronize();
   cudaSetDevice(prev);
@@ -781,6 +848,25 @@ int op_destroy(zt_operator* op) {
 size_t solve_workspace_bytes(int n, int batch) {
   const int C = (n + SR - 1) / SR;
   return (size_t)batch * (2 * (size_t)C * n + 2 * (size_t)C + 2) * sizeof(double2) + 256;
+}
+
+// Launch a generic-tile kernel; with `pdl` it may start while the preceding
+// interior-tile kernel of the same pass is still running (they touch
+// disjoint tiles; the preceding kernel signals launch_dependents at entry).
+static cudaError_t launch_pdl(const void* fn, dim3 grid, int smem, cudaStream_t st, SolveArgs A,
+                              const int2* tiles, int count, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(SOLVE_WARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  void* args[] = {&A, (void*)&tiles, &count};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
@@ -807,13 +893,26 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
   A.m0acc = A.xst + (size_t)batch * C * n;
   A.m0mg = A.m0acc + (size_t)batch * C * 2;
   const int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
-  const int tb = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  k_solve_tiles<false><<<dim3(tb, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+  A.ntiles = fast_ntiles(fast_chunks(n));
+  const int tf = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
+  const int tg = (op->ngen + SOLVE_WARPS - 1) / SOLVE_WARPS;
+  // pass 1: interior tiles, then (programmatically overlapped) boundary tiles
+  if (tf > 0) {
+    k_solve_fast<false><<<dim3(tf, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+    ZT_LAUNCHED();
+  }
+  ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<false>), dim3(tg, batch), smem, st,
+                           A, op->gen_tiles, op->ngen, tf > 0));
   ZT_LAUNCHED();
   k_solve_carry<<<dim3((n + 31) / 32, batch), 256, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x, A.yend,
                                                           A.xst, A.m0acc, A.m0mg);
   ZT_LAUNCHED();
-  k_solve_tiles<true><<<dim3(tb, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+  if (tf > 0) {
+    k_solve_fast<true><<<dim3(tf, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+    ZT_LAUNCHED();
+  }
+  ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<true>), dim3(tg, batch), smem, st,
+                           A, op->gen_tiles, op->ngen, tf > 0));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
