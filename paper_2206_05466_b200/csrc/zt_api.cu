@@ -9,7 +9,7 @@
 #include <string>
 #include <vector>
 
-#include "zt_common.cuh"
+#include "zt_tma.cuh"
 
 
 
@@ -17,6 +17,24 @@ namespace zt {
 
 std::atomic<int64_t> g_launches{0};
 static thread_local std::string t_err;
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int encode_tiled_f64(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
+                     const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    ZT_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(ZT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ZT_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return ZT_OK;
+}
 
 void set_error(const std::string& msg) { t_err = msg; }
 int fail(int status, const std::string& msg) {

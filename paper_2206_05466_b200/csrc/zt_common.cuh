@@ -13,6 +13,7 @@
 struct zt_operator {
   int n = 0, device = 0, C = 0;
   double* sqB = nullptr;
+  double* Bq = nullptr;  // (j+1)(N-1-j) as exact doubles
   double* L0 = nullptr;
   double* dinv0 = nullptr;
   double* d0 = nullptr;
@@ -23,6 +24,12 @@ struct zt_operator {
   double* m0x = nullptr;  // m = 0 per-chunk constant-RHS responses
   int2* gen_tiles = nullptr;  // (chunk, group) of the boundary tiles
   int ngen = 0;
+  int fast_blocks = 0;
+  bool solve_tma = false;
+  bool solve_amortize = true;
+  int nside = 0;              // side streams for batched solves
+  cudaStream_t side[8] = {};
+  cudaEvent_t fork = nullptr, join[8] = {};  // batch > 1: one factor chain per tile for all matrices  // interior tiles: persistent TMA-prefetch kernel vs direct loads  // resident blocks of the persistent interior-tile kernel
   void* block = nullptr;  // single allocation holding every table
 };
 

@@ -29,15 +29,21 @@
 #include <string>
 #include <vector>
 
-#include "zt_common.cuh"
+#include "zt_tma.cuh"
 
 namespace zt {
 
-constexpr int SUB = 16;        // rows per lane (sub-chunk)
-constexpr int LPD = 4;         // lanes per diagonal
+#ifndef SOLVE_SUB
+#define SOLVE_SUB 16
+#endif
+constexpr int SUB = SOLVE_SUB;  // rows per lane (sub-chunk)
+constexpr int LPD = 64 / SUB;   // lanes per diagonal
 constexpr int DPW = 32 / LPD;  // diagonals per warp tile
 constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
+#ifndef SOLVE_DIRECT_MINB
+#define SOLVE_DIRECT_MINB 4
+#endif
 #ifndef SOLVE_FAST_MINB
 #define SOLVE_FAST_MINB 4
 #endif
@@ -50,9 +56,12 @@ constexpr int M0X = 5;  // m = 0 per-chunk responses: Y1, X1, S1, SH, SK
 // sub-chunk start, and per 64-row chunk the coupling into the chunk and the
 // carry gains G (forward), H (backward), K (forward carry -> backward start).
 // ---------------------------------------------------------------------------
-__global__ void k_op_sqrt_table(int n, double* sqB) {
+__global__ void k_op_sqrt_table(int n, double* sqB, double* Bq) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) sqB[j] = sqrt((j + 1.0) * (n - 1.0 - j));  // sqrt((i+1)(N-1-i)), laplacian.py:134-136
+  if (j < n) {
+    Bq[j] = (j + 1.0) * (n - 1.0 - j);
+    sqB[j] = sqrt(Bq[j]);  // sqrt((i+1)(N-1-i)), laplacian.py:134-136
+  }
 }
 
 __global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double* d0s, double* lin,
@@ -154,6 +163,7 @@ __device__ __forceinline__ double fast_rcp(double d) {
 struct SolveArgs {
   int n, C, ntiles;
   const double* sqB;
+  const double* Bq;  // (j+1)(N-1-j), exact
   const double* d0s;
   const double* lin;
   const double* L0;
@@ -204,10 +214,11 @@ static int solve_ntiles(int C) { return 4 * C * (C + 1); }
 template <bool FINAL, bool FAST>
 __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __restrict__ w,
                                           double* __restrict__ p, int b, int c, int m0, int lane,
-                                          double2* sm) {
+                                          double2* sm, const double2* vpre = nullptr,
+                                          bool do_factors = true, double2* xstage = nullptr) {
   const int n = A.n;
   const int i0 = c * SR;
-  const int dl = lane & (DPW - 1), s = lane >> 3;
+  const int dl = lane % DPW, s = lane / DPW;
   const int m = m0 + dl;
   const int ib = i0 + s * SUB;
   const bool mok = m < n;
@@ -220,36 +231,54 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   const double* wp = w + ((int64_t)ib * A.ldw + (ib - m)) * 2;
 #define ROW_OK(r) (FAST || ((r) >= rs && (r) <= re))
 
-  // 1. loads (16 rows; each instruction covers 4 rows x 128 B)
+  // 1. loads (16 rows; each instruction covers 4 rows x 128 B), or the
+  // values already staged by TMA (FAST persistent path)
   double2 v[SUB];
+  if (FAST && vpre) {
 #pragma unroll
-  for (int r = 0; r < SUB; ++r)
-    v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
+    for (int r = 0; r < SUB; ++r) v[r] = vpre[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < SUB; ++r)
+      v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
+  }
 
   // 2. factor chain from the exact sub-chunk pivot (dpttrf order, fast rcp)
-  if (has) {
+  if (has && do_factors) {
     if (!FAST && m == 0) {
 #pragma unroll
       for (int r = 0; r < SUB; ++r)
         if (r <= re) sm[(s * SUB + r) * DPW + dl] = make_double2(A.L0[ib + r], A.dinv0[ib + r]);
     } else {
-      double d = A.d0s[(size_t)(ib / SUB) * n + m];
+      // Leading-minor form of the pivot recurrence: with q_{-1} = 1 and
+      // q_0 = d(k0) (exact dpttrf pivot), q_j = diag q_{j-1} - e^2 q_{j-2}
+      // gives d(k0+j) = q_j / q_{j-1}; e^2 = B(i) B(k) is exact
+      // (B(j) = (j+1)(N-1-j)), so the loop-carried chain is one FMA per row
+      // and the reciprocals are off the chain.  |q| <= d_max^16 < 1e150.
       int k = ib + rs - m;
+      double qm1 = 1.0, q0 = A.d0s[(size_t)(ib / SUB) * n + m];
       double dg = block_diag(n, m, k);
       double inc = 2.0 * (double)(n - 2 - 2 * k - m);  // diag(k+1) - diag(k), exact
       const double* sqi = A.sqB + ib + rs;
       const double* sqk = A.sqB + k;
+      const double* bqi = A.Bq + ib + rs;
+      const double* bqk = A.Bq + k;
 #pragma unroll
       for (int r = 0; r < SUB; ++r) {
         if (ROW_OK(r)) {
-          const double di = fast_rcp(d);
+          const int rr = r - rs;
+          const double rq = fast_rcp(q0);
+          const double di = qm1 * rq;  // 1 / d_k
           double L = 0.0;
-          if (FAST || k + (r - rs) < len - 1) {
-            const double e = -sqi[r - rs] * sqk[r - rs];
+          if (FAST || k + rr < len - 1) {
+            const double e = -sqi[rr] * sqk[rr];
             L = e * di;
+            const double e2 = bqi[rr] * bqk[rr];
             dg += inc;
             inc -= 4.0;
-            d = fma(-L, e, dg);
+            const double q1 = fma(dg, q0, -e2 * qm1);
+            qm1 = q0;
+            q0 = q1;
           }
           sm[(s * SUB + r) * DPW + dl] = make_double2(L, di);
         }
@@ -293,13 +322,12 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   }
   // 4. compose the 4 segment maps of each diagonal (lanes dl, dl+8, dl+16, dl+24)
   AffW inc = fm;
-  {
-    AffW o = aff_shfl(inc, max(lane - 8, 0));
-    if (s >= 1) inc = aff_compose(o, inc);
-    o = aff_shfl(inc, max(lane - 16, 0));
-    if (s >= 2) inc = aff_compose(o, inc);
+#pragma unroll
+  for (int step = 1; step < LPD; step <<= 1) {
+    AffW o = aff_shfl(inc, max(lane - step * DPW, 0));
+    if (s >= step) inc = aff_compose(o, inc);
   }
-  AffW exm = aff_shfl(inc, max(lane - 8, 0));
+  AffW exm = aff_shfl(inc, max(lane - DPW, 0));
   if (s == 0) {
     exm.a = make_double2(0.0, 0.0);
     exm.g = 1.0;
@@ -341,13 +369,12 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   }
   // 7. reverse composition over segments: x_in(s) = x_start(s+1)
   AffW rinc = bm;
-  {
-    AffW o = aff_shfl(rinc, min(lane + 8, 31));
-    if (s <= 2) rinc = aff_compose(o, rinc);
-    o = aff_shfl(rinc, min(lane + 16, 31));
-    if (s <= 1) rinc = aff_compose(o, rinc);
+#pragma unroll
+  for (int step = 1; step < LPD; step <<= 1) {
+    AffW o = aff_shfl(rinc, min(lane + step * DPW, 31));
+    if (s + step <= LPD - 1) rinc = aff_compose(o, rinc);
   }
-  AffW rex = aff_shfl(rinc, min(lane + 8, 31));
+  AffW rex = aff_shfl(rinc, min(lane + DPW, 31));
   if (s == LPD - 1) {
     rex.a = make_double2(0.0, 0.0);
     rex.g = 1.0;
@@ -370,7 +397,7 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
         }
       }
 #pragma unroll
-      for (int off = 8; off < 32; off <<= 1) {
+      for (int off = DPW; off < 32; off <<= 1) {
         tb.x += __shfl_xor_sync(0xffffffff, tb.x, off);
         tb.y += __shfl_xor_sync(0xffffffff, tb.y, off);
         xs.x += __shfl_xor_sync(0xffffffff, xs.x, off);
@@ -406,36 +433,43 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   }
 #undef ROW_OK
   __syncwarp();
-  // stage x for the transposed store (reuse the factor tile)
+  // stage x for the transposed store (reuse the factor tile unless the
+  // caller keeps the factors for further right-hand sides)
+  double2* xs_buf = xstage ? xstage : sm;
 #pragma unroll
-  for (int r = 0; r < SUB; ++r) sm[(s * SUB + r) * DPW + dl] = v[r];
+  for (int r = 0; r < SUB; ++r) xs_buf[(s * SUB + r) * DPW + dl] = v[r];
   __syncwarp();
   // strict upper by skew reflection: P[i-m][i] = conj(x) (laplacian.py:306-316).
   // Output row j = i0 - m0 + t holds columns i0 + t + u, u = 0..7 (one 128 B
   // run); each instruction writes 4 such rows.
-  const int u = lane & 7;
+  const int u = lane % DPW;
   const int mm = m0 + u;
   const bool uok = mm >= 1 && mm < n;
-  for (int t0 = -(DPW - 1); t0 < SR; t0 += 4) {
-    const int tt = t0 + (lane >> 3);
+  for (int t0 = -(DPW - 1); t0 < SR; t0 += 32 / DPW) {
+    const int tt = t0 + lane / DPW;
     const int r = tt + u;  // row in chunk of diagonal m0 + u
     const int i = i0 + r;
     if (uok && tt < SR && r >= 0 && r < SR && i >= mm && i < n) {
-      const double2 xv = sm[r * DPW + u];
+      const double2 xv = xs_buf[r * DPW + u];
       st2(p + ((size_t)(i - mm) * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
     }
   }
 }
 
 // Interior tiles: chunks c < Cf (the chunk ends before row n-2), groups
-// g = 1 .. 8c-1 (all 8 diagonals start before the chunk).  Count per chunk
-// 8c-1, prefix (c-1)(4c-1).
+// g = 1 .. GPC*c-1 with GPC = SR/DPW groups per chunk height (all DPW
+// diagonals start before the chunk).  Count per chunk GPC*c-1, prefix
+// P(c) = GPC*c(c-1)/2 - (c-1) for c >= 1.
+constexpr int GPC = SR / DPW;
+__host__ __device__ __forceinline__ long long fast_prefix(long long c) {
+  return c >= 1 ? (long long)GPC * c * (c - 1) / 2 - (c - 1) : 0;
+}
 __device__ __forceinline__ void fast_tile_coords(int t, int& c, int& g) {
-  int q = (int)(sqrt((double)t * 0.25)) + 1;
-  while (q > 1 && (q - 1) * (4 * q - 1) > t) --q;
-  while (q * (4 * q + 3) <= t) ++q;
+  int q = (int)(sqrt(2.0 * (double)t / GPC)) + 1;
+  while (q > 1 && fast_prefix(q) > t) --q;
+  while (fast_prefix(q + 1) <= t) ++q;
   c = q;
-  g = 1 + t - (q - 1) * (4 * q - 1);
+  g = 1 + (int)(t - fast_prefix(q));
 }
 
 static int fast_chunks(int n) {
@@ -444,12 +478,69 @@ static int fast_chunks(int n) {
   while ((cf + 1) * SR < n - 1) ++cf;
   return cf;
 }
-static int fast_ntiles(int cf) { return cf >= 1 ? (cf - 1) * (4 * cf - 1) : 0; }
+static int fast_ntiles(int cf) { return (int)fast_prefix(cf); }
+
+// Persistent interior-tile kernel: each warp walks tiles id = gw, gw + nw,
+// ...; the next tile's 64 x 8 sheared block (8 KB) is fetched by TMA from a
+// 3D tensor map over W with row stride ld+1 while the current one is swept.
+constexpr int FAST_SMEM_PER_WARP = 2 * SR * DPW * (int)sizeof(double2);  // factors + staged tile
 
 template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_FAST_MINB) k_solve_fast(SolveArgs A) {
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_FAST_MINB)
+    k_solve_fast(const __grid_constant__ SolveArgs A, const __grid_constant__ CUtensorMap tw, int total) {
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  // TMA destinations need 128 B alignment: align the dynamic base by hand
+  unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 127) & ~(uintptr_t)127);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SOLVE_WARPS * FAST_SMEM_PER_WARP);
+  // independent of the boundary-tile launch of the same pass: let it start
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* sm = reinterpret_cast<double2*>(smem_raw + warp * FAST_SMEM_PER_WARP);
+  double2* vbuf = sm + SR * DPW;
+  if (lane == 0) {
+    mbar_init(&bar[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int nw = gridDim.x * SOLVE_WARPS;
+  int id = blockIdx.x * SOLVE_WARPS + warp;
+  const int n = A.n;
+  auto issue = [&](int tid) {
+    const int bb = tid / A.ntiles;
+    int c, g;
+    fast_tile_coords(tid - bb * A.ntiles, c, g);
+    mbar_arrive_expect_tx(&bar[warp], SR * DPW * 16);
+    tma_3d(vbuf, &tw, 2 * (n - DPW - g * DPW), c * SR, bb, &bar[warp]);
+  };
+  if (id < total && lane == 0) issue(id);
+  uint32_t phase = 0;
+  while (id < total) {
+    const int b = id / A.ntiles;
+    int c, g;
+    fast_tile_coords(id - b * A.ntiles, c, g);
+    mbar_wait(&bar[warp], phase);
+    phase ^= 1;
+    double2 vv[SUB];
+    {
+      const int dl = lane % DPW, s = lane / DPW;
+#pragma unroll
+      for (int r = 0; r < SUB; ++r) vv[r] = vbuf[(s * SUB + r) * DPW + (DPW - 1 - dl)];
+    }
+    // all lanes' reads of vbuf precede the next async-proxy write into it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    const int nid = id + nw;
+    if (nid < total && lane == 0) issue(nid);  // refill while this tile is swept
+    tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane,
+                           sm, vv);
+    id = nid;
+  }
+}
+
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_DIRECT_MINB) k_solve_fast_direct(SolveArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // independent of the generic launch of the same pass: let it start now
   asm volatile("griddepcontrol.launch_dependents;");
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -459,6 +550,26 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_FAST_MINB) k_solve_fas
   fast_tile_coords(t, c, g);
   double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
   tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane, sm);
+}
+
+// Batched interior tiles: the LDL^T factors of a tile do not depend on the
+// right-hand side, so they are generated once and reused for every matrix
+// of the batch (config 2: 8 matrices share each factor chain).
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_DIRECT_MINB) k_solve_fast_batch(SolveArgs A, int batch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * SOLVE_WARPS + warp;
+  if (t >= A.ntiles) return;
+  int c, g;
+  fast_tile_coords(t, c, g);
+  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW * (FINAL ? 2 : 1);
+  double2* xstage = FINAL ? sm + SR * DPW : nullptr;
+  for (int b = 0; b < batch; ++b) {
+    tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane, sm,
+                           nullptr, b == 0, xstage);
+  }
 }
 
 template <bool FINAL>
@@ -758,7 +869,7 @@ static std::vector<int2> generic_tiles(int n) {
   for (int c = 0; c < C; ++c) {
     const int gmax = std::min(Gt - 1, (c * SR + SR - 1) / DPW);
     for (int g = 0; g <= gmax; ++g) {
-      const bool fast = (c < cf) && g >= 1 && g <= 8 * c - 1;
+      const bool fast = (c < cf) && g >= 1 && g <= GPC * c - 1;
       if (!fast) v.push_back(make_int2(c, g));
     }
   }
@@ -768,7 +879,7 @@ static std::vector<int2> generic_tiles(int n) {
 static size_t op_bytes(int n, int C) {
   const size_t nsub = (size_t)(n + SUB - 1) / SUB;
   const size_t ngen = generic_tiles(n).size();
-  return sizeof(double) * ((size_t)3 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
+  return sizeof(double) * ((size_t)4 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
          sizeof(int2) * ngen + 512;
 }
 
@@ -791,6 +902,8 @@ int op_create(int n, int device, zt_operator** out) {
   }
   double* q = reinterpret_cast<double*>(op->block);
   op->sqB = q;
+  q += n;
+  op->Bq = q;
   q += n;
   op->L0 = q;
   q += n;
@@ -815,18 +928,41 @@ int op_create(int n, int device, zt_operator** out) {
     op->ngen = (int)gt.size();
     cudaMemcpy(op->gen_tiles, gt.data(), sizeof(int2) * gt.size(), cudaMemcpyHostToDevice);
   }
-  k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB);
+  k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB, op->Bq);
   ZT_LAUNCHED();
   k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lin, op->G, op->H, op->K, op->L0,
                                         op->dinv0, op->m0x);
   ZT_LAUNCHED();
   int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   int asmem = SOLVE_WARPS * TR * 32 * (int)sizeof(double2);
-  cudaFuncSetAttribute(k_solve_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
+  cudaFuncSetAttribute(k_solve_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
   cudaFuncSetAttribute(k_solve_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast_batch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_fast_batch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * smem);
+  {
+    const char* e = getenv("ZT_SOLVE_FAST");
+    op->solve_tma = e && std::string(e) == "tma";
+    op->solve_amortize = e && std::string(e) == "batch";
+  }
   cudaFuncSetAttribute(k_solve_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+  {
+    const char* e = getenv("ZT_SOLVE_STREAMS");
+    op->nside = e ? std::max(1, std::min(8, atoi(e))) : 1;
+    for (int q = 0; q < op->nside; ++q) cudaStreamCreateWithFlags(&op->side[q], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming);
+    for (int q = 0; q < op->nside; ++q) cudaEventCreateWithFlags(&op->join[q], cudaEventDisableTiming);
+  }
+  {
+    int nb = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_fast<true>, SOLVE_WARPS * 32,
+                                                  SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    op->fast_blocks = std::max(1, nb) * std::max(1, sms);
+  }
   e = cudaDeviceSynchronize();
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
@@ -840,6 +976,11 @@ int op_create(int n, int device, zt_operator** out) {
 
 int op_destroy(zt_operator* op) {
   if (!op) return ZT_OK;
+  for (int q = 0; q < op->nside; ++q) {
+    cudaStreamDestroy(op->side[q]);
+    cudaEventDestroy(op->join[q]);
+  }
+  if (op->fork) cudaEventDestroy(op->fork);
   cudaFree(op->block);
   delete op;
   return ZT_OK;
@@ -847,7 +988,8 @@ int op_destroy(zt_operator* op) {
 
 size_t solve_workspace_bytes(int n, int batch) {
   const int C = (n + SR - 1) / SR;
-  return (size_t)batch * (2 * (size_t)C * n + 2 * (size_t)C + 2) * sizeof(double2) + 256;
+  const size_t one = ((2 * (size_t)C * n + 2 * (size_t)C + 2) * sizeof(double2) + 511) & ~(size_t)255;
+  return one * batch;
 }
 
 // Launch a generic-tile kernel; with `pdl` it may start while the preceding
@@ -869,8 +1011,9 @@ static cudaError_t launch_pdl(const void* fn, dim3 grid, int smem, cudaStream_t 
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
-                 int64_t sp, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
+static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p,
+                            int64_t ldp, int64_t sp, int batch, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
   const int n = op->n, C = op->C;
   if (ws_bytes < solve_workspace_bytes(n, batch)) return fail(ZT_ENOMEM, "solve workspace too small");
   SolveArgs A;
@@ -878,6 +1021,7 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
   A.C = C;
   A.ntiles = solve_ntiles(C);
   A.sqB = op->sqB;
+  A.Bq = op->Bq;
   A.d0s = op->d0;
   A.lin = op->lin;
   A.L0 = op->L0;
@@ -894,11 +1038,29 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
   A.m0mg = A.m0acc + (size_t)batch * C * 2;
   const int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   A.ntiles = fast_ntiles(fast_chunks(n));
-  const int tf = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
+  const int total = A.ntiles * batch;
+  const int tf = total > 0 ? std::min((total + SOLVE_WARPS - 1) / SOLVE_WARPS, op->fast_blocks) : 0;
   const int tg = (op->ngen + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  // pass 1: interior tiles, then (programmatically overlapped) boundary tiles
+  CUtensorMap tw;
   if (tf > 0) {
-    k_solve_fast<false><<<dim3(tf, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+    // sheared 3D view of W: element (x, i, b) = W_b[i][i - (N-1-x/2)], row stride ld+1
+    if ((reinterpret_cast<uintptr_t>(w) & 15) || ((ldw + 1) * 16) % 16) return fail(ZT_EINVAL, "solve: W must be 16B aligned");
+    cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)n, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(ldw + 1) * 16, (cuuint64_t)std::max<int64_t>(sw, 1) * 16};
+    cuuint32_t box[3] = {2 * DPW, SR, 1};
+    int rc = encode_tiled_f64(&tw, 3, w - 2 * (int64_t)(n - 1), dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+  }
+  const int fsm = SOLVE_WARPS * FAST_SMEM_PER_WARP + 256;
+  // pass 1: interior tiles, then (programmatically overlapped) boundary tiles
+  const int td = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
+  if (tf > 0) {
+    if (op->solve_tma)
+      k_solve_fast<false><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
+    else if (batch > 1 && op->solve_amortize)
+      k_solve_fast_batch<false><<<td, SOLVE_WARPS * 32, smem, st>>>(A, batch);
+    else
+      k_solve_fast_direct<false><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
     ZT_LAUNCHED();
   }
   ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<false>), dim3(tg, batch), smem, st,
@@ -908,13 +1070,43 @@ int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, doub
                                                           A.xst, A.m0acc, A.m0mg);
   ZT_LAUNCHED();
   if (tf > 0) {
-    k_solve_fast<true><<<dim3(tf, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+    if (op->solve_tma)
+      k_solve_fast<true><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
+    else if (batch > 1 && op->solve_amortize)
+      k_solve_fast_batch<true><<<td, SOLVE_WARPS * 32, 2 * smem, st>>>(A, batch);
+    else
+      k_solve_fast_direct<true><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
     ZT_LAUNCHED();
   }
   ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<true>), dim3(tg, batch), smem, st,
                            A, op->gen_tiles, op->ngen, tf > 0));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+// Batched solve: matrices are pipelined over the operator's side streams
+// (fork/join with events, graph-capturable) so that one matrix's
+// compute-heavy pass 1 overlaps another's bandwidth-heavy pass 3.
+int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
+                 int64_t sp, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int S = op->nside;
+  if (batch <= 1 || S <= 1)
+    return stream_solve_one(op, w, ldw, sw, p, ldp, sp, batch, ws, ws_bytes, st);
+  const size_t per = solve_workspace_bytes(op->n, 1);
+  if (ws_bytes < per * batch) return fail(ZT_ENOMEM, "solve workspace too small");
+  ZT_CUDA_CHECK(cudaEventRecord(op->fork, st));
+  for (int q = 0; q < S && q < batch; ++q) ZT_CUDA_CHECK(cudaStreamWaitEvent(op->side[q], op->fork, 0));
+  for (int b = 0; b < batch; ++b) {
+    cudaStream_t ss = op->side[b % S];
+    int rc = stream_solve_one(op, w + (size_t)b * sw * 2, ldw, 0, p + (size_t)b * sp * 2, ldp, 0, 1,
+                              static_cast<char*>(ws) + per * b, per, ss);
+    if (rc) return rc;
+  }
+  for (int q = 0; q < S && q < batch; ++q) {
+    ZT_CUDA_CHECK(cudaEventRecord(op->join[q], op->side[q]));
+    ZT_CUDA_CHECK(cudaStreamWaitEvent(st, op->join[q], 0));
+  }
   return ZT_OK;
 }
 
