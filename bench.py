@@ -18,8 +18,9 @@ ours:       device-resident steps through the C ABI (zt_midpoint_step);
 reference:  the CPU oracle port (restating the reference's numpy/OpenBLAS
             path; the reference itself is Python and is not on the GPU box)
             timed on all host cores, same config/metric.
-Multi-GPU (torchrun): each rank runs an independent replica ("replicas");
-`value` = total steps/s over ranks, time = max over ranks.
+Multi-GPU (torchrun): the row-block sharded step (sharded.py) of the same
+workload, NCCL collectives, strong scaling, time = max over ranks
+(`--replicas` runs independent replicas instead; `--sharded --n 4096` is cfg 5).
 """
 
 from __future__ import annotations
@@ -185,6 +186,110 @@ def load_fp64_peak():
         pass
     return best or 37.2, ("measured: DMMA.8x8x4 issue-rate microbenchmark, profiles/r01_fp64_peaks.jsonl"
                           if best else "nominal 148 SM x 128 flop/clk x 1.965 GHz")
+
+
+def run_sharded(args):
+    """Row-block sharded step (paper_2206_05466_b200/sharded.py): the same cfg
+    workload split over the ranks (strong scaling), NCCL collectives."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if "RANK" not in os.environ:  # plain `python bench.py --sharded`: one-rank group
+        import socket
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(s.getsockname()[1]))
+        s.close()
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_2206_05466_b200 as zt
+    from paper_2206_05466_b200 import _lib
+    from paper_2206_05466_b200.sharded import DeviceBackend, ShardedStepper
+
+    n = args.n
+    h = H if n == N else 0.0025
+    be = DeviceBackend(n, dev)
+    st = ShardedStepper(n, be, force_collectives=True)
+    r = torch.from_numpy(cfg4_initial_numpy(n)).to(dev)
+    w0 = zt.solve_stream(r, be.op)
+    w0 = w0 / torch.linalg.norm(w0)
+    rows = w0[st.r0:st.r0 + st.m].contiguous()
+    for _ in range(args.warmup):
+        rows, k, _ = st.midpoint_step(rows, h, TOL, MAX_ITER)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.lib.zt_launch_count()
+    iters = []
+    dist.barrier(device_ids=[local])
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            rows, k, _ = st.midpoint_step(rows, h, TOL, MAX_ITER)
+            iters.append(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier(device_ids=[local])
+    launches = _lib.lib.zt_launch_count() - launches0
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = args.steps / (ms / 1e3)
+    # e2e: each rank's row block from pinned host memory in, result out, every step
+    host_in = torch.empty_like(rows, device="cpu").pin_memory()
+    host_in.copy_(rows.cpu())
+    host_out = torch.empty_like(host_in).pin_memory()
+    e2e_steps = max(1, min(args.steps, 10))
+    dist.barrier(device_ids=[local])
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        rd = host_in.to(dev, non_blocking=True)
+        rd, _, _ = st.midpoint_step(rd, h, TOL, MAX_ITER)
+        host_out.copy_(rd, non_blocking=True)
+        stream.synchronize()
+        host_in, host_out = host_out, host_in
+    f1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = e2e_steps / (float(t.item()) / 1e3)
+    peak, peak_src = load_fp64_peak()
+    kbar = statistics.mean(iters)
+    alg = 16.0 * n**3 * (kbar + 1)
+    achieved = alg / (ms_per_step * 1e-3) / 1e12
+    line = {
+        "metric": METRIC if n == N else f"isospectral time-steps/sec at N={n} complex128",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"row-block sharded midpoint step, N={n}, h={h}", "N": n, "h": h,
+                   "iterations_per_step": sorted(set(iters)), "parallelism": f"rowblock{world}",
+                   "collectives": "NCCL all_gather(X) + all_to_all(a tiles) + all_reduce(max residual) per update",
+                   "l2": "no flush: per-step working set > 126 MB L2"},
+        "roofline": {"bound": "tensor", "kernel": "whole sharded step (all ranks)", "achieved": achieved,
+                     "peak": peak * world, "unit": "TFLOP/s", "frac": achieved / (peak * world),
+                     "traffic": None, "peak_source": peak_src,
+                     "note": "algorithmic 16 N^3 (k+1) flop per step; GEMM-2 runs full per rank (no lower-tile saving)"},
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 16 * n * n,
+                "d2h_bytes_per_step": 16 * n * n, "steps": e2e_steps,
+                "api": "ShardedStepper.midpoint_step with pinned-host row blocks in/out every step"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -354,11 +459,19 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="row-block sharded step over the ranks (default when WORLD_SIZE > 1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with WORLD_SIZE > 1: independent replicas per rank instead of sharding")
+    ap.add_argument("--n", type=int, default=N, help="matrix size for --sharded (cfg 5: 4096, 8192)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
+    elif args.sharded or (world > 1 and not args.replicas):
+        run_sharded(args)
     else:
         run_ours(args)
 

@@ -92,6 +92,21 @@ int zt_residuals_ws(int n, const double* w, int64_t ldw, double* out_dev, void* 
 int zt_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
              int64_t ldc, int algo, void* stream);
 
+/* Rectangular C (m x n) = A (m x k) @ B (k x n), row-major, 16B-aligned
+ * operands (the local products of the sharded step). */
+int zt_zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
+                  double* c, int64_t ldc, int algo, void* stream);
+
+/* Row-block update of the sharded step (rows R of the N x N update held
+ * by one rank): b = a_R @ P (a_R: m x n, P: n x n); out = base +
+ * hh (a_R - ah_R) + qq b where ah_R = rows R of a^H; *resid_dev (device
+ * uint64, zeroed by the caller) receives the bit pattern of
+ * max|out - xprev| (NaN-propagating).  All row blocks use leading dim ld. */
+int zt_zgemm_update_rows(int m, int n, const double* a_rows, const double* p,
+                         const double* ah_rows, const double* base, const double* xprev,
+                         double* out, int64_t ld, double hh, double qq,
+                         unsigned long long* resid_dev, void* stream);
+
 /* Workspace for zt_fixed_point / zt_midpoint_step at size n (bytes). */
 size_t zt_step_workspace_bytes(int n);
 

@@ -36,6 +36,11 @@ SIGNATURES = {
     "zt_residuals_ws": (_c_int, [_c_int, _vp, _c_i64, _vp, _vp, _vp]),
     "zt_zgemm": (_c_int, [_c_int, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_int, _vp]),
     "zt_step_workspace_bytes": (_c_sz, [_c_int]),
+    "zt_zgemm_rect": (_c_int, [_c_int, _c_int, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_int, _vp]),
+    "zt_zgemm_update_rows": (
+        _c_int,
+        [_c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_dbl, _vp, _vp],
+    ),
     "zt_fixed_point": (_c_int, [_vp, _vp, _vp, _c_dbl, _c_dbl, _c_int, _vp, _c_sz, _PI, _PD, _vp]),
     "zt_midpoint_step": (
         _c_int,

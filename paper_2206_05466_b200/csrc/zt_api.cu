@@ -63,6 +63,11 @@ int zgemm_update(int n, const double* amat, const double* p, const double* base,
                  const double* wn, double* out, int64_t ld, double hh, double qq,
                  unsigned long long* resid, unsigned long long* cons, int algo, cudaStream_t st);
 int skew_diff(int n, const double* a, double* c, cudaStream_t st);
+int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+               int64_t ldc, int algo, cudaStream_t st);
+int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const double* ah_rows,
+                      const double* base, const double* xprev, double* out, int64_t ld, double hh,
+                      double qq, unsigned long long* resid, int algo, cudaStream_t st);
 
 static int g_algo = 0;  // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
 
@@ -316,6 +321,21 @@ int zt_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
              int algo, void* stream) {
   if (n < 1 || !a || !b || !c) return fail(ZT_EINVAL, "zt_zgemm: bad argument");
   return zgemm(n, a, lda, b, ldb, c, ldc, algo, (cudaStream_t)stream);
+}
+
+int zt_zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                  int64_t ldc, int algo, void* stream) {
+  if (!a || !b || !c) return fail(ZT_EINVAL, "zt_zgemm_rect: bad argument");
+  return zgemm_rect(m, n, k, a, lda, b, ldb, c, ldc, algo, (cudaStream_t)stream);
+}
+
+int zt_zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const double* ah_rows,
+                         const double* base, const double* xprev, double* out, int64_t ld, double hh,
+                         double qq, unsigned long long* resid_dev, void* stream) {
+  if (m < 1 || n < 1 || !a_rows || !p || !ah_rows || !base || !out)
+    return fail(ZT_EINVAL, "zt_zgemm_update_rows: bad argument");
+  return zgemm_update_rows(m, n, a_rows, p, ah_rows, base, xprev, out, ld, hh, qq, resid_dev, g_algo,
+                           (cudaStream_t)stream);
 }
 
 size_t zt_step_workspace_bytes(int n) { return ws_layout(n, nullptr, nullptr); }

@@ -51,10 +51,15 @@ constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024 + 64;
 
 enum { ALGO_3M = 0, ALGO_4M = 1, ALGO_3M_NOSUM = 2 /* timing experiment only: wrong results */ };
-enum { EPI_STORE = 0, EPI_UPDATE = 1 };
+enum {
+  EPI_STORE = 0,   // C = A B
+  EPI_UPDATE = 1,  // square, lower tiles + mirror: new = base + hh (a - a^H) + qq b
+  EPI_ROWS = 2     // row block (sharded step): new = base + hh (a - ah) + qq b, ah given
+};
 
 struct GemmArgs {
-  int n;
+  int n;        // square size (EPI_UPDATE) / output columns
+  int m, k;     // rows of A / C, inner dimension (rectangular EPI_STORE / EPI_ROWS)
   CUtensorMap tma_a;  // 2D map of A (and "a" operand) as doubles, box 16 x BM
   CUtensorMap tma_b;  // 2D map of B, box 16 x BK
   const double* a;  // row-major n x n complex, lda
@@ -65,6 +70,7 @@ struct GemmArgs {
   int64_t ldc;
   // EPI_UPDATE
   const double* amat;  // the left operand "a" again (for a^H in the epilogue)
+  const double* ah;    // EPI_ROWS: rows of a^H matching the output rows
   const double* base;  // W_n (iterate) or W~ (final)
   const double* xprev; // previous iterate for the residual (may alias out), or null
   const double* wn;    // for consistency (final step), or null
@@ -118,13 +124,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
   uint64_t* empty = full + STAGES;
   __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
 
-  const int n = g.n;
+  const int n = g.n;           // output columns
+  const int mrows = g.m;       // output rows
   const int T = (n + BM - 1) / BM;
   int I, J;
-  tile_of(blockIdx.x, EPI == EPI_UPDATE, T, I, J);
+  if (EPI == EPI_UPDATE) {
+    tile_of(blockIdx.x, true, T, I, J);
+  } else {
+    // grouped rasterisation over a (ceil(m/64) x ceil(n/64)) tile grid
+    const int Tm = (mrows + BM - 1) / BM;
+    const int G = 8, per = G * T, t = blockIdx.x;
+    const int grp = t / per, first = grp * G, rows = min(G, Tm - first), r = t - grp * per;
+    I = first + r % rows;
+    J = r / rows;
+  }
   const int row0 = I * BM, col0 = J * BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KT = (n + BK - 1) / BK;
+  const int KT = (g.k + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -242,9 +258,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
         }
         const int gi = row0 + wm * 32 + i * 8 + fr;
         const int gj = col0 + wn * 16 + j * 8 + fk * 2 + e;
-        if (gi >= n || gj >= n) continue;
+        if (gi >= mrows || gj >= n) continue;
         if (EPI == EPI_STORE) {
           st2(g.c + ((size_t)gi * g.ldc + gj) * 2, make_double2(cr, ci));
+        } else if (EPI == EPI_ROWS) {
+          const size_t o = ((size_t)gi * g.ld + gj) * 2;
+          const double2 aij = ld2_plain(g.amat + o), ahij = ld2_plain(g.ah + o);
+          const double2 dij = csub(aij, ahij);  // (a - a^H) on this row block
+          const double2 base = ld2_plain(g.base + o);
+          const double2 nw = cadd(cadd(base, rmul(g.hh, dij)), rmul(g.qq, make_double2(cr, ci)));
+          if (g.xprev) {
+            const double2 xp = ld2_plain(g.xprev + o);
+            rmax = nanmax(rmax, hypot(nw.x - xp.x, nw.y - xp.y));
+          }
+          st2(g.out + o, nw);
         } else {
           const size_t oij = ((size_t)gi * g.ld + gj) * 2, oji = ((size_t)gj * g.ld + gi) * 2;
           const double2 aij = ld2_plain(g.amat + oij), aji = ld2_plain(g.amat + oji);
@@ -290,7 +317,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
       }
     }
   }
-  if (EPI == EPI_UPDATE) {
+  if (EPI != EPI_STORE) {
     // NaN-propagating max: compare on the (sign-cleared) bit pattern
     unsigned long long rb = (unsigned long long)__double_as_longlong(fabs(rmax));
     unsigned long long cb = (unsigned long long)__double_as_longlong(fabs(cmax));
@@ -338,25 +365,25 @@ __global__ void k_skew_diff(int n, const double* __restrict__ a, double* __restr
   }
 }
 
-static int make_map(CUtensorMap* map, const double* base, int n, int64_t ld, int box_rows) {
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || ld < n) return fail(ZT_EINVAL, "zgemm: operand must be 16B aligned with ld >= n");
-  cuuint64_t dims[2] = {(cuuint64_t)2 * n, (cuuint64_t)n};
+static int make_map(CUtensorMap* map, const double* base, int rows, int cols, int64_t ld, int box_rows) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ld < cols) return fail(ZT_EINVAL, "zgemm: operand must be 16B aligned with ld >= cols");
+  cuuint64_t dims[2] = {(cuuint64_t)2 * cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 16};
   cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
   return encode_tiled_f64(map, 2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-static bool g_attr[16][8];
+static bool g_attr[16][16];
 
 template <int ALGO, int EPI>
 static int launch(GemmArgs& g, int ntiles, cudaStream_t st) {
-  int rc = make_map(&g.tma_a, g.a, g.n, g.lda, BM);
+  int rc = make_map(&g.tma_a, g.a, g.m, g.k, g.lda, BM);
   if (rc) return rc;
-  rc = make_map(&g.tma_b, g.b, g.n, g.ldb, BK);
+  rc = make_map(&g.tma_b, g.b, g.k, g.n, g.ldb, BK);
   if (rc) return rc;
   int dev;
   cudaGetDevice(&dev);
-  const int slot = ALGO * 2 + EPI;
+  const int slot = ALGO * 3 + EPI;
   if (dev < 16 && !g_attr[dev][slot]) {
     ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zgemm<ALGO, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
     g_attr[dev][slot] = true;
@@ -372,6 +399,8 @@ int zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, dou
   if (n < 1) return fail(ZT_EINVAL, "zgemm: n must be positive");
   GemmArgs g{};
   g.n = n;
+  g.m = n;
+  g.k = n;
   g.a = a;
   g.lda = lda;
   g.b = b;
@@ -390,6 +419,8 @@ int zgemm_update(int n, const double* amat, const double* p, const double* base,
                  unsigned long long* resid, unsigned long long* cons, int algo, cudaStream_t st) {
   GemmArgs g{};
   g.n = n;
+  g.m = n;
+  g.k = n;
   g.a = amat;
   g.lda = ld;
   g.b = p;
@@ -408,6 +439,52 @@ int zgemm_update(int n, const double* amat, const double* p, const double* base,
   const int nt = T * (T + 1) / 2;
   if (algo == ALGO_4M) return launch<ALGO_4M, EPI_UPDATE>(g, nt, st);
   return launch<ALGO_3M, EPI_UPDATE>(g, nt, st);
+}
+
+// Rectangular C (m x n) = A (m x k) B (k x n)
+int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+               int64_t ldc, int algo, cudaStream_t st) {
+  if (m < 1 || n < 1 || k < 1) return fail(ZT_EINVAL, "zgemm: sizes must be positive");
+  GemmArgs g{};
+  g.n = n;
+  g.m = m;
+  g.k = k;
+  g.a = a;
+  g.lda = lda;
+  g.b = b;
+  g.ldb = ldb;
+  g.c = c;
+  g.ldc = ldc;
+  const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, nt, st);
+  return launch<ALGO_3M, EPI_STORE>(g, nt, st);
+}
+
+// Row-block update of the sharded step: b = a_R P (m x n, inner n);
+// out = base + hh (a_R - ah_R) + qq b, residual max|out - xprev|.
+int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const double* ah_rows,
+                      const double* base, const double* xprev, double* out, int64_t ld, double hh,
+                      double qq, unsigned long long* resid, int algo, cudaStream_t st) {
+  GemmArgs g{};
+  g.n = n;
+  g.m = m;
+  g.k = n;
+  g.a = a_rows;
+  g.lda = ld;
+  g.b = p;
+  g.ldb = n;
+  g.amat = a_rows;
+  g.ah = ah_rows;
+  g.base = base;
+  g.xprev = xprev;
+  g.out = out;
+  g.ld = ld;
+  g.hh = hh;
+  g.qq = qq;
+  g.resid = resid;
+  const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  if (algo == ALGO_4M) return launch<ALGO_4M, EPI_ROWS>(g, nt, st);
+  return launch<ALGO_3M, EPI_ROWS>(g, nt, st);
 }
 
 int skew_diff(int n, const double* a, double* c, cudaStream_t st) {
