@@ -121,3 +121,42 @@ def test_casimirs_match_oracle(zt):
     w = zo.random_admissible(16, np.random.default_rng(3))
     for k in (2, 5, 9):
         np.testing.assert_allclose(zt.casimirs(dev(w), k), zo.casimirs(w, k), rtol=1e-12, atol=1e-12)
+
+
+def test_cfg4_full_size_steps_vs_oracle(zt):
+    """BASELINE cfg 4 at its full size (N = 2048, h = 0.005): 3 steps against
+    the oracle — identical iteration counts, relF(W) <= 1e-10, Casimir C2/C3
+    and energy drift no larger than the oracle's (floor 1e-13 relative)."""
+    n = 2048
+    w = zo.smooth_initial(n)
+    c0, h0 = zo.casimirs(w, 3), zo.hamiltonian(w)
+    x = dev(w)
+    op = zt.build_operator(n)
+    ref = w
+    for _ in range(3):
+        ref, kr, _ = zo.midpoint_step(ref, 0.005, op=zo.build_operator(n))
+        x, k, _, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, op)
+        assert k == kr
+    got = x.cpu().numpy()
+    assert relf(got, ref) <= 1e-10
+    c_ref, c_gpu = zo.casimirs(ref, 3), zt.casimirs(x, 3)
+    floor = 1e-13
+    for j in (1, 2):
+        assert abs(c_gpu[j] - c0[j]) <= max(abs(c_ref[j] - c0[j]), floor * abs(c0[j]))
+    assert abs(zt.hamiltonian(x) - h0) <= max(abs(zo.hamiltonian(ref) - h0), floor * abs(h0))
+
+
+@pytest.mark.parametrize("n", (2048,))
+def test_long_run_structure_full_size(zt, n):
+    """Size-independent invariants over 20 device steps at N = 2048: skew and
+    trace residuals stay at round-off, C2 (= -||W||_F^2) is conserved."""
+    w = zo.smooth_initial(n)
+    x = dev(w)
+    op = zt.build_operator(n)
+    c2_0 = zt.casimirs(x, 2)[1]
+    for _ in range(20):
+        x, k, _, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, op)
+        assert k == 2
+    assert zt.skewness_residual(x) <= 1e-13
+    assert zt.trace_residual(x) <= 1e-13
+    assert abs(zt.casimirs(x, 2)[1] - c2_0) <= 1e-12 * abs(c2_0)
