@@ -63,13 +63,17 @@ int zgemm_update(int n, const double* amat, const double* p, const double* base,
                  const double* wn, double* out, int64_t ld, double hh, double qq,
                  unsigned long long* resid, unsigned long long* cons, int algo, cudaStream_t st);
 int skew_diff(int n, const double* a, double* c, cudaStream_t st);
+int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
+                  const double* wn, double* out, double hh, double qq, unsigned long long* resid,
+                  unsigned long long* cons, unsigned int* sync, int algo, cudaStream_t st);
 int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                int64_t ldc, int algo, cudaStream_t st);
 int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const double* ah_rows,
                       const double* base, const double* xprev, double* out, int64_t ld, double hh,
                       double qq, unsigned long long* resid, int algo, cudaStream_t st);
 
-static int g_algo = 0;  // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
+static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
+static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
 
 // ---- step workspace layout -------------------------------------------------
 struct StepWS {
@@ -80,6 +84,7 @@ struct StepWS {
   void* resid;   // residual partials
   unsigned long long* flags;  // [0] residual bits, [1] consistency bits
   double* val;   // [0..2] validation residuals
+  unsigned int* sync;  // fused update: tile counter + per-panel completion counts
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -88,6 +93,7 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
   const size_t mat = align_up((size_t)n * n * 16);
   const size_t sb = align_up(solve_workspace_bytes(n, 1));
   const size_t rb = align_up(resid_workspace_bytes(n));
+  const size_t yb = align_up(sizeof(unsigned int) * ((n + 63) / 64 + 1));
   size_t off = 0;
   if (w) {
     w->p = reinterpret_cast<double*>(base + off);
@@ -97,8 +103,9 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
     w->resid = base + off + 2 * mat + sb;
     w->flags = reinterpret_cast<unsigned long long*>(base + off + 2 * mat + sb + rb);
     w->val = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 64);
+    w->sync = reinterpret_cast<unsigned int*>(base + off + 2 * mat + sb + rb + 256);
   }
-  return 2 * mat + sb + rb + 256;
+  return 2 * mat + sb + rb + 256 + yb;
 }
 
 // small pinned host mailbox for the per-iteration read-back
@@ -165,6 +172,13 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
+  if (g_fused) {
+    // GEMM-1 and GEMM-2 in one persistent launch (profiled as "gemm1")
+    rc = zupdate_fused(n, w.p, x, w.a, base, xprev, wn, out, hh, qq, resid, cons, w.sync, g_algo, st);
+    prof_mark(2, st);
+    prof_mark(3, st);
+    return rc;
+  }
   rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
   if (rc) return rc;
   prof_mark(2, st);
@@ -267,6 +281,7 @@ int zt_profile_read(double* ms, int64_t* counts, int reset) {
 int zt_op_create(int n, int device, zt_op_t* op) {
   if (!op) return fail(ZT_EINVAL, "null output");
   if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : 0;
+  if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
   return op_create(n, device, op);
 }
 int zt_op_destroy(zt_op_t op) { return op_destroy(op); }

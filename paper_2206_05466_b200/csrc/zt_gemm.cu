@@ -30,6 +30,8 @@
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
+#include <algorithm>
+#include <cstring>
 #include <string>
 
 #include "zt_tma.cuh"
@@ -48,7 +50,7 @@ constexpr int B_STAGE_BYTES = B_BOXES * B_BOX_BYTES;
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int CONSUMER_WARPS = 8;
 constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
-constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024 + 64;
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 1024 + 64;
 
 enum { ALGO_3M = 0, ALGO_4M = 1, ALGO_3M_NOSUM = 2 /* timing experiment only: wrong results */ };
 enum {
@@ -113,135 +115,79 @@ __device__ __forceinline__ void tile_of(int t, bool lower, int T, int& I, int& J
   }
 }
 
-// ---- kernel ---------------------------------------------------------------
-template <int ALGO, int EPI>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant__ GemmArgs g) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 128B swizzle needs 1024B-aligned boxes
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
-
-  const int n = g.n;           // output columns
-  const int mrows = g.m;       // output rows
-  const int T = (n + BM - 1) / BM;
-  int I, J;
-  if (EPI == EPI_UPDATE) {
-    tile_of(blockIdx.x, true, T, I, J);
-  } else {
-    // grouped rasterisation over a (ceil(m/64) x ceil(n/64)) tile grid
-    const int Tm = (mrows + BM - 1) / BM;
-    const int G = 8, per = G * T, t = blockIdx.x;
-    const int grp = t / per, first = grp * G, rows = min(G, Tm - first), r = t - grp * per;
-    I = first + r % rows;
-    J = r / rows;
+// ---- shared pieces --------------------------------------------------------
+template <int ALGO>
+struct Acc {
+  static constexpr int NACC = (ALGO != ALGO_4M) ? 3 : 2;
+  double v[NACC][4][2][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < NACC; ++q)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v[q][i][j][0] = v[q][i][j][1] = 0.0;
   }
-  const int row0 = I * BM, col0 = J * BN;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KT = (g.k + BK - 1) / BK;
+};
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CONSUMER_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == CONSUMER_WARPS) {
-    // ===== producer: one thread issues 2D TMA boxes into the ring =====
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_a) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_b) : "memory");
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        const uint32_t ph = (kt / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        unsigned char* st = smem + s * STAGE_BYTES;
-        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        const int k0 = kt * BK;
-#pragma unroll
-        for (int j = 0; j < A_BOXES; ++j)
-          tma_2d(st + j * A_BOX_BYTES, &g.tma_a, 2 * (k0 + 8 * j), row0, &full[s]);
-#pragma unroll
-        for (int q = 0; q < B_BOXES; ++q)
-          tma_2d(st + A_STAGE_BYTES + q * B_BOX_BYTES, &g.tma_b, 2 * (col0 + 8 * q), k0, &full[s]);
-      }
-    }
-    return;
-  }
-
-  // ===== consumer warps: 2 (M) x 4 (N), warp tile 32 x 16 complex =====
-  const int wm = warp >> 2, wn = warp & 3;
-  constexpr int NACC = (ALGO != ALGO_4M) ? 3 : 2;
-  double acc[NACC][4][2][2];
-#pragma unroll
-  for (int q = 0; q < NACC; ++q)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
-
+// One BK-deep stage of DMMA for warp (wm, wn) from the swizzled stage `st`.
+template <int ALGO>
+__device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>& A, int wm, int wn, int lane) {
   const int fr = lane >> 2, fk = lane & 3;
   // A fragment row r = wm*32 + i*8 + fr (r & 7 == fr); B fragment column
   // n = wn*16 + j*8 + fr lives in box (wn*2 + j), in-box column fr.
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const unsigned char* st = smem + s * STAGE_BYTES;
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int jb = ks >> 1, par = ks & 1;
-      const int c = 2 * fk + par;           // 16B chunk inside the 128B row
-      const int kr = 8 * jb + c;            // k row of the B stage
-      double2 af[4], bf[2];
+  for (int ks = 0; ks < BK / 4; ++ks) {
+    const int jb = ks >> 1, par = ks & 1;
+    const int c = 2 * fk + par;  // 16B chunk inside the 128B row
+    const int kr = 8 * jb + c;   // k row of the B stage
+    double2 af[4], bf[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = wm * 32 + i * 8 + fr;
+      af[i] = *reinterpret_cast<const double2*>(st + jb * A_BOX_BYTES + r * 128 + ((c ^ fr) << 4));
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * 2 + j) * B_BOX_BYTES + kr * 128 +
+                                                 ((fr ^ (kr & 7)) << 4));
+    if (ALGO != ALGO_4M) {
+      double bsum[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int r = wm * 32 + i * 8 + fr;
-        af[i] = *reinterpret_cast<const double2*>(st + jb * A_BOX_BYTES + r * 128 + ((c ^ fr) << 4));
-      }
+        const double asum = (ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * 2 + j) * B_BOX_BYTES +
-                                                   kr * 128 + ((fr ^ (kr & 7)) << 4));
-      }
-      if (ALGO != ALGO_4M) {
-        double bsum[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double asum = (ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
-            dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].y);
-            dmma(acc[2][i][j][0], acc[2][i][j][1], asum, bsum[j]);
-          }
+        for (int j = 0; j < 2; ++j) {
+          dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
+          dmma(A.v[1][i][j][0], A.v[1][i][j][1], af[i].y, bf[j].y);
+          dmma(A.v[2][i][j][0], A.v[2][i][j][1], asum, bsum[j]);
         }
-      } else {
+      }
+    } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double ain = -af[i].y;
+      for (int i = 0; i < 4; ++i) {
+        const double ain = -af[i].y;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
-            dmma(acc[0][i][j][0], acc[0][i][j][1], ain, bf[j].y);
-            dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].x, bf[j].y);
-            dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].x);
-          }
+        for (int j = 0; j < 2; ++j) {
+          dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
+          dmma(A.v[0][i][j][0], A.v[0][i][j][1], ain, bf[j].y);
+          dmma(A.v[1][i][j][0], A.v[1][i][j][1], af[i].x, bf[j].y);
+          dmma(A.v[1][i][j][0], A.v[1][i][j][1], af[i].y, bf[j].x);
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
+}
 
-  // ===== epilogue =====
-  double rmax = 0.0, cmax = 0.0;
+// Epilogue of one 64 x 64 tile (I, J) for warp (wm, wn).
+template <int ALGO, int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const Acc<ALGO>& A, int I, int J, int wm, int wn,
+                                              int lane, double& rmax, double& cmax) {
+  const int fr = lane >> 2, fk = lane & 3;
+  const int n = g.n, mrows = g.m;
+  const int row0 = I * BM, col0 = J * BN;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
@@ -250,11 +196,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
       for (int e = 0; e < 2; ++e) {
         double cr, ci;
         if (ALGO != ALGO_4M) {
-          cr = acc[0][i][j][e] - acc[1][i][j][e];
-          ci = acc[2][i][j][e] - acc[0][i][j][e] - acc[1][i][j][e];
+          cr = A.v[0][i][j][e] - A.v[1][i][j][e];
+          ci = A.v[2][i][j][e] - A.v[0][i][j][e] - A.v[1][i][j][e];
         } else {
-          cr = acc[0][i][j][e];
-          ci = acc[1][i][j][e];
+          cr = A.v[0][i][j][e];
+          ci = A.v[1][i][j][e];
         }
         const int gi = row0 + wm * 32 + i * 8 + fr;
         const int gj = col0 + wn * 16 + j * 8 + fk * 2 + e;
@@ -317,32 +263,257 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
       }
     }
   }
-  if (EPI != EPI_STORE) {
-    // NaN-propagating max: compare on the (sign-cleared) bit pattern
-    unsigned long long rb = (unsigned long long)__double_as_longlong(fabs(rmax));
-    unsigned long long cb = (unsigned long long)__double_as_longlong(fabs(cmax));
-    if (rmax != rmax) rb = 0x7ff8000000000000ull;
-    if (cmax != cmax) cb = 0x7ff8000000000000ull;
+}
+
+// CTA-wide NaN-propagating max of the consumer warps, one atomic per CTA.
+__device__ __forceinline__ void reduce_max_atomic(double rmax, double cmax, unsigned long long* resid,
+                                                  unsigned long long* cons, unsigned long long* red_res,
+                                                  unsigned long long* red_cons) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long rb = (unsigned long long)__double_as_longlong(fabs(rmax));
+  unsigned long long cb = (unsigned long long)__double_as_longlong(fabs(cmax));
+  if (rmax != rmax) rb = 0x7ff8000000000000ull;
+  if (cmax != cmax) cb = 0x7ff8000000000000ull;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      rb = max(rb, __shfl_xor_sync(0xffffffff, rb, off));
-      cb = max(cb, __shfl_xor_sync(0xffffffff, cb, off));
+  for (int off = 16; off > 0; off >>= 1) {
+    rb = max(rb, __shfl_xor_sync(0xffffffff, rb, off));
+    cb = max(cb, __shfl_xor_sync(0xffffffff, cb, off));
+  }
+  if (lane == 0) {
+    red_res[warp] = rb;
+    red_cons[warp] = cb;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(CONSUMER_WARPS * 32));
+  if (threadIdx.x == 0) {
+    unsigned long long r = 0, c = 0;
+    for (int q = 0; q < CONSUMER_WARPS; ++q) {
+      r = max(r, red_res[q]);
+      c = max(c, red_cons[q]);
     }
+    if (resid) atomicMax(resid, r);
+    if (cons) atomicMax(cons, c);
+  }
+}
+
+__device__ __forceinline__ void producer_load_stage(unsigned char* st, const CUtensorMap* ma, const CUtensorMap* mb,
+                                                    int k0, int row0, int col0, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, STAGE_BYTES);
+#pragma unroll
+  for (int j = 0; j < A_BOXES; ++j) tma_2d(st + j * A_BOX_BYTES, ma, 2 * (k0 + 8 * j), row0, bar);
+#pragma unroll
+  for (int q = 0; q < B_BOXES; ++q) tma_2d(st + A_STAGE_BYTES + q * B_BOX_BYTES, mb, 2 * (col0 + 8 * q), k0, bar);
+}
+
+// ---- one-tile-per-CTA kernel (generic products, config-3 ops, sharded) ----
+template <int ALGO, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant__ GemmArgs g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128B swizzle needs 1024B-aligned boxes
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
+
+  const int n = g.n;
+  const int mrows = g.m;
+  const int T = (n + BM - 1) / BM;
+  int I, J;
+  if (EPI == EPI_UPDATE) {
+    tile_of(blockIdx.x, true, T, I, J);
+  } else {
+    // grouped rasterisation over a (ceil(m/64) x ceil(n/64)) tile grid
+    const int Tm = (mrows + BM - 1) / BM;
+    const int G = 8, per = G * T, t = blockIdx.x;
+    const int grp = t / per, first = grp * G, rows = min(G, Tm - first), r = t - grp * per;
+    I = first + r % rows;
+    J = r / rows;
+  }
+  const int row0 = I * BM, col0 = J * BN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (g.k + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {
+    // ===== producer: one thread issues 2D TMA boxes into the ring =====
     if (lane == 0) {
-      red_res[warp] = rb;
-      red_cons[warp] = cb;
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(CONSUMER_WARPS * 32));
-    if (threadIdx.x == 0) {
-      unsigned long long r = 0, c = 0;
-      for (int q = 0; q < CONSUMER_WARPS; ++q) {
-        r = max(r, red_res[q]);
-        c = max(c, red_cons[q]);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_b) : "memory");
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+        producer_load_stage(smem + s * STAGE_BYTES, &g.tma_a, &g.tma_b, kt * BK, row0, col0, &full[s]);
       }
-      if (g.resid) atomicMax(g.resid, r);
-      if (g.cons) atomicMax(g.cons, c);
+    }
+    return;
+  }
+
+  // ===== consumer warps: 2 (M) x 4 (N), warp tile 32 x 16 complex =====
+  const int wm = warp >> 2, wn = warp & 3;
+  Acc<ALGO> acc;
+  acc.zero();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    consume_stage<ALGO>(smem + s * STAGE_BYTES, acc, wm, wn, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  double rmax = 0.0, cmax = 0.0;
+  epilogue_tile<ALGO, EPI>(g, acc, I, J, wm, wn, lane, rmax, cmax);
+  if (EPI != EPI_STORE) reduce_max_atomic(rmax, cmax, g.resid, g.cons, red_res, red_cons);
+}
+
+// ---- persistent fused update: GEMM-1 tiles then GEMM-2 lower tiles --------
+// Work ids [0, T^2) are GEMM-1 tiles a = P X (grouped rasterisation, store a
+// and count the finished tiles of each row panel); ids [T^2, T^2 + T(T+1)/2)
+// are GEMM-2 lower tiles b = a P with the fused update epilogue, which need
+// a's row panels I (operand) and J (a^H in the epilogue) complete.  Ids are
+// handed out in order by one global atomic, so every dependency of a running
+// tile belongs to a tile already held by a co-resident CTA: no deadlock.
+struct FusedArgs {
+  GemmArgs g2;           // GEMM-2 + update (EPI_UPDATE fields; tma_a = a, tma_b = P)
+  CUtensorMap tma_p;     // GEMM-1 A operand (P)
+  CUtensorMap tma_x;     // GEMM-1 B operand (X)
+  double* a_out;         // GEMM-1 output a
+  unsigned int* next;    // global tile counter (zeroed per launch)
+  unsigned int* done;    // [T] finished GEMM-1 tiles per row panel (zeroed per launch)
+};
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_constant__ FusedArgs f) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tq_full = empty + STAGES;  // [2]
+  uint64_t* tq_empty = tq_full + 2;    // [2]
+  __shared__ int tq[2];
+  __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
+
+  const GemmArgs& g = f.g2;
+  const int n = g.n;
+  const int T = (n + BM - 1) / BM;
+  const int T1 = T * T, total = T1 + T * (T + 1) / 2;
+  const int KT = (n + BK - 1) / BK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tq_full[q], 1);
+      mbar_init(&tq_empty[q], CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {
+    if (lane != 0) return;
+    // ===== producer thread: fetch tile ids, resolve dependencies, stream stages =====
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&f.tma_p) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&f.tma_x) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tma_b) : "memory");
+    unsigned int gs = 0;  // running stage count (ring position)
+    for (int j = 0;; ++j) {
+      const int id = (int)atomicAdd(f.next, 1u);
+      const int slot = j & 1;
+      mbar_wait(&tq_empty[slot], ((j >> 1) & 1) ^ 1);
+      tq[slot] = id < total ? id : -1;
+      mbar_arrive(&tq_full[slot]);
+      if (id >= total) break;
+      int I, J;
+      const CUtensorMap *ma, *mb;
+      if (id < T1) {
+        tile_of(id, false, T, I, J);
+        ma = &f.tma_p;
+        mb = &f.tma_x;
+      } else {
+        tile_of(id - T1, true, T, I, J);
+        ma = &g.tma_a;
+        mb = &g.tma_b;
+        // a's row panels I and J must be complete (stored by other CTAs)
+        while (ld_acquire(f.done + I) < (unsigned)T) __nanosleep(64);
+        while (ld_acquire(f.done + J) < (unsigned)T) __nanosleep(64);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      for (int kt = 0; kt < KT; ++kt, ++gs) {
+        const int s = gs % STAGES;
+        mbar_wait(&empty[s], ((gs / STAGES) & 1) ^ 1);
+        producer_load_stage(smem + s * STAGE_BYTES, ma, mb, kt * BK, I * BM, J * BN, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int wm = warp >> 2, wn = warp & 3;
+  double rmax = 0.0, cmax = 0.0;
+  unsigned int gs = 0;
+  GemmArgs g1 = g;  // GEMM-1 epilogue: plain store of a
+  g1.c = f.a_out;
+  g1.ldc = g.ld;
+  g1.m = n;
+  for (int j = 0;; ++j) {
+    const int slot = j & 1;
+    mbar_wait(&tq_full[slot], (j >> 1) & 1);
+    const int id = tq[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tq_empty[slot]);
+    if (id < 0) break;
+    int I, J;
+    const bool phase1 = id < T1;
+    if (phase1)
+      tile_of(id, false, T, I, J);
+    else
+      tile_of(id - T1, true, T, I, J);
+    Acc<ALGO> acc;
+    acc.zero();
+    for (int kt = 0; kt < KT; ++kt, ++gs) {
+      const int s = gs % STAGES;
+      mbar_wait(&full[s], (gs / STAGES) & 1);
+      consume_stage<ALGO>(smem + s * STAGE_BYTES, acc, wm, wn, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (phase1) {
+      epilogue_tile<ALGO, EPI_STORE>(g1, acc, I, J, wm, wn, lane, rmax, cmax);
+      // publish the tile: every thread fences its stores (generic and async
+      // proxy), the consumer group syncs, one thread counts the tile
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+      if (threadIdx.x == 0) atomicAdd(f.done + I, 1u);
+    } else {
+      if (lane == 0) {
+        // order this warp's epilogue reads of a after the producer's acquire
+        while (ld_acquire(f.done + I) < (unsigned)T) __nanosleep(32);
+        while (ld_acquire(f.done + J) < (unsigned)T) __nanosleep(32);
+      }
+      __syncwarp();
+      epilogue_tile<ALGO, EPI_UPDATE>(g, acc, I, J, wm, wn, lane, rmax, cmax);
     }
   }
+  reduce_max_atomic(rmax, cmax, g.resid, g.cons, red_res, red_cons);
 }
 
 // elementwise c = a - a^H (commutator op, integrator.py:127-128 form)
@@ -485,6 +656,66 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
   const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   if (algo == ALGO_4M) return launch<ALGO_4M, EPI_ROWS>(g, nt, st);
   return launch<ALGO_3M, EPI_ROWS>(g, nt, st);
+}
+
+// One fixed-point update after the solve: a = P X and the GEMM-2 update in
+// one persistent launch (grid = SMs).  `sync` must hold (T + 1) u32 zeros.
+static bool g_fattr[16][2];
+static int g_sms[16];
+
+int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
+                  const double* wn, double* out, double hh, double qq, unsigned long long* resid,
+                  unsigned long long* cons, unsigned int* sync, int algo, cudaStream_t st) {
+  FusedArgs f;
+  memset(&f, 0, sizeof f);
+  GemmArgs& g = f.g2;
+  g.n = n;
+  g.m = n;
+  g.k = n;
+  g.a = a;
+  g.lda = n;
+  g.b = p;
+  g.ldb = n;
+  g.amat = a;
+  g.base = base;
+  g.xprev = xprev;
+  g.wn = wn;
+  g.out = out;
+  g.ld = n;
+  g.hh = hh;
+  g.qq = qq;
+  g.resid = resid;
+  g.cons = cons;
+  int rc = make_map(&g.tma_a, a, n, n, n, BM);
+  if (!rc) rc = make_map(&g.tma_b, p, n, n, n, BK);
+  if (!rc) rc = make_map(&f.tma_p, p, n, n, n, BM);
+  if (!rc) rc = make_map(&f.tma_x, x, n, n, n, BK);
+  if (rc) return rc;
+  f.a_out = a;
+  f.next = sync;
+  f.done = sync + 1;
+  int dev;
+  cudaGetDevice(&dev);
+  const int slot = algo == ALGO_4M ? 1 : 0;
+  if (dev < 16 && !g_fattr[dev][slot]) {
+    if (algo == ALGO_4M)
+      ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zupdate<ALGO_4M>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+    else
+      ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zupdate<ALGO_3M>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+    cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    g_fattr[dev][slot] = true;
+  }
+  const int T = (n + BM - 1) / BM;
+  const int total = T * T + T * (T + 1) / 2;
+  const int grid = std::min(total, dev < 16 ? g_sms[dev] : 148);
+  ZT_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (T + 1), st));
+  if (algo == ALGO_4M)
+    k_zupdate<ALGO_4M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
+  else
+    k_zupdate<ALGO_3M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
 }
 
 int skew_diff(int n, const double* a, double* c, cudaStream_t st) {
