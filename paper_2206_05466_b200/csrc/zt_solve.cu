@@ -211,7 +211,7 @@ static int solve_ntiles(int C) { return 4 * C * (C + 1); }
 // Per-lane body.  FAST: every lane owns 16 interior rows of its diagonal
 // (k >= 1 at the first row, the diagonal's last row not inside, m != 0), so
 // all boundary predicates vanish and addresses advance by a constant stride.
-template <bool FINAL, bool FAST>
+template <bool FINAL, bool FAST, bool LAST = false>
 __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __restrict__ w,
                                           double* __restrict__ p, int b, int c, int m0, int lane,
                                           double2* sm, const double2* vpre = nullptr,
@@ -226,6 +226,9 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   const int rs = FAST ? 0 : max(0, m - ib);
   const int re = FAST ? SUB - 1 : min(SUB - 1, n - 1 - ib);
   const bool has = FAST || (mok && rs <= re);
+  // FAST tiles may end exactly at row N-1 (N % 64 == 0): that row is every
+  // diagonal's last element (no coupling below it)
+  const bool lastrow = FAST && LAST && (ib + SUB - 1 == n - 1);
   const size_t cm = (size_t)b * A.C * n + (size_t)c * n + m;
   const int64_t wstride = (A.ldw + 1) * 2;  // doubles between W[i][i-m] and W[i+1][i+1-m]
   const double* wp = w + ((int64_t)ib * A.ldw + (ib - m)) * 2;
@@ -270,7 +273,7 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
           const double rq = fast_rcp(q0);
           const double di = qm1 * rq;  // 1 / d_k
           double L = 0.0;
-          if (FAST || k + rr < len - 1) {
+          if (FAST ? !(lastrow && r == SUB - 1) : (k + rr < len - 1)) {
             const double e = -sqi[rr] * sqk[rr];
             L = e * di;
             const double e2 = bqi[rr] * bqk[rr];
@@ -356,7 +359,7 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
     for (int r = SUB - 1; r >= 0; --r) {
       if (ROW_OK(r)) {
         const double2 f = sm[(s * SUB + r) * DPW + dl];
-        if (!FAST && ib + r - m == len - 1) {
+        if (FAST ? (lastrow && r == SUB - 1) : (ib + r - m == len - 1)) {
           bm.a = make_double2(f.y * v[r].x, f.y * v[r].y);
           bm.g = 0.0;
         } else {
@@ -418,7 +421,8 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
 #pragma unroll
     for (int r = SUB - 1; r >= 0; --r) {
       if (ROW_OK(r)) {
-        hh = (!FAST && ib + r - m == len - 1) ? 0.0 : -sm[(s * SUB + r) * DPW + dl].x * hh;
+        hh = (FAST ? (lastrow && r == SUB - 1) : (ib + r - m == len - 1)) ? 0.0
+                                                                             : -sm[(s * SUB + r) * DPW + dl].x * hh;
         const double2 x = make_double2(fma(hh, xin.x, v[r].x), fma(hh, xin.y, v[r].y));
         if (!FAST && m == 0) {
           // zero-mean gauge (laplacian.py:293-298): P[i][i] = -(x - g)
@@ -473,7 +477,7 @@ __device__ __forceinline__ void fast_tile_coords(int t, int& c, int& g) {
 }
 
 static int fast_chunks(int n) {
-  // chunks whose rows i0 .. i0+63 all satisfy i < n-1
+
   int cf = 0;
   while ((cf + 1) * SR < n - 1) ++cf;
   return cf;
@@ -581,7 +585,11 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_generic(SolveArgs
   if (t >= count) return;
   const int2 cg = tiles[t];
   double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
-  tile_body<FINAL, false>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, cg.x, cg.y * DPW, lane, sm);
+  const int c = cg.x & ~(1 << 30);
+  if (cg.x & (1 << 30))
+    tile_body<FINAL, true, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, cg.y * DPW, lane, sm);
+  else
+    tile_body<FINAL, false>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, cg.y * DPW, lane, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -869,8 +877,12 @@ static std::vector<int2> generic_tiles(int n) {
   for (int c = 0; c < C; ++c) {
     const int gmax = std::min(Gt - 1, (c * SR + SR - 1) / DPW);
     for (int g = 0; g <= gmax; ++g) {
-      const bool fast = (c < cf) && g >= 1 && g <= GPC * c - 1;
-      if (!fast) v.push_back(make_int2(c, g));
+      const bool interior = g >= 1 && g <= GPC * c - 1;
+      const bool fast = (c < cf) && interior;
+      // the chunk ending exactly at row N-1 runs the fast body with the
+      // last-row special case (flag bit 30 of .x)
+      const bool fast_last = !fast && interior && (c + 1) * SR == n;
+      if (!fast) v.push_back(make_int2(c | (fast_last ? (1 << 30) : 0), g));
     }
   }
   return v;

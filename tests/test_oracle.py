@@ -93,3 +93,20 @@ def test_oracle_errors():
     with pytest.raises(zo.OracleFixedPointError) as e:
         zo.fixed_point_solve(w / 4, 0.05, tol=1e-14, max_iter=1)
     assert e.value.iterations == 1 and e.value.residual > 1e-14
+
+
+def test_closed_form_ldlt_matches_dpttrf():
+    """The pivots of every m >= 1 block are the integers (k+m+1)(N-1-k) and
+    L_k = -sqrt((N-1-k-m)(k+1) / ((k+m+1)(N-1-k))): the GPU solve uses this
+    closed form; LAPACK dpttrf (laplacian.py:208) reproduces it to rounding."""
+    import scipy.linalg.lapack as lapack
+
+    for n in (17, 128, 512):
+        for m in range(1, n - 1):
+            dm, em = zo.block_entries(n, m)
+            d, e, info = lapack.dpttrf(dm, em)
+            k = np.arange(n - m, dtype=np.float64)
+            np.testing.assert_allclose(d, (k + m + 1) * (n - 1 - k), rtol=4e-15)
+            kk = k[:-1]
+            lex = -np.sqrt((n - 1 - kk - m) / (kk + m + 1)) * np.sqrt((kk + 1) / (n - 1 - kk))
+            np.testing.assert_allclose(e, lex, rtol=4e-15)
