@@ -18,6 +18,12 @@ Contents (all complex128 C-order unless noted):
                     per-step iterations, C2/C3/H series
   known.npz         known answers: pinv-oracle P at N=5, casimirs of
                     i*diag(1,-1,0,0), blocks N=2 m=0 / N=3 m=1
+  modes.npz         inputs of the reference's integrator property tests
+                    (test_integrator.py) built with its spherical-harmonic basis
+                    (out of scope here): single modes (N=8 l=4 m=1, N=9 l=2 m=0),
+                    normalized states (N=32, N=16, N=8, N=128), the rigid-rotation
+                    state (N=16) and the basis matrix T_{5,3} used to extract the
+                    advected coefficient, plus the reference's own results
 """
 
 from __future__ import annotations
@@ -120,7 +126,57 @@ def known():
     )
 
 
+def modes():
+    from test_basis import random_real_field_coeffs
+    from zeitlin.basis import HarmonicCoefficients, compute_basis, extract, project
+
+    def single(n, l, m, amp):
+        c = HarmonicCoefficients.zeros(n)
+        c.set(l, m, amp)
+        c.enforce_reality()
+        return project(c, compute_basis(n))
+
+    def normalized(n, seed, l_hi=None):
+        rng = np.random.default_rng(seed)
+        c = random_real_field_coeffs(n, rng, l_lo=2, l_hi=l_hi or min(n - 2, 10))
+        w = project(c, compute_basis(n))
+        return w / laplacian.spectral_norm(w)
+
+    d = {}
+    d["mode_8_4_1"] = single(8, 4, 1, 0.9 - 0.3j)
+    d["mode_9_2_0"] = single(9, 2, 0, 1.1)
+    d["norm32"] = normalized(32, 11)
+    d["norm16"] = normalized(16, 12)
+    d["norm8"] = normalized(8, 13, l_hi=4)
+    d["norm128"] = normalized(128, 14, l_hi=20)
+    # rigid rotation (test_integrator.py:190-218)
+    n = 16
+    basis = compute_basis(n)
+    c = HarmonicCoefficients.zeros(n)
+    c.set(1, 0, 1.3)
+    c.set(5, 3, 1e-6)
+    c.enforce_reality()
+    w = project(c, basis)
+    d["rot16"] = w
+    # T_{5,3}: the coefficient is Tr(T^H W) for the trace-orthonormal basis;
+    # recover the linear functional by probing extract with unit matrices
+    f = np.zeros((n, n), dtype=complex)
+    for i in range(n):
+        for j in range(n):
+            e = np.zeros((n, n), dtype=complex)
+            e[i, j] = 1.0
+            f[i, j] = extract(e, basis).get(5, 3)
+    d["extract_5_3"] = f  # coefficient = sum(f * W)
+    st = integrator.StepperState(w=w.copy(), h=1e-3, tol=1e-14, max_iter=60)
+    for _ in range(1000):
+        st = integrator.midpoint_step(st)
+    d["rot16_after_1000"] = st.w
+    d["rot16_time"] = np.array(st.time)
+    np.savez_compressed(os.path.join(OUT, "modes.npz"), **d)
+
+
 if __name__ == "__main__":
+    modes()
     solve_small()
     cfg1()
     cfg4_n64()
