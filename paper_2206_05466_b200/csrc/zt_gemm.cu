@@ -48,7 +48,15 @@ constexpr int B_BOX_BYTES = BK * 128;
 constexpr int A_STAGE_BYTES = A_BOXES * A_BOX_BYTES;
 constexpr int B_STAGE_BYTES = B_BOXES * B_BOX_BYTES;
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int CONSUMER_WARPS = 8;
+// Warp layout: WNB n8-blocks per consumer warp (warp tile 32 x 8*WNB complex);
+// WNB = 2: 8 consumer warps (2 x 4), WNB = 4: 4 consumer warps (2 x 2) with
+// fewer 3M operand-sum DADDs per DMMA (8 per 48 instead of 6 per 24).
+#ifndef ZT_WNB
+#define ZT_WNB 2
+#endif
+constexpr int WNB = ZT_WNB;
+constexpr int WN_WARPS = 64 / (8 * WNB);
+constexpr int CONSUMER_WARPS = 2 * WN_WARPS;
 constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 1024 + 64;
 
@@ -119,14 +127,14 @@ __device__ __forceinline__ void tile_of(int t, bool lower, int T, int& I, int& J
 template <int ALGO>
 struct Acc {
   static constexpr int NACC = (ALGO != ALGO_4M) ? 3 : 2;
-  double v[NACC][4][2][2];
+  double v[NACC][4][WNB][2];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) v[q][i][j][0] = v[q][i][j][1] = 0.0;
+        for (int j = 0; j < WNB; ++j) v[q][i][j][0] = v[q][i][j][1] = 0.0;
   }
 };
 
@@ -141,25 +149,25 @@ __device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>
     const int jb = ks >> 1, par = ks & 1;
     const int c = 2 * fk + par;  // 16B chunk inside the 128B row
     const int kr = 8 * jb + c;   // k row of the B stage
-    double2 af[4], bf[2];
+    double2 af[4], bf[WNB];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int r = wm * 32 + i * 8 + fr;
       af[i] = *reinterpret_cast<const double2*>(st + jb * A_BOX_BYTES + r * 128 + ((c ^ fr) << 4));
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * 2 + j) * B_BOX_BYTES + kr * 128 +
+    for (int j = 0; j < WNB; ++j)
+      bf[j] = *reinterpret_cast<const double2*>(st + A_STAGE_BYTES + (wn * WNB + j) * B_BOX_BYTES + kr * 128 +
                                                  ((fr ^ (kr & 7)) << 4));
     if (ALGO != ALGO_4M) {
-      double bsum[2];
+      double bsum[WNB];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
+      for (int j = 0; j < WNB; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const double asum = (ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < WNB; ++j) {
           dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
           dmma(A.v[1][i][j][0], A.v[1][i][j][1], af[i].y, bf[j].y);
           dmma(A.v[2][i][j][0], A.v[2][i][j][1], asum, bsum[j]);
@@ -170,7 +178,7 @@ __device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>
       for (int i = 0; i < 4; ++i) {
         const double ain = -af[i].y;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < WNB; ++j) {
           dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
           dmma(A.v[0][i][j][0], A.v[0][i][j][1], ain, bf[j].y);
           dmma(A.v[1][i][j][0], A.v[1][i][j][1], af[i].x, bf[j].y);
@@ -191,7 +199,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const Acc<ALGO>
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < WNB; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         double cr, ci;
@@ -203,7 +211,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const Acc<ALGO>
           ci = A.v[1][i][j][e];
         }
         const int gi = row0 + wm * 32 + i * 8 + fr;
-        const int gj = col0 + wn * 16 + j * 8 + fk * 2 + e;
+        const int gj = col0 + wn * 8 * WNB + j * 8 + fk * 2 + e;
         if (gi >= mrows || gj >= n) continue;
         if (EPI == EPI_STORE) {
           st2(g.c + ((size_t)gi * g.ldc + gj) * 2, make_double2(cr, ci));
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
   }
 
   // ===== consumer warps: 2 (M) x 4 (N), warp tile 32 x 16 complex =====
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / WN_WARPS, wn = warp % WN_WARPS;
   Acc<ALGO> acc;
   acc.zero();
   for (int kt = 0; kt < KT; ++kt) {
@@ -466,7 +474,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
   }
 
   // ===== consumers =====
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / WN_WARPS, wn = warp % WN_WARPS;
   double rmax = 0.0, cmax = 0.0;
   unsigned int gs = 0;
   GemmArgs g1 = g;  // GEMM-1 epilogue: plain store of a

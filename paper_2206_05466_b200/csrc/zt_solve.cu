@@ -576,6 +576,36 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_DIRECT_MINB) k_solve_f
   }
 }
 
+// One launch for a whole tile pass: blocks [0, gblocks) take the boundary
+// tiles (dispatched first, so their latency hides under the interior tiles
+// that follow), the rest the interior tiles.
+template <bool FINAL>
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4)
+    k_solve_merged(SolveArgs A, const int2* __restrict__ tiles, int count, int gblocks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
+  const double* w = A.w + (size_t)b * A.sw * 2;
+  double* p = A.p + (size_t)b * A.sp * 2;
+  if ((int)blockIdx.x < gblocks) {
+    const int t = blockIdx.x * SOLVE_WARPS + warp;
+    if (t >= count) return;
+    const int2 cg = tiles[t];
+    const int c = cg.x & ~(1 << 30);
+    if (cg.x & (1 << 30))
+      tile_body<FINAL, true, true>(A, w, p, b, c, cg.y * DPW, lane, sm);
+    else
+      tile_body<FINAL, false>(A, w, p, b, c, cg.y * DPW, lane, sm);
+  } else {
+    const int t = (blockIdx.x - gblocks) * SOLVE_WARPS + warp;
+    if (t >= A.ntiles) return;
+    int c, g;
+    fast_tile_coords(t, c, g);
+    tile_body<FINAL, true>(A, w, p, b, c, g * DPW, lane, sm);
+  }
+}
+
 template <bool FINAL>
 __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_generic(SolveArgs A, const int2* __restrict__ tiles, int count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -597,14 +627,21 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_generic(SolveArgs
 // segments (warps); loads are coalesced across diagonals; the segment maps
 // are composed through shared memory.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_solve_carry(int n, int C, const double* __restrict__ G,
-                                                     const double* __restrict__ H,
-                                                     const double* __restrict__ K,
-                                                     const double* __restrict__ m0x, double2* yend,
-                                                     double2* xst, const double2* __restrict__ m0acc,
-                                                     double2* m0mg) {
-  __shared__ AffW agg[8][32];
-  __shared__ double2 red[8];
+// Block = 32 diagonals (lanes) x SEG chunk segments (warps, SEG = 8..32);
+// each thread caches its <= CE chunks' values in registers so every phase
+// costs one memory round trip.
+constexpr int CE = 8;
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) k_solve_carry(int n, int C, const double* __restrict__ G,
+                                                      const double* __restrict__ H,
+                                                      const double* __restrict__ K,
+                                                      const double* __restrict__ m0x, double2* yend,
+                                                      double2* xst, const double2* __restrict__ m0acc,
+                                                      double2* m0mg) {
+  __shared__ AffW agg[32][32];
+  __shared__ double2 red[32];
+  const int SEG = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, wseg = threadIdx.x >> 5;
   const int m = blockIdx.x * 32 + lane;
   const int b = blockIdx.y;
@@ -612,8 +649,9 @@ __global__ void __launch_bounds__(256) k_solve_carry(int n, int C, const double*
   const bool ok = m < n;
   const int cs = (blockIdx.x * 32) / SR;  // first chunk holding any of the 32 diagonals
   const int nc = C - cs;
-  const int E = (nc + 7) / 8;
+  const int E = (nc + SEG - 1) / SEG;  // <= CE (host picks SEG)
   const int cb = cs + wseg * E, ce = min(cb + E, C);
+  const bool is0 = (m == 0);
   // m = 0: mu = tr W / N from the chunk trace partials (laplacian.py:276-279)
   double2 mu = make_double2(0.0, 0.0);
   if (blockIdx.x == 0) {
@@ -626,89 +664,107 @@ __global__ void __launch_bounds__(256) k_solve_carry(int n, int C, const double*
     if (lane == 0) red[wseg] = tr;
     __syncthreads();
     double2 t = make_double2(0.0, 0.0);
-    for (int q = 0; q < 8; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
+    for (int q = 0; q < SEG; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
     mu = make_double2(t.x / n, t.y / n);
     __syncthreads();
   }
-  const bool is0 = (m == 0);
-  // forward: segment composition
+  // ---- forward: y_end(c) = a(c) + G(c) y_end(c-1) ----
+  double2 av[CE];
+  double gv[CE];
+#pragma unroll
+  for (int q = 0; q < CE; ++q) {
+    const int c = cb + q;
+    if (ok && c < ce) {
+      const size_t o = (size_t)c * n + m;
+      av[q] = yend[base + o];
+      gv[q] = G[o];
+      if (is0) av[q] = make_double2(av[q].x - mu.x * m0x[c * M0X + 0], av[q].y - mu.y * m0x[c * M0X + 0]);
+    } else {
+      av[q] = make_double2(0.0, 0.0);
+      gv[q] = 1.0;
+    }
+  }
   AffW f;
   f.a = make_double2(0.0, 0.0);
   f.g = 1.0;
-  if (ok)
-    for (int c = cb; c < ce; ++c) {
-      const size_t o = (size_t)c * n + m;
-      double2 a = yend[base + o];
-      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 0], a.y - mu.y * m0x[c * M0X + 0]);
-      const double gg = G[o];
-      f.a = make_double2(fma(gg, f.a.x, a.x), fma(gg, f.a.y, a.y));
-      f.g *= gg;
-    }
+#pragma unroll
+  for (int q = 0; q < CE; ++q) {
+    f.a = make_double2(fma(gv[q], f.a.x, av[q].x), fma(gv[q], f.a.y, av[q].y));
+    f.g *= gv[q];
+  }
   agg[wseg][lane] = f;
   __syncthreads();
   AffW pre;
   pre.a = make_double2(0.0, 0.0);
   pre.g = 1.0;
   for (int q = 0; q < wseg; ++q) pre = aff_compose(pre, agg[q][lane]);
-  double2 y = pre.a;
-  if (ok)
-    for (int c = cb; c < ce; ++c) {
-      const size_t o = (size_t)c * n + m;
-      double2 a = yend[base + o];
-      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 0], a.y - mu.y * m0x[c * M0X + 0]);
-      yend[base + o] = y;  // y_in(c)
-      const double gg = G[o];
-      y = make_double2(fma(gg, y.x, a.x), fma(gg, y.y, a.y));
+  double2 yin[CE];
+  {
+    double2 y = pre.a;
+#pragma unroll
+    for (int q = 0; q < CE; ++q) {
+      yin[q] = y;
+      y = make_double2(fma(gv[q], y.x, av[q].x), fma(gv[q], y.y, av[q].y));
+      const int c = cb + q;
+      if (ok && c < ce) yend[base + (size_t)c * n + m] = yin[q];  // y_in(c)
     }
+  }
   __syncthreads();
-  // backward: x_start(c) = (xst(c) + K y_in(c)) + H x_start(c+1)
+  // ---- backward: x_start(c) = (xst(c) + K y_in(c)) + H x_start(c+1) ----
+  double hv[CE];
+#pragma unroll
+  for (int q = 0; q < CE; ++q) {
+    const int c = cb + q;
+    if (ok && c < ce) {
+      const size_t o = (size_t)c * n + m;
+      av[q] = xst[base + o];
+      if (is0) av[q] = make_double2(av[q].x - mu.x * m0x[c * M0X + 1], av[q].y - mu.y * m0x[c * M0X + 1]);
+      const double kk = K[o];
+      hv[q] = H[o];
+      av[q] = make_double2(fma(kk, yin[q].x, av[q].x), fma(kk, yin[q].y, av[q].y));
+    } else {
+      av[q] = make_double2(0.0, 0.0);
+      hv[q] = 1.0;
+    }
+  }
   AffW bk;
   bk.a = make_double2(0.0, 0.0);
   bk.g = 1.0;
-  if (ok)
-    for (int c = ce - 1; c >= cb; --c) {
-      const size_t o = (size_t)c * n + m;
-      double2 a = xst[base + o];
-      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 1], a.y - mu.y * m0x[c * M0X + 1]);
-      const double2 yi = yend[base + o];
-      const double kk = K[o], hh = H[o];
-      a = make_double2(fma(kk, yi.x, a.x), fma(kk, yi.y, a.y));
-      bk.a = make_double2(fma(hh, bk.a.x, a.x), fma(hh, bk.a.y, a.y));
-      bk.g *= hh;
-    }
+#pragma unroll
+  for (int q = CE - 1; q >= 0; --q) {
+    bk.a = make_double2(fma(hv[q], bk.a.x, av[q].x), fma(hv[q], bk.a.y, av[q].y));
+    bk.g *= hv[q];
+  }
   agg[wseg][lane] = bk;
   __syncthreads();
   AffW suf;
   suf.a = make_double2(0.0, 0.0);
   suf.g = 1.0;
-  for (int q = 7; q > wseg; --q) suf = aff_compose(suf, agg[q][lane]);
+  for (int q = SEG - 1; q > wseg; --q) suf = aff_compose(suf, agg[q][lane]);
   double2 x = suf.a;
   double2 gs = make_double2(0.0, 0.0);
-  if (ok)
-    for (int c = ce - 1; c >= cb; --c) {
-      const size_t o = (size_t)c * n + m;
-      double2 a = xst[base + o];
-      if (is0) a = make_double2(a.x - mu.x * m0x[c * M0X + 1], a.y - mu.y * m0x[c * M0X + 1]);
-      const double2 yi = yend[base + o];
-      const double kk = K[o], hh = H[o];
-      xst[base + o] = x;  // x_in(c)
+#pragma unroll
+  for (int q = CE - 1; q >= 0; --q) {
+    const int c = cb + q;
+    if (ok && c < ce) {
+      xst[base + (size_t)c * n + m] = x;  // x_in(c)
       if (is0) {
         // chunk x-sum = (sum x^ - mu S1) + SH x_in + SK y_in  (zero-mean gauge)
         const double2 sx = m0acc[((size_t)b * C + c) * 2 + 1];
-        const double* q = m0x + (size_t)c * M0X;
-        gs.x += (sx.x - mu.x * q[2]) + q[3] * x.x + q[4] * yi.x;
-        gs.y += (sx.y - mu.y * q[2]) + q[3] * x.y + q[4] * yi.y;
+        const double* qq = m0x + (size_t)c * M0X;
+        gs.x += (sx.x - mu.x * qq[2]) + qq[3] * x.x + qq[4] * yin[q].x;
+        gs.y += (sx.y - mu.y * qq[2]) + qq[3] * x.y + qq[4] * yin[q].y;
       }
-      a = make_double2(fma(kk, yi.x, a.x), fma(kk, yi.y, a.y));
-      x = make_double2(fma(hh, x.x, a.x), fma(hh, x.y, a.y));
     }
+    x = make_double2(fma(hv[q], x.x, av[q].x), fma(hv[q], x.y, av[q].y));
+  }
   if (blockIdx.x == 0) {
     __syncthreads();
     if (lane == 0) red[wseg] = gs;
     __syncthreads();
     if (threadIdx.x == 0) {
       double2 t = make_double2(0.0, 0.0);
-      for (int q = 0; q < 8; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
+      for (int q = 0; q < SEG; ++q) t = make_double2(t.x + red[q].x, t.y + red[q].y);
       m0mg[2 * b] = mu;
       m0mg[2 * b + 1] = make_double2(t.x / n, t.y / n);  // laplacian.py:293-296
     }
@@ -897,7 +953,7 @@ static size_t op_bytes(int n, int C) {
 
 int op_create(int n, int device, zt_operator** out) {
   if (n < 2) return fail(ZT_EINVAL, "matrix truncation must be at least 2, got " + std::to_string(n));
-  if (n > 65536) return fail(ZT_EINVAL, "matrix truncation above 65536 is not supported");
+  if (n > 16384) return fail(ZT_EINVAL, "matrix truncation above 16384 is not supported");
   int prev;
   ZT_CUDA_CHECK(cudaGetDevice(&prev));
   ZT_CUDA_CHECK(cudaSetDevice(device));
@@ -951,6 +1007,8 @@ int op_create(int n, int device, zt_operator** out) {
   cudaFuncSetAttribute(k_solve_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
   cudaFuncSetAttribute(k_solve_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_fast_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_merged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_solve_merged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_fast_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_fast_batch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_fast_batch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * smem);
@@ -958,6 +1016,7 @@ int op_create(int n, int device, zt_operator** out) {
     const char* e = getenv("ZT_SOLVE_FAST");
     op->solve_tma = e && std::string(e) == "tma";
     op->solve_amortize = e && std::string(e) == "batch";
+    op->solve_merged = !(e && (std::string(e) == "split" || std::string(e) == "batch"));
   }
   cudaFuncSetAttribute(k_solve_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
@@ -965,6 +1024,9 @@ int op_create(int n, int device, zt_operator** out) {
     const char* e = getenv("ZT_SOLVE_STREAMS");
     op->nside = e ? std::max(1, std::min(8, atoi(e))) : 1;
     for (int q = 0; q < op->nside; ++q) cudaStreamCreateWithFlags(&op->side[q], cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&op->gstream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&op->gfork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&op->gjoin, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming);
     for (int q = 0; q < op->nside; ++q) cudaEventCreateWithFlags(&op->join[q], cudaEventDisableTiming);
   }
@@ -993,6 +1055,9 @@ int op_destroy(zt_operator* op) {
     cudaEventDestroy(op->join[q]);
   }
   if (op->fork) cudaEventDestroy(op->fork);
+  if (op->gstream) cudaStreamDestroy(op->gstream);
+  if (op->gfork) cudaEventDestroy(op->gfork);
+  if (op->gjoin) cudaEventDestroy(op->gjoin);
   cudaFree(op->block);
   delete op;
   return ZT_OK;
@@ -1064,35 +1129,64 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
     if (rc) return rc;
   }
   const int fsm = SOLVE_WARPS * FAST_SMEM_PER_WARP + 256;
-  // pass 1: interior tiles, then (programmatically overlapped) boundary tiles
+  // Each tile pass: the boundary tiles (few, latency bound) start first on
+  // the operator's side stream and run beside the interior tiles on the
+  // caller's stream (fork/join events; graph-capturable).
   const int td = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  if (tf > 0) {
-    if (op->solve_tma)
-      k_solve_fast<false><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
-    else if (batch > 1 && op->solve_amortize)
-      k_solve_fast_batch<false><<<td, SOLVE_WARPS * 32, smem, st>>>(A, batch);
-    else
-      k_solve_fast_direct<false><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
-    ZT_LAUNCHED();
-  }
-  ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<false>), dim3(tg, batch), smem, st,
-                           A, op->gen_tiles, op->ngen, tf > 0));
+  auto pass = [&](bool fin) -> int {
+    if (op->solve_merged && !op->solve_tma) {
+      const dim3 grid(tg + td, batch);
+      if (fin)
+        k_solve_merged<true><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
+      else
+        k_solve_merged<false><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
+      ZT_LAUNCHED();
+      return ZT_OK;
+    }
+    ZT_CUDA_CHECK(cudaEventRecord(op->gfork, st));
+    ZT_CUDA_CHECK(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
+    if (op->ngen > 0) {
+      if (fin)
+        k_solve_generic<true><<<dim3(tg, batch), SOLVE_WARPS * 32, smem, op->gstream>>>(A, op->gen_tiles, op->ngen);
+      else
+        k_solve_generic<false><<<dim3(tg, batch), SOLVE_WARPS * 32, smem, op->gstream>>>(A, op->gen_tiles, op->ngen);
+      ZT_LAUNCHED();
+    }
+    if (tf > 0) {
+      if (op->solve_tma) {
+        if (fin)
+          k_solve_fast<true><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
+        else
+          k_solve_fast<false><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
+      } else if (batch > 1 && op->solve_amortize) {
+        if (fin)
+          k_solve_fast_batch<true><<<td, SOLVE_WARPS * 32, 2 * smem, st>>>(A, batch);
+        else
+          k_solve_fast_batch<false><<<td, SOLVE_WARPS * 32, smem, st>>>(A, batch);
+      } else {
+        if (fin)
+          k_solve_fast_direct<true><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+        else
+          k_solve_fast_direct<false><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
+      }
+      ZT_LAUNCHED();
+    }
+    ZT_CUDA_CHECK(cudaEventRecord(op->gjoin, op->gstream));
+    ZT_CUDA_CHECK(cudaStreamWaitEvent(st, op->gjoin, 0));
+    return ZT_OK;
+  };
+  int rc = pass(false);
+  if (rc) return rc;
+  const int seg = std::max(8, (C + CE - 1) / CE);  // chunk segments per carry block
+  if (seg <= 16)
+    k_solve_carry<512><<<dim3((n + 31) / 32, batch), 32 * seg, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x,
+                                                                       A.yend, A.xst, A.m0acc, A.m0mg);
+  else  // N > 8192: 32 segments, register-limited
+    k_solve_carry<1024><<<dim3((n + 31) / 32, batch), 32 * seg, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x,
+                                                                        A.yend, A.xst, A.m0acc, A.m0mg);
   ZT_LAUNCHED();
-  k_solve_carry<<<dim3((n + 31) / 32, batch), 256, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x, A.yend,
-                                                          A.xst, A.m0acc, A.m0mg);
-  ZT_LAUNCHED();
-  if (tf > 0) {
-    if (op->solve_tma)
-      k_solve_fast<true><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
-    else if (batch > 1 && op->solve_amortize)
-      k_solve_fast_batch<true><<<td, SOLVE_WARPS * 32, 2 * smem, st>>>(A, batch);
-    else
-      k_solve_fast_direct<true><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
-    ZT_LAUNCHED();
-  }
-  ZT_CUDA_CHECK(launch_pdl(reinterpret_cast<const void*>(&k_solve_generic<true>), dim3(tg, batch), smem, st,
-                           A, op->gen_tiles, op->ngen, tf > 0));
-  ZT_LAUNCHED();
+  rc = pass(true);
+  if (rc) return rc;
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
 }
