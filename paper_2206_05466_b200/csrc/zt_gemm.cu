@@ -56,11 +56,22 @@ constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 #endif
 constexpr int WNB = ZT_WNB;
 constexpr int WN_WARPS = 64 / (8 * WNB);
+// 3M sum planes (ALGO_3MS): per 64-row x 16-k A tile and 16-k x 64-col B tile,
+// 1024 doubles each in DMMA-fragment order, so one 8 KB bulk copy per tile
+// lands them in shared memory ready for conflict-free LDS.64.
+constexpr int PLANE_TILE = 1024;                   // doubles per plane tile
+constexpr int SUM_STAGE_BYTES = 2 * PLANE_TILE * 8;  // A + B plane tiles per stage
 constexpr int CONSUMER_WARPS = 2 * WN_WARPS;
 constexpr int GEMM_THREADS = (CONSUMER_WARPS + 1) * 32;
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 1024 + 64;
+constexpr int GEMM_SMEM_S = STAGES * (STAGE_BYTES + 2 * 1024 * 8) + (2 * STAGES + 4) * 8 + 1024 + 64;
 
-enum { ALGO_3M = 0, ALGO_4M = 1, ALGO_3M_NOSUM = 2 /* timing experiment only: wrong results */ };
+enum {
+  ALGO_3M = 0,        // Gauss 3M, operand sums (re + im) formed per warp in registers
+  ALGO_4M = 1,        // classical 4 real products
+  ALGO_3M_NOSUM = 2,  // timing experiment only: skips the sums (wrong results)
+  ALGO_3MS = 3        // Gauss 3M, sums read from precomputed fragment-order sum planes
+};
 enum {
   EPI_STORE = 0,   // C = A B
   EPI_UPDATE = 1,  // square, lower tiles + mirror: new = base + hh (a - a^H) + qq b
@@ -141,6 +152,8 @@ struct Acc {
 // One BK-deep stage of DMMA for warp (wm, wn) from the swizzled stage `st`.
 template <int ALGO>
 __device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>& A, int wm, int wn, int lane) {
+  const double* sa = reinterpret_cast<const double*>(st + STAGE_BYTES);  // ALGO_3MS planes
+  const double* sb = sa + PLANE_TILE;
   const int fr = lane >> 2, fk = lane & 3;
   // A fragment row r = wm*32 + i*8 + fr (r & 7 == fr); B fragment column
   // n = wn*16 + j*8 + fr lives in box (wn*2 + j), in-box column fr.
@@ -162,10 +175,13 @@ __device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>
     if (ALGO != ALGO_4M) {
       double bsum[WNB];
 #pragma unroll
-      for (int j = 0; j < WNB; ++j) bsum[j] = (ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x;
+      for (int j = 0; j < WNB; ++j)
+        bsum[j] = (ALGO == ALGO_3MS) ? sb[((ks * WN_WARPS + wn) * WNB + j) * 32 + lane]
+                                     : ((ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const double asum = (ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y;
+        const double asum = (ALGO == ALGO_3MS) ? sa[((ks * 2 + wm) * 4 + i) * 32 + lane]
+                                               : ((ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y);
 #pragma unroll
         for (int j = 0; j < WNB; ++j) {
           dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
@@ -304,8 +320,14 @@ __device__ __forceinline__ void reduce_max_atomic(double rmax, double cmax, unsi
 }
 
 __device__ __forceinline__ void producer_load_stage(unsigned char* st, const CUtensorMap* ma, const CUtensorMap* mb,
-                                                    int k0, int row0, int col0, uint64_t* bar) {
-  mbar_arrive_expect_tx(bar, STAGE_BYTES);
+                                                    int k0, int row0, int col0, uint64_t* bar,
+                                                    const double* pa = nullptr, const double* pb = nullptr) {
+  // pa / pb: the sum-plane tiles (A: rows row0.., k k0..; B: k k0.., cols col0..)
+  mbar_arrive_expect_tx(bar, STAGE_BYTES + (pa ? SUM_STAGE_BYTES : 0));
+  if (pa) {
+    bulk_g2s(st + STAGE_BYTES, pa, PLANE_TILE * 8, bar);
+    bulk_g2s(st + STAGE_BYTES + PLANE_TILE * 8, pb, PLANE_TILE * 8, bar);
+  }
 #pragma unroll
   for (int j = 0; j < A_BOXES; ++j) tma_2d(st + j * A_BOX_BYTES, ma, 2 * (k0 + 8 * j), row0, bar);
 #pragma unroll
@@ -380,6 +402,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
   if (EPI != EPI_STORE) reduce_max_atomic(rmax, cmax, g.resid, g.cons, red_res, red_cons);
 }
 
+// ---- 3M sum planes --------------------------------------------------------
+// A layout (operand rows r, inner index k): tile (r/64, k/16), slot
+// ((ks*2 + wm)*4 + i)*32 + fr*4 + fk with r%64 = wm*32 + i*8 + fr and
+// k%16 = 8*(ks>>1) + 2*fk + (ks&1) — exactly the DMMA A-fragment order of
+// consume_stage.  B layout (inner k, columns c): tile (k/16, c/64), slot
+// ((ks*WN_WARPS + wn)*WNB + j)*32 + fr*4 + fk with c%64 = wn*8*WNB + j*8 + fr.
+__device__ __forceinline__ size_t a_plane_index(int r, int k, int kbt) {
+  const int ri = r & 63, ki = k & 15;
+  const int wm = ri >> 5, i = (ri >> 3) & 3, fr = ri & 7;
+  const int ks = 2 * (ki >> 3) + (ki & 1), fk = (ki & 7) >> 1;
+  return ((size_t)(r >> 6) * kbt + (k >> 4)) * PLANE_TILE + (((ks * 2 + wm) * 4 + i) * 32 + fr * 4 + fk);
+}
+
+__global__ void __launch_bounds__(256) k_sum_planes(int n, const double* __restrict__ p, const double* __restrict__ x,
+                                                    int64_t ld, double* pa, double* pb, double* xb) {
+  // blockIdx.y: 0 -> P in A layout, 1 -> P in B layout, 2 -> X in B layout
+  const int which = blockIdx.y;
+  const int kbt = (n + 15) / 16, cbt = (n + 63) / 64;
+  const int ntiles = (which == 0) ? cbt * kbt : kbt * cbt;
+  const int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const double* src = (which == 2) ? x : p;
+  double* out = (which == 0) ? pa : (which == 1 ? pb : xb);
+  for (int slot = threadIdx.x; slot < PLANE_TILE; slot += blockDim.x) {
+    const int qq = slot >> 5, ln = slot & 31, fr = ln >> 2, fk = ln & 3;
+    int r, c;
+    if (which == 0) {
+      const int rb = tile / kbt, kb = tile % kbt;
+      const int ks = qq >> 3, wm = (qq >> 2) & 1, i = qq & 3;
+      r = rb * 64 + wm * 32 + i * 8 + fr;
+      c = kb * 16 + 8 * (ks >> 1) + 2 * fk + (ks & 1);
+    } else {
+      const int kb = tile / cbt, cb = tile % cbt;
+      const int ks = qq / (WN_WARPS * WNB), wn = (qq / WNB) % WN_WARPS, j = qq % WNB;
+      r = kb * 16 + 8 * (ks >> 1) + 2 * fk + (ks & 1);
+      c = cb * 64 + wn * 8 * WNB + j * 8 + fr;
+    }
+    double v = 0.0;
+    if (r < n && c < n) {
+      const double2 z = ld2(src + ((size_t)r * ld + c) * 2);
+      v = z.x + z.y;
+    }
+    out[(size_t)tile * PLANE_TILE + slot] = v;
+  }
+}
+
 // ---- persistent fused update: GEMM-1 tiles then GEMM-2 lower tiles --------
 // Work ids [0, T^2) are GEMM-1 tiles a = P X (grouped rasterisation, store a
 // and count the finished tiles of each row panel); ids [T^2, T^2 + T(T+1)/2)
@@ -394,6 +462,12 @@ struct FusedArgs {
   double* a_out;         // GEMM-1 output a
   unsigned int* next;    // global tile counter (zeroed per launch)
   unsigned int* done;    // [T] finished GEMM-1 tiles per row panel (zeroed per launch)
+  // ALGO_3MS sum planes: GEMM-1 A (P, A layout) / B (X, B layout); GEMM-2
+  // A (a, A layout, written by the GEMM-1 epilogue) / B (P, B layout)
+  const double* pa1;
+  const double* pb1;
+  double* pa2;
+  const double* pb2;
 };
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
@@ -405,9 +479,11 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
 template <int ALGO>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_constant__ FusedArgs f) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr bool PL = (ALGO == ALGO_3MS);
+  constexpr int SB = STAGE_BYTES + (PL ? SUM_STAGE_BYTES : 0);
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
   uint64_t* empty = full + STAGES;
   uint64_t* tq_full = empty + STAGES;  // [2]
   uint64_t* tq_empty = tq_full + 2;    // [2]
@@ -451,23 +527,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
       if (id >= total) break;
       int I, J;
       const CUtensorMap *ma, *mb;
+      const double *pla, *plb;
       if (id < T1) {
         tile_of(id, false, T, I, J);
         ma = &f.tma_p;
         mb = &f.tma_x;
+        pla = f.pa1;
+        plb = f.pb1;
       } else {
         tile_of(id - T1, true, T, I, J);
         ma = &g.tma_a;
         mb = &g.tma_b;
+        pla = f.pa2;
+        plb = f.pb2;
         // a's row panels I and J must be complete (stored by other CTAs)
         while (ld_acquire(f.done + I) < (unsigned)T) __nanosleep(64);
         while (ld_acquire(f.done + J) < (unsigned)T) __nanosleep(64);
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
+      const int kbt = KT;  // k blocks of 16
       for (int kt = 0; kt < KT; ++kt, ++gs) {
         const int s = gs % STAGES;
         mbar_wait(&empty[s], ((gs / STAGES) & 1) ^ 1);
-        producer_load_stage(smem + s * STAGE_BYTES, ma, mb, kt * BK, I * BM, J * BN, &full[s]);
+        if (PL)
+          producer_load_stage(smem + s * SB, ma, mb, kt * BK, I * BM, J * BN, &full[s],
+                              pla + ((size_t)I * kbt + kt) * PLANE_TILE, plb + ((size_t)kt * T + J) * PLANE_TILE);
+        else
+          producer_load_stage(smem + s * SB, ma, mb, kt * BK, I * BM, J * BN, &full[s]);
       }
     }
     return;
@@ -499,12 +585,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
     for (int kt = 0; kt < KT; ++kt, ++gs) {
       const int s = gs % STAGES;
       mbar_wait(&full[s], (gs / STAGES) & 1);
-      consume_stage<ALGO>(smem + s * STAGE_BYTES, acc, wm, wn, lane);
+      consume_stage<ALGO>(smem + s * SB, acc, wm, wn, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     if (phase1) {
       epilogue_tile<ALGO, EPI_STORE>(g1, acc, I, J, wm, wn, lane, rmax, cmax);
+      if (PL) {
+        // a's 3M sum plane (A layout) for the GEMM-2 tiles of this row panel
+        const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < WNB; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int gi = I * BM + wm * 32 + i * 8 + fr;
+              const int gj = J * BN + wn * 8 * WNB + j * 8 + fk * 2 + e;
+              const double cr = acc.v[0][i][j][e] - acc.v[1][i][j][e];
+              const double ci = acc.v[2][i][j][e] - acc.v[0][i][j][e] - acc.v[1][i][j][e];
+              // padding rows/cols (>= n) must hold zeros, as the zero-filled TMA
+              // tiles; columns past the plane's 16*KT width do not exist in it
+              if (gj < KT * BK) f.pa2[a_plane_index(gi, gj, KT)] = (gi < n && gj < n) ? cr + ci : 0.0;
+            }
+      }
       // publish the tile: every thread fences its stores (generic and async
       // proxy), the consumer group syncs, one thread counts the tile
       __threadfence();
@@ -668,12 +772,16 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
 
 // One fixed-point update after the solve: a = P X and the GEMM-2 update in
 // one persistent launch (grid = SMs).  `sync` must hold (T + 1) u32 zeros.
-static bool g_fattr[16][2];
+static bool g_fattr[16][3];
 static int g_sms[16];
+
+size_t sum_plane_bytes(int n) {
+  return (size_t)((n + 63) / 64) * 64 * ((n + 15) / 16) * 16 * sizeof(double);
+}
 
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
-                  unsigned long long* cons, unsigned int* sync, int algo, cudaStream_t st) {
+                  unsigned long long* cons, unsigned int* sync, int algo, double* planes, cudaStream_t st) {
   FusedArgs f;
   memset(&f, 0, sizeof f);
   GemmArgs& g = f.g2;
@@ -702,12 +810,26 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
   f.a_out = a;
   f.next = sync;
   f.done = sync + 1;
+  if (algo == ALGO_3MS) {
+    if (!planes) return fail(ZT_EINVAL, "3M sum planes need workspace");
+    const size_t pe = sum_plane_bytes(n) / sizeof(double);
+    double *pa = planes, *pb = planes + pe, *xb = planes + 2 * pe, *aa = planes + 3 * pe;
+    f.pa1 = pa;
+    f.pb1 = xb;
+    f.pa2 = aa;
+    f.pb2 = pb;
+    const int kbt = (n + 15) / 16, cbt = (n + 63) / 64;
+    k_sum_planes<<<dim3(kbt * cbt, 3), 256, 0, st>>>(n, p, x, n, pa, pb, xb);
+    ZT_LAUNCHED();
+  }
   int dev;
   cudaGetDevice(&dev);
-  const int slot = algo == ALGO_4M ? 1 : 0;
+  const int slot = algo == ALGO_4M ? 1 : (algo == ALGO_3MS ? 2 : 0);
   if (dev < 16 && !g_fattr[dev][slot]) {
     if (algo == ALGO_4M)
       ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zupdate<ALGO_4M>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+    else if (algo == ALGO_3MS)
+      ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zupdate<ALGO_3MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_S));
     else
       ZT_CUDA_CHECK(cudaFuncSetAttribute(k_zupdate<ALGO_3M>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
     cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
@@ -719,6 +841,8 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
   ZT_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (T + 1), st));
   if (algo == ALGO_4M)
     k_zupdate<ALGO_4M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
+  else if (algo == ALGO_3MS)
+    k_zupdate<ALGO_3MS><<<grid, GEMM_THREADS, GEMM_SMEM_S, st>>>(f);
   else
     k_zupdate<ALGO_3M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
   ZT_LAUNCHED();
