@@ -400,7 +400,7 @@ def run_ours(args):
     achieved = alg / (g1_ms * 1e-3) / 1e12
     roofline = {
         "bound": "tensor",
-        "kernel": "k_zupdate<3M>: GEMM-1 a = P X + GEMM-2 b = a P (lower tiles) + fused update" if fused
+        "kernel": "k_zupdate<3M, sum planes>: GEMM-1 a = P X + GEMM-2 b = a P (lower tiles) + fused update" if fused
         else "k_zgemm<3M,STORE> (GEMM-1 a = P X)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": TRAFFIC_FUSED if fused else None,
@@ -455,7 +455,7 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-update launch at
 # N=2048 from the committed `ncu --set full` capture (profiles/r01_ncu_summary.md)
-TRAFFIC_FUSED = 915.75e6  # 787.35 MB read + 128.41 MB written (ncu --set full, profiles/r01_ncu_summary.md)
+TRAFFIC_FUSED = 1451.03e6  # 1286.38 MB read + 164.64 MB written (ncu --set full, profiles/r01_ncu_summary.md)
 
 
 def main():
