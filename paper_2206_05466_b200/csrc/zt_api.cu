@@ -140,8 +140,10 @@ static size_t g_used = 0;
 static double g_prof_ms[3] = {0, 0, 0};
 static int64_t g_prof_cnt[3] = {0, 0, 0};
 
+static thread_local bool t_capturing = false;
+
 static void prof_mark(int which, cudaStream_t st) {
-  if (!g_prof) return;
+  if (!g_prof || t_capturing) return;
   if (which == 0) {
     if (g_used == g_slots.size()) {
       ProfSlot s;
@@ -240,6 +242,168 @@ static int fixed_point_impl(zt_operator* op, const double* wn, double* x, double
   return fail(ZT_ENOCONV, buf);
 }
 
+// ---- CUDA-graph step: the fixed point as a conditional WHILE node ------------
+// Prologue (input gate, X <- W_n, counter reset) -> while(cond) { update;
+// decide } -> final update.  One graph launch and one 40-byte read-back per
+// step instead of a host round trip per fixed-point iteration.
+__global__ void k_fp_decide(unsigned long long* flags, double tol, int max_iter, cudaGraphConditionalHandle h) {
+  const unsigned long long bits = flags[0];
+  double r;
+  memcpy(&r, &bits, sizeof r);
+  const unsigned long long k = ++flags[2];
+  flags[3] = bits;  // last residual
+  // continue while not converged (NaN never converges, integrator.py:131)
+  cudaGraphSetConditional(h, (!(r <= tol) && (int)k < max_iter) ? 1u : 0u);
+}
+
+struct GraphEntry {
+  zt_operator* op;
+  int n;
+  const double* wn;
+  double* wnext;
+  void* ws;
+  double h, tol;
+  int max_iter;
+  bool cons;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kp = 0, kb = 0, ke = 0;  // kernels in prologue / per iteration / epilogue
+};
+static thread_local std::vector<GraphEntry> t_graphs;
+static thread_local cudaStream_t t_cap[2] = {nullptr, nullptr};
+static bool g_graph = true;  // ZT_GRAPH=0: eager step with per-iteration host sync
+
+static int build_step_graph(GraphEntry& e, StepWS& w) {
+  zt_operator* op = e.op;
+  const int n = op->n;
+  for (auto& s : t_cap)
+    if (!s) ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaStream_t cs = t_cap[0], cb = t_cap[1];
+  const double hh = 0.5 * e.h, qq = 0.25 * e.h * e.h;
+  double* x = e.wnext;
+  t_capturing = true;
+  int rc = ZT_OK;
+  cudaGraph_t graph = nullptr;
+  ZT_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  int64_t c0 = g_launches.load();
+  rc = residuals(n, e.wn, n, w.val, w.resid, cs);
+  if (!rc) rc = cudaMemcpyAsync(x, e.wn, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, cs) ? ZT_ECUDA : ZT_OK;
+  if (!rc) rc = cudaMemsetAsync(w.flags + 2, 0, sizeof(unsigned long long), cs) ? ZT_ECUDA : ZT_OK;
+  int64_t c1 = g_launches.load();
+  cudaGraphConditionalHandle hc;
+  if (!rc) {
+    cudaStreamCaptureStatus stt;
+    cudaGraph_t cg;
+    const cudaGraphNode_t* deps;
+    size_t nd;
+    cudaError_t ce = cudaStreamGetCaptureInfo(cs, &stt, nullptr, &cg, &deps, &nd);
+    if (!ce) ce = cudaGraphConditionalHandleCreate(&hc, cg, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hc;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    if (!ce) ce = cudaGraphAddNode(&cnode, cg, deps, nd, &cp);
+    if (!ce) ce = cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies);
+    cudaGraph_t body = cp.conditional.phGraph_out ? cp.conditional.phGraph_out[0] : nullptr;
+    if (!ce) ce = cudaStreamBeginCaptureToGraph(cb, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (ce) rc = cuda_fail(ce, "graph: conditional node");
+    if (!rc) {
+      rc = cudaMemsetAsync(w.flags, 0, sizeof(unsigned long long), cb) ? ZT_ECUDA : ZT_OK;
+      if (!rc) rc = update(op, x, e.wn, x, nullptr, x, hh, qq, w, w.flags, nullptr, cb);
+      if (!rc) {
+        k_fp_decide<<<1, 1, 0, cb>>>(w.flags, e.tol, e.max_iter, hc);
+        ZT_LAUNCHED();
+      }
+      cudaGraph_t bg;
+      cudaError_t ce2 = cudaStreamEndCapture(cb, &bg);
+      if (!rc && ce2) rc = cuda_fail(ce2, "graph: body capture");
+    }
+  }
+  int64_t c2 = g_launches.load();
+  if (!rc && e.cons) rc = cudaMemsetAsync(w.flags + 1, 0, sizeof(unsigned long long), cs) ? ZT_ECUDA : ZT_OK;
+  if (!rc)
+    rc = update(op, x, x, nullptr, e.cons ? e.wn : nullptr, x, hh, -qq, w, nullptr, e.cons ? w.flags + 1 : nullptr, cs);
+  int64_t c3 = g_launches.load();
+  cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+  t_capturing = false;
+  g_launches.fetch_sub(c3 - c0);  // captured, not executed
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce) return cuda_fail(ce, "graph: capture");
+  ce = cudaGraphInstantiate(&e.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce) return cuda_fail(ce, "graph: instantiate");
+  e.kp = c1 - c0;
+  e.kb = c2 - c1;
+  e.ke = c3 - c2;
+  return ZT_OK;
+}
+
+static int midpoint_step_graph(zt_operator* op, const double* wn, double* w_next, double h, double tol,
+                               int max_iter, StepWS& w, void* ws, int* iterations, double* residual,
+                               double* consistency, cudaStream_t st) {
+  if (!(h >= 0.0)) return fail(ZT_EINVAL, "time-step must be nonnegative, got " + std::to_string(h));
+  if (!(tol > 0.0)) return fail(ZT_EINVAL, "tolerance must be positive, got " + std::to_string(tol));
+  if (max_iter < 1) return fail(ZT_EINVAL, "max_iter must be at least 1, got " + std::to_string(max_iter));
+  if (!t_mail.h) return fail(ZT_ENOMEM, "pinned mailbox allocation failed");
+  const bool cons = consistency != nullptr;
+  GraphEntry* hit = nullptr;
+  for (auto& e : t_graphs)
+    if (e.op == op && e.n == op->n && e.wn == wn && e.wnext == w_next && e.ws == ws && e.h == h && e.tol == tol &&
+        e.max_iter == max_iter && e.cons == cons)
+      hit = &e;
+  if (!hit) {
+    if (t_graphs.size() >= 8) {
+      cudaGraphExecDestroy(t_graphs.front().exec);
+      t_graphs.erase(t_graphs.begin());
+    }
+    GraphEntry e;
+    e.op = op;
+    e.n = op->n;
+    e.wn = wn;
+    e.wnext = w_next;
+    e.ws = ws;
+    e.h = h;
+    e.tol = tol;
+    e.max_iter = max_iter;
+    e.cons = cons;
+    int rc = build_step_graph(e, w);
+    if (rc) return rc;
+    t_graphs.push_back(e);
+    hit = &t_graphs.back();
+  }
+  ZT_CUDA_CHECK(cudaGraphLaunch(hit->exec, st));
+  ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h, w.flags, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h + 8, w.val, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  ZT_CUDA_CHECK(cudaStreamSynchronize(st));
+  const int k = (int)t_mail.h[2];
+  g_launches.fetch_add(hit->kp + (int64_t)k * hit->kb + hit->ke);
+  const double sk = bits_to_double(t_mail.h[8]), tr = bits_to_double(t_mail.h[9]);
+  char buf[200];
+  if (sk > 1e-10) {
+    snprintf(buf, sizeof buf, "matrix is not skew-Hermitian: residual %.3e > 1.0e-10", sk);
+    return fail(ZT_ESTRUCTURE, buf);
+  }
+  if (tr > 1e-10) {
+    snprintf(buf, sizeof buf, "matrix is not traceless: residual %.3e > 1.0e-10", tr);
+    return fail(ZT_ESTRUCTURE, buf);
+  }
+  const double r = bits_to_double(t_mail.h[3]);
+  *iterations = k;
+  *residual = r;
+  if (!(r <= tol)) {
+    snprintf(buf, sizeof buf,
+             "fixed-point iteration did not reach tol=%.1e in %d iterations (last residual %.3e)", tol,
+             max_iter, r);
+    return fail(ZT_ENOCONV, buf);
+  }
+  if (cons) *consistency = bits_to_double(t_mail.h[1]);
+  return ZT_OK;
+}
+
 }  // namespace zt
 
 using namespace zt;
@@ -289,6 +453,7 @@ int zt_op_create(int n, int device, zt_op_t* op) {
   if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : 0;
   if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
+  if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
   return op_create(n, device, op);
 }
 int zt_op_destroy(zt_op_t op) { return op_destroy(op); }
@@ -383,6 +548,9 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
   cudaStream_t st = (cudaStream_t)stream;
   StepWS w;
   ws_layout(op->n, reinterpret_cast<char*>(workspace), &w);
+  if (g_graph && !g_prof)
+    return midpoint_step_graph(op, wn, w_next, h_eff, tol, max_iter, w, workspace, iterations, residual,
+                               consistency, st);
   int rc = fixed_point_impl(op, wn, w_next, h_eff, tol, max_iter, w, iterations, residual, st);
   if (rc) return rc;
   // final update (integrator.py:154-158): W_{n+1} = W~ + (h/2)(a - a^H) - (h^2/4) a P~
