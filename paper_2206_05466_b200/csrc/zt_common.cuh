@@ -24,15 +24,6 @@ struct zt_operator {
   double* m0x = nullptr;  // m = 0 per-chunk constant-RHS responses
   int2* gen_tiles = nullptr;  // (chunk, group) of the boundary tiles
   int ngen = 0;
-  int fast_blocks = 0;
-  bool solve_tma = false;
-  bool solve_amortize = true;
-  bool solve_merged = true;  // boundary + interior tiles in one launch per pass
-  int nside = 0;              // side streams for batched solves
-  cudaStream_t side[8] = {};
-  cudaEvent_t fork = nullptr, join[8] = {};
-  cudaStream_t gstream = nullptr;  // boundary tiles run here beside the interior tiles
-  cudaEvent_t gfork = nullptr, gjoin = nullptr;  // batch > 1: one factor chain per tile for all matrices  // interior tiles: persistent TMA-prefetch kernel vs direct loads  // resident blocks of the persistent interior-tile kernel
   void* block = nullptr;  // single allocation holding every table
 };
 

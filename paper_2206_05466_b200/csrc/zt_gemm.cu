@@ -69,7 +69,6 @@ constexpr int GEMM_SMEM_S = STAGES * (STAGE_BYTES + 2 * 1024 * 8) + (2 * STAGES 
 enum {
   ALGO_3M = 0,        // Gauss 3M, operand sums (re + im) formed per warp in registers
   ALGO_4M = 1,        // classical 4 real products
-  ALGO_3M_NOSUM = 2,  // timing experiment only: skips the sums (wrong results)
   ALGO_3MS = 3        // Gauss 3M, sums read from precomputed fragment-order sum planes
 };
 enum {
@@ -176,12 +175,10 @@ __device__ __forceinline__ void consume_stage(const unsigned char* st, Acc<ALGO>
       double bsum[WNB];
 #pragma unroll
       for (int j = 0; j < WNB; ++j)
-        bsum[j] = (ALGO == ALGO_3MS) ? sb[((ks * WN_WARPS + wn) * WNB + j) * 32 + lane]
-                                     : ((ALGO == ALGO_3M) ? bf[j].x + bf[j].y : bf[j].x);
+        bsum[j] = (ALGO == ALGO_3MS) ? sb[((ks * WN_WARPS + wn) * WNB + j) * 32 + lane] : bf[j].x + bf[j].y;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const double asum = (ALGO == ALGO_3MS) ? sa[((ks * 2 + wm) * 4 + i) * 32 + lane]
-                                               : ((ALGO == ALGO_3M) ? af[i].x + af[i].y : af[i].y);
+        const double asum = (ALGO == ALGO_3MS) ? sa[((ks * 2 + wm) * 4 + i) * 32 + lane] : af[i].x + af[i].y;
 #pragma unroll
         for (int j = 0; j < WNB; ++j) {
           dmma(A.v[0][i][j][0], A.v[0][i][j][1], af[i].x, bf[j].x);
@@ -692,7 +689,6 @@ int zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, dou
   g.ldc = ldc;
   const int T = (n + BM - 1) / BM;
   if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, T * T, st);
-  if (algo == ALGO_3M_NOSUM) return launch<ALGO_3M_NOSUM, EPI_STORE>(g, T * T, st);
   return launch<ALGO_3M, EPI_STORE>(g, T * T, st);
 }
 

@@ -41,12 +41,6 @@ constexpr int LPD = 64 / SUB;   // lanes per diagonal
 constexpr int DPW = 32 / LPD;  // diagonals per warp tile
 constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
-#ifndef SOLVE_DIRECT_MINB
-#define SOLVE_DIRECT_MINB 4
-#endif
-#ifndef SOLVE_FAST_MINB
-#define SOLVE_FAST_MINB 4
-#endif
 constexpr int TR = 32;  // rows per apply tile / diagonals per apply tile
 constexpr int M0X = 5;  // m = 0 per-chunk responses: Y1, X1, S1, SH, SK
 
@@ -214,8 +208,7 @@ static int solve_ntiles(int C) { return 4 * C * (C + 1); }
 template <bool FINAL, bool FAST, bool LAST = false>
 __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __restrict__ w,
                                           double* __restrict__ p, int b, int c, int m0, int lane,
-                                          double2* sm, const double2* vpre = nullptr,
-                                          bool do_factors = true, double2* xstage = nullptr) {
+                                          double2* sm) {
   const int n = A.n;
   const int i0 = c * SR;
   const int dl = lane % DPW, s = lane / DPW;
@@ -234,20 +227,13 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   const double* wp = w + ((int64_t)ib * A.ldw + (ib - m)) * 2;
 #define ROW_OK(r) (FAST || ((r) >= rs && (r) <= re))
 
-  // 1. loads (16 rows; each instruction covers 4 rows x 128 B), or the
-  // values already staged by TMA (FAST persistent path)
+  // 1. loads (16 rows; each instruction covers 4 rows x 128 B)
   double2 v[SUB];
-  if (FAST && vpre) {
 #pragma unroll
-    for (int r = 0; r < SUB; ++r) v[r] = vpre[r];
-  } else {
-#pragma unroll
-    for (int r = 0; r < SUB; ++r)
-      v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
-  }
+  for (int r = 0; r < SUB; ++r) v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
 
   // 2. factor chain from the exact sub-chunk pivot (dpttrf order, fast rcp)
-  if (has && do_factors) {
+  if (has) {
     if (!FAST && m == 0) {
 #pragma unroll
       for (int r = 0; r < SUB; ++r)
@@ -437,9 +423,8 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   }
 #undef ROW_OK
   __syncwarp();
-  // stage x for the transposed store (reuse the factor tile unless the
-  // caller keeps the factors for further right-hand sides)
-  double2* xs_buf = xstage ? xstage : sm;
+  // stage x for the transposed store (reuse the factor tile)
+  double2* xs_buf = sm;
 #pragma unroll
   for (int r = 0; r < SUB; ++r) xs_buf[(s * SUB + r) * DPW + dl] = v[r];
   __syncwarp();
@@ -484,98 +469,6 @@ static int fast_chunks(int n) {
 }
 static int fast_ntiles(int cf) { return (int)fast_prefix(cf); }
 
-// Persistent interior-tile kernel: each warp walks tiles id = gw, gw + nw,
-// ...; the next tile's 64 x 8 sheared block (8 KB) is fetched by TMA from a
-// 3D tensor map over W with row stride ld+1 while the current one is swept.
-constexpr int FAST_SMEM_PER_WARP = 2 * SR * DPW * (int)sizeof(double2);  // factors + staged tile
-
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_FAST_MINB)
-    k_solve_fast(const __grid_constant__ SolveArgs A, const __grid_constant__ CUtensorMap tw, int total) {
-  extern __shared__ __align__(128) unsigned char smem_dyn[];
-  // TMA destinations need 128 B alignment: align the dynamic base by hand
-  unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dyn) + 127) & ~(uintptr_t)127);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SOLVE_WARPS * FAST_SMEM_PER_WARP);
-  // independent of the boundary-tile launch of the same pass: let it start
-  asm volatile("griddepcontrol.launch_dependents;");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* sm = reinterpret_cast<double2*>(smem_raw + warp * FAST_SMEM_PER_WARP);
-  double2* vbuf = sm + SR * DPW;
-  if (lane == 0) {
-    mbar_init(&bar[warp], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const int nw = gridDim.x * SOLVE_WARPS;
-  int id = blockIdx.x * SOLVE_WARPS + warp;
-  const int n = A.n;
-  auto issue = [&](int tid) {
-    const int bb = tid / A.ntiles;
-    int c, g;
-    fast_tile_coords(tid - bb * A.ntiles, c, g);
-    mbar_arrive_expect_tx(&bar[warp], SR * DPW * 16);
-    tma_3d(vbuf, &tw, 2 * (n - DPW - g * DPW), c * SR, bb, &bar[warp]);
-  };
-  if (id < total && lane == 0) issue(id);
-  uint32_t phase = 0;
-  while (id < total) {
-    const int b = id / A.ntiles;
-    int c, g;
-    fast_tile_coords(id - b * A.ntiles, c, g);
-    mbar_wait(&bar[warp], phase);
-    phase ^= 1;
-    double2 vv[SUB];
-    {
-      const int dl = lane % DPW, s = lane / DPW;
-#pragma unroll
-      for (int r = 0; r < SUB; ++r) vv[r] = vbuf[(s * SUB + r) * DPW + (DPW - 1 - dl)];
-    }
-    // all lanes' reads of vbuf precede the next async-proxy write into it
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    const int nid = id + nw;
-    if (nid < total && lane == 0) issue(nid);  // refill while this tile is swept
-    tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane,
-                           sm, vv);
-    id = nid;
-  }
-}
-
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_DIRECT_MINB) k_solve_fast_direct(SolveArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  asm volatile("griddepcontrol.launch_dependents;");
-  const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * SOLVE_WARPS + warp;
-  if (t >= A.ntiles) return;
-  int c, g;
-  fast_tile_coords(t, c, g);
-  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
-  tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane, sm);
-}
-
-// Batched interior tiles: the LDL^T factors of a tile do not depend on the
-// right-hand side, so they are generated once and reused for every matrix
-// of the batch (config 2: 8 matrices share each factor chain).
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, SOLVE_DIRECT_MINB) k_solve_fast_batch(SolveArgs A, int batch) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  asm volatile("griddepcontrol.launch_dependents;");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * SOLVE_WARPS + warp;
-  if (t >= A.ntiles) return;
-  int c, g;
-  fast_tile_coords(t, c, g);
-  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW * (FINAL ? 2 : 1);
-  double2* xstage = FINAL ? sm + SR * DPW : nullptr;
-  for (int b = 0; b < batch; ++b) {
-    tile_body<FINAL, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, g * DPW, lane, sm,
-                           nullptr, b == 0, xstage);
-  }
-}
-
 // One launch for a whole tile pass: blocks [0, gblocks) take the boundary
 // tiles (dispatched first, so their latency hides under the interior tiles
 // that follow), the rest the interior tiles.
@@ -604,22 +497,6 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4)
     fast_tile_coords(t, c, g);
     tile_body<FINAL, true>(A, w, p, b, c, g * DPW, lane, sm);
   }
-}
-
-template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4) k_solve_generic(SolveArgs A, const int2* __restrict__ tiles, int count) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * SOLVE_WARPS + warp;
-  if (t >= count) return;
-  const int2 cg = tiles[t];
-  double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
-  const int c = cg.x & ~(1 << 30);
-  if (cg.x & (1 << 30))
-    tile_body<FINAL, true, true>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, cg.y * DPW, lane, sm);
-  else
-    tile_body<FINAL, false>(A, A.w + (size_t)b * A.sw * 2, A.p + (size_t)b * A.sp * 2, b, c, cg.y * DPW, lane, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -1003,40 +880,9 @@ int op_create(int n, int device, zt_operator** out) {
   ZT_LAUNCHED();
   int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   int asmem = SOLVE_WARPS * TR * 32 * (int)sizeof(double2);
-  cudaFuncSetAttribute(k_solve_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
-  cudaFuncSetAttribute(k_solve_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
-  cudaFuncSetAttribute(k_solve_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_fast_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_merged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_merged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_fast_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_fast_batch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_solve_fast_batch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * smem);
-  {
-    const char* e = getenv("ZT_SOLVE_FAST");
-    op->solve_tma = e && std::string(e) == "tma";
-    op->solve_amortize = e && std::string(e) == "batch";
-    op->solve_merged = !(e && (std::string(e) == "split" || std::string(e) == "batch"));
-  }
-  cudaFuncSetAttribute(k_solve_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
-  {
-    const char* e = getenv("ZT_SOLVE_STREAMS");
-    op->nside = e ? std::max(1, std::min(8, atoi(e))) : 1;
-    for (int q = 0; q < op->nside; ++q) cudaStreamCreateWithFlags(&op->side[q], cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&op->gstream, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&op->gfork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&op->gjoin, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming);
-    for (int q = 0; q < op->nside; ++q) cudaEventCreateWithFlags(&op->join[q], cudaEventDisableTiming);
-  }
-  {
-    int nb = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_fast<true>, SOLVE_WARPS * 32,
-                                                  SOLVE_WARPS * FAST_SMEM_PER_WARP + 256);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    op->fast_blocks = std::max(1, nb) * std::max(1, sms);
-  }
   e = cudaDeviceSynchronize();
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
@@ -1050,14 +896,6 @@ int op_create(int n, int device, zt_operator** out) {
 
 int op_destroy(zt_operator* op) {
   if (!op) return ZT_OK;
-  for (int q = 0; q < op->nside; ++q) {
-    cudaStreamDestroy(op->side[q]);
-    cudaEventDestroy(op->join[q]);
-  }
-  if (op->fork) cudaEventDestroy(op->fork);
-  if (op->gstream) cudaStreamDestroy(op->gstream);
-  if (op->gfork) cudaEventDestroy(op->gfork);
-  if (op->gjoin) cudaEventDestroy(op->gjoin);
   cudaFree(op->block);
   delete op;
   return ZT_OK;
@@ -1067,25 +905,6 @@ size_t solve_workspace_bytes(int n, int batch) {
   const int C = (n + SR - 1) / SR;
   const size_t one = ((2 * (size_t)C * n + 2 * (size_t)C + 2) * sizeof(double2) + 511) & ~(size_t)255;
   return one * batch;
-}
-
-// Launch a generic-tile kernel; with `pdl` it may start while the preceding
-// interior-tile kernel of the same pass is still running (they touch
-// disjoint tiles; the preceding kernel signals launch_dependents at entry).
-static cudaError_t launch_pdl(const void* fn, dim3 grid, int smem, cudaStream_t st, SolveArgs A,
-                              const int2* tiles, int count, bool pdl) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(SOLVE_WARPS * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
-  void* args[] = {&A, (void*)&tiles, &count};
-  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p,
@@ -1115,64 +934,17 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
   A.m0mg = A.m0acc + (size_t)batch * C * 2;
   const int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
   A.ntiles = fast_ntiles(fast_chunks(n));
-  const int total = A.ntiles * batch;
-  const int tf = total > 0 ? std::min((total + SOLVE_WARPS - 1) / SOLVE_WARPS, op->fast_blocks) : 0;
   const int tg = (op->ngen + SOLVE_WARPS - 1) / SOLVE_WARPS;
-  CUtensorMap tw;
-  if (tf > 0) {
-    // sheared 3D view of W: element (x, i, b) = W_b[i][i - (N-1-x/2)], row stride ld+1
-    if ((reinterpret_cast<uintptr_t>(w) & 15) || ((ldw + 1) * 16) % 16) return fail(ZT_EINVAL, "solve: W must be 16B aligned");
-    cuuint64_t dims[3] = {(cuuint64_t)2 * n, (cuuint64_t)n, (cuuint64_t)batch};
-    cuuint64_t strides[2] = {(cuuint64_t)(ldw + 1) * 16, (cuuint64_t)std::max<int64_t>(sw, 1) * 16};
-    cuuint32_t box[3] = {2 * DPW, SR, 1};
-    int rc = encode_tiled_f64(&tw, 3, w - 2 * (int64_t)(n - 1), dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
-    if (rc) return rc;
-  }
-  const int fsm = SOLVE_WARPS * FAST_SMEM_PER_WARP + 256;
-  // Each tile pass: the boundary tiles (few, latency bound) start first on
-  // the operator's side stream and run beside the interior tiles on the
-  // caller's stream (fork/join events; graph-capturable).
   const int td = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
+  // one launch per tile pass: boundary tiles first (dispatched first, their
+  // latency hides under the interior tiles), then the interior tiles
   auto pass = [&](bool fin) -> int {
-    if (op->solve_merged && !op->solve_tma) {
-      const dim3 grid(tg + td, batch);
-      if (fin)
-        k_solve_merged<true><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
-      else
-        k_solve_merged<false><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
-      ZT_LAUNCHED();
-      return ZT_OK;
-    }
-    ZT_CUDA_CHECK(cudaEventRecord(op->gfork, st));
-    ZT_CUDA_CHECK(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
-    if (op->ngen > 0) {
-      if (fin)
-        k_solve_generic<true><<<dim3(tg, batch), SOLVE_WARPS * 32, smem, op->gstream>>>(A, op->gen_tiles, op->ngen);
-      else
-        k_solve_generic<false><<<dim3(tg, batch), SOLVE_WARPS * 32, smem, op->gstream>>>(A, op->gen_tiles, op->ngen);
-      ZT_LAUNCHED();
-    }
-    if (tf > 0) {
-      if (op->solve_tma) {
-        if (fin)
-          k_solve_fast<true><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
-        else
-          k_solve_fast<false><<<tf, SOLVE_WARPS * 32, fsm, st>>>(A, tw, total);
-      } else if (batch > 1 && op->solve_amortize) {
-        if (fin)
-          k_solve_fast_batch<true><<<td, SOLVE_WARPS * 32, 2 * smem, st>>>(A, batch);
-        else
-          k_solve_fast_batch<false><<<td, SOLVE_WARPS * 32, smem, st>>>(A, batch);
-      } else {
-        if (fin)
-          k_solve_fast_direct<true><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
-        else
-          k_solve_fast_direct<false><<<dim3(td, batch), SOLVE_WARPS * 32, smem, st>>>(A);
-      }
-      ZT_LAUNCHED();
-    }
-    ZT_CUDA_CHECK(cudaEventRecord(op->gjoin, op->gstream));
-    ZT_CUDA_CHECK(cudaStreamWaitEvent(st, op->gjoin, 0));
+    const dim3 grid(tg + td, batch);
+    if (fin)
+      k_solve_merged<true><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
+    else
+      k_solve_merged<false><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
+    ZT_LAUNCHED();
     return ZT_OK;
   };
   int rc = pass(false);
@@ -1191,29 +963,9 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
   return ZT_OK;
 }
 
-// Batched solve: matrices are pipelined over the operator's side streams
-// (fork/join with events, graph-capturable) so that one matrix's
-// compute-heavy pass 1 overlaps another's bandwidth-heavy pass 3.
 int stream_solve(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p, int64_t ldp,
                  int64_t sp, int batch, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int S = op->nside;
-  if (batch <= 1 || S <= 1)
-    return stream_solve_one(op, w, ldw, sw, p, ldp, sp, batch, ws, ws_bytes, st);
-  const size_t per = solve_workspace_bytes(op->n, 1);
-  if (ws_bytes < per * batch) return fail(ZT_ENOMEM, "solve workspace too small");
-  ZT_CUDA_CHECK(cudaEventRecord(op->fork, st));
-  for (int q = 0; q < S && q < batch; ++q) ZT_CUDA_CHECK(cudaStreamWaitEvent(op->side[q], op->fork, 0));
-  for (int b = 0; b < batch; ++b) {
-    cudaStream_t ss = op->side[b % S];
-    int rc = stream_solve_one(op, w + (size_t)b * sw * 2, ldw, 0, p + (size_t)b * sp * 2, ldp, 0, 1,
-                              static_cast<char*>(ws) + per * b, per, ss);
-    if (rc) return rc;
-  }
-  for (int q = 0; q < S && q < batch; ++q) {
-    ZT_CUDA_CHECK(cudaEventRecord(op->join[q], op->side[q]));
-    ZT_CUDA_CHECK(cudaStreamWaitEvent(st, op->join[q], 0));
-  }
-  return ZT_OK;
+  return stream_solve_one(op, w, ldw, sw, p, ldp, sp, batch, ws, ws_bytes, st);
 }
 
 int apply_laplacian(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* y,
