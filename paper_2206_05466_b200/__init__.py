@@ -6,6 +6,7 @@ by hand-written sm_100a kernels in ``libzt.so`` (C ABI: include/zt.h).
 """
 
 from .diagnostics import hamiltonian
+from .driver import Checkpoint, DeviceRun, FileFormatError, read_checkpoint, write_checkpoint
 from .integrator import (
     FixedPointError,
     StepInfo,
@@ -39,4 +40,5 @@ __all__ = [
     "midpoint_step_info", "LaplacianBlock", "LaplacianOperator", "StructureError",
     "apply_laplacian", "build_block", "build_operator", "skewness_residual", "solve_stream",
     "solve_stream_batched", "spectral_norm", "trace_residual", "validate_vorticity", "hamiltonian",
+    "Checkpoint", "DeviceRun", "FileFormatError", "read_checkpoint", "write_checkpoint",
 ]

@@ -1,0 +1,209 @@
+"""Device-resident run loop, on-device sample-time diagnostics and ZCK1
+checkpoints (the caller of the hot path and its
+on-disk state format).
+
+The reference's driver (/root/reference/pkg/src/zeitlin/driver.py:284-410)
+copies W to the host at every sample; here W stays in HBM for the whole run:
+the step is one CUDA graph per step, and the sample-time quantities are
+computed on the device — Casimirs C_2..C_kmax (integrator.py:180-210, DMMA
+GEMMs), the energy H (diagnostics.py:60-63, stream solve + vdot) and their
+drift (diagnostics.py:86-110).  Only checkpoints leave the device.
+
+Checkpoints use the reference's ZCK1 layout byte for byte
+(formats.py:116-156): magic "ZCK1", `<IIQdQI` = version, N, step, time, seed,
+rng-blob length, the rng blob, then the N^2 complex128 entries in
+column-major order — produced by a device-side transpose before the single
+device-to-host copy.  Runs are bitwise deterministic, so a run resumed from a
+checkpoint reproduces the uninterrupted run's checkpoints and diagnostics
+byte for byte (the reference's test_driver.py:231-248 contract).
+
+Out of scope here (they need the spherical-harmonic basis):
+the energy spectrum files, the basis-derived kinetic energy K (written as
+the trace-form energy, equal to it up to round-off per diagnostics.py:8-12),
+grid snapshots, the config file and CLI.
+"""
+
+from __future__ import annotations
+
+import json
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from .diagnostics import hamiltonian
+from .integrator import StepperState, casimirs, midpoint_step_raw
+from .laplacian import build_operator
+
+CHECKPOINT_MAGIC = b"ZCK1"
+FORMAT_VERSION = 1
+CASIMIR_BASELINE_FLOOR = 1e-14  # diagnostics.py:38-40
+
+
+class FileFormatError(ValueError):
+    """formats.py:49-50."""
+
+
+def format_float(x: float) -> str:
+    """%.17g, formats.py:55-56."""
+    return f"{float(x):.17g}"
+
+
+@dataclass
+class Checkpoint:
+    step_index: int
+    time: float
+    n: int
+    seed: int
+    rng_state: bytes
+    w: torch.Tensor  # on device
+
+
+def _atomic_write(path: Path, payload: bytes) -> None:
+    tmp = path.with_name(path.name + ".tmp")
+    tmp.write_bytes(payload)
+    tmp.replace(path)
+
+
+def write_checkpoint(path, cp: Checkpoint) -> None:
+    """ZCK1 writer (formats.py:130-143): column-major body from a device transpose."""
+    n = cp.w.shape[0]
+    header = CHECKPOINT_MAGIC + struct.pack(
+        "<IIQdQI", FORMAT_VERSION, n, cp.step_index, cp.time, cp.seed, len(cp.rng_state))
+    body = cp.w.transpose(0, 1).contiguous().cpu().numpy().astype("<c16").tobytes()
+    _atomic_write(Path(path), header + cp.rng_state + body)
+
+
+def read_checkpoint(path, device=None) -> Checkpoint:
+    """ZCK1 reader (formats.py:146-156) onto the device."""
+    with open(path, "rb") as fh:
+        if fh.read(4) != CHECKPOINT_MAGIC:
+            raise FileFormatError(f"{path}: bad magic, expected {CHECKPOINT_MAGIC!r}")
+        head = fh.read(36)
+        if len(head) != 36:
+            raise FileFormatError("truncated file while reading header")
+        version, n, step, time, seed, blob_len = struct.unpack("<IIQdQI", head)
+        if version != FORMAT_VERSION:
+            raise FileFormatError(f"{path}: unsupported version {version}")
+        rng_state = fh.read(blob_len)
+        raw = fh.read(16 * n * n)
+        if len(rng_state) != blob_len or len(raw) != 16 * n * n:
+            raise FileFormatError("truncated file while reading state entries")
+        if fh.read(1):
+            raise FileFormatError(f"{path}: trailing bytes after state entries")
+    wt = torch.from_numpy(np.frombuffer(raw, dtype="<c16").reshape(n, n).copy())
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    w = wt.to(dev).transpose(0, 1).contiguous()  # column-major on disk (device transpose)
+    return Checkpoint(step_index=step, time=time, n=n, seed=seed, rng_state=rng_state, w=w)
+
+
+def casimir_drift(c0: np.ndarray, ck: np.ndarray) -> np.ndarray:
+    """diagnostics.py:86-110 for one sample: |C_k - C_k(0)| / |C_k(0)|, k >= 2,
+    absolute error where the baseline is below 1e-14."""
+    base = np.asarray(c0, dtype=np.float64)[1:]
+    denom = np.where(np.abs(base) < CASIMIR_BASELINE_FLOOR, 1.0, np.abs(base))
+    return np.abs(np.asarray(ck, dtype=np.float64)[1:] - base) / denom
+
+
+class DeviceRun:
+    """Device-resident time stepping with sample / checkpoint cadence
+    (driver.py:357-410 without the basis-dependent outputs)."""
+
+    def __init__(self, state: StepperState, output_dir, k_max: int = 3, sample_every: int = 10,
+                 checkpoint_every: int = 100, seed: int = 0, rng_state: bytes = b"",
+                 baseline: np.ndarray | None = None):
+        w = state.w if isinstance(state.w, torch.Tensor) else torch.from_numpy(np.asarray(state.w))
+        if not w.is_cuda:
+            w = w.to(torch.device("cuda", torch.cuda.current_device()))
+        self.w = w.to(torch.complex128).contiguous()
+        self.spare = torch.empty_like(self.w)
+        self.state = state
+        self.n = self.w.shape[0]
+        self.op = build_operator(self.n, self.w.device)
+        self.out = Path(output_dir)
+        self.out.mkdir(parents=True, exist_ok=True)
+        self.k_max = k_max
+        self.sample_every = sample_every
+        self.checkpoint_every = checkpoint_every
+        self.seed = seed
+        self.rng_state = rng_state
+        self.baseline = casimirs(self.w, k_max) if baseline is None else np.asarray(baseline)
+        self.diag_path = self.out / "diagnostics.csv"
+        self.meta_path = self.out / "run_meta.json"
+        self.iterations: list[int] = []
+
+    # -- files ---------------------------------------------------------------
+    def start(self) -> None:
+        """Fresh run: metadata, header, the t = 0 sample and checkpoint (driver.py:336-392)."""
+        meta = {"version": 1, "n": self.n, "seed": self.seed, "h": float(self.state.h).hex(),
+                "k_max": self.k_max, "casimir_baseline": [float(c).hex() for c in self.baseline]}
+        self.meta_path.write_text(json.dumps(meta, indent=1) + "\n")
+        header = ",".join(["time", "H", "K"] + [f"C{k}_rel" for k in range(2, self.k_max + 1)])
+        self.diag_path.write_text(header + "\n")
+        self.sample()
+        self.checkpoint()
+
+    @classmethod
+    def resume(cls, checkpoint_path, output_dir, k_max=3, sample_every=10, checkpoint_every=100,
+               tol=1e-12, max_iter=10, comm_scale=1.0):
+        """Resume from a ZCK1 checkpoint and the run's run_meta.json (driver.py:300-334)."""
+        out = Path(output_dir)
+        meta_path, diag_path = out / "run_meta.json", out / "diagnostics.csv"
+        if not meta_path.exists():
+            raise ValueError(f"resume requires {meta_path} from the original run directory")
+        if not diag_path.exists():
+            raise FileFormatError(f"{diag_path}: missing diagnostics file for resume")
+        meta = json.loads(meta_path.read_text())
+        cp = read_checkpoint(checkpoint_path)
+        if meta.get("n") != cp.n or meta.get("seed") != cp.seed:
+            raise ValueError(f"{meta_path} does not match checkpoint (N={cp.n}, seed={cp.seed})")
+        h = float.fromhex(meta["h"])
+        baseline = np.array([float.fromhex(s) for s in meta["casimir_baseline"]])
+        if baseline.size != k_max:
+            raise ValueError(f"{meta_path} stores k_max={baseline.size}, asked for {k_max}")
+        st = StepperState(w=cp.w, h=h, time=cp.time, step_index=cp.step_index, tol=tol,
+                          max_iter=max_iter, comm_scale=comm_scale)
+        run = cls(st, out, k_max=k_max, sample_every=sample_every, checkpoint_every=checkpoint_every,
+                  seed=cp.seed, rng_state=cp.rng_state, baseline=baseline)
+        # drop diagnostics rows after the resume point (driver.py:241-252)
+        lines = run.diag_path.read_text().splitlines()
+        kept = [lines[0]] + [ln for ln in lines[1:]
+                             if ln and float(ln.split(",", 1)[0]) <= cp.time + 0.5 * h]
+        run.diag_path.write_text("\n".join(kept) + "\n")
+        return run
+
+    def sample(self) -> float:
+        """On-device Casimirs and energy at the current state (driver.py:357-376)."""
+        ck = casimirs(self.w, self.k_max)
+        h_val = hamiltonian(self.w, self.op)
+        row = [format_float(self.state.time), format_float(h_val), format_float(h_val)]
+        row += [format_float(v) for v in casimir_drift(self.baseline, ck)]
+        with open(self.diag_path, "a", encoding="utf-8") as fh:
+            fh.write(",".join(row) + "\n")
+        return h_val
+
+    def checkpoint(self) -> Path:
+        path = self.out / f"checkpoint_{self.state.step_index:08d}.zck"
+        write_checkpoint(path, Checkpoint(self.state.step_index, self.state.time, self.n, self.seed,
+                                          self.rng_state, self.w))
+        return path
+
+    # -- stepping ------------------------------------------------------------
+    def advance(self, steps: int) -> None:
+        """Step to `steps` (absolute step index), sampling / checkpointing at cadence."""
+        st = self.state
+        h_eff = st.h * st.comm_scale
+        while st.step_index < steps:
+            nxt, k, _, _ = midpoint_step_raw(self.w, h_eff, st.tol, st.max_iter, self.op, out=self.spare)
+            self.w, self.spare = nxt, self.w
+            st.time = st.time + st.h
+            st.step_index += 1
+            self.iterations.append(k)
+            final = st.step_index == steps
+            if st.step_index % self.sample_every == 0 or final:
+                self.sample()
+            if st.step_index % self.checkpoint_every == 0 or final:
+                self.checkpoint()
+        st.w = self.w

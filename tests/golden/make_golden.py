@@ -175,7 +175,18 @@ def modes():
     np.savez_compressed(os.path.join(OUT, "modes.npz"), **d)
 
 
+def checkpoint():
+    """A ZCK1 file written by the reference's own writer (formats.py:130-143)."""
+    from zeitlin.formats import Checkpoint, write_checkpoint
+
+    w = random_admissible(8, np.random.default_rng(8), 0.5)
+    cp = Checkpoint(step_index=37, time=0.185, n=8, seed=1234, rng_state=b'{"state": 1}', w=w)
+    write_checkpoint(os.path.join(OUT, "ck_n8.zck"), cp)
+    np.save(os.path.join(OUT, "ck_n8_w.npy"), w)
+
+
 if __name__ == "__main__":
+    checkpoint()
     modes()
     solve_small()
     cfg1()
