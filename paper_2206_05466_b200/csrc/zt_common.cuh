@@ -17,6 +17,7 @@ struct zt_operator {
   double* L0 = nullptr;
   double* dinv0 = nullptr;
   double* d0 = nullptr;
+  double* lins = nullptr;  // L of the row before every 16-row sub-chunk start
   double* lin = nullptr;
   double* G = nullptr;
   double* H = nullptr;

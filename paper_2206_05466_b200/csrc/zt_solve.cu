@@ -58,14 +58,16 @@ __global__ void k_op_sqrt_table(int n, double* sqB, double* Bq) {
   }
 }
 
-__global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double* d0s, double* lin,
-                           double* G, double* H, double* K, double* L0, double* dinv0, double* m0x) {
+__global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double* d0s, double* lins,
+                           double* lin, double* G, double* H, double* K, double* L0, double* dinv0,
+                           double* m0x) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   const int len = n - m;
   double d = block_diag(n, m, 0);
   double Lprev = 0.0;
   double Lc[SR], Dc[SR], g[SR], z[SR], hh[SR];
+  double Lrow = 0.0;  // L of the previous row
   int k = 0;
   // m = 0 is deflated to its leading (N-1) block; row N-1 is the gauge row
   const int last = (m == 0) ? n - 2 : len - 1;  // last factored row
@@ -77,7 +79,10 @@ __global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double*
     const double lin_c = (k0 == 0) ? 0.0 : Lprev;
     lin[(size_t)c * n + m] = lin_c;
     for (int r = 0; r < cnt; ++r, ++k) {
-      if ((m + k) % SUB == 0 || r == 0) d0s[(size_t)((m + k) / SUB) * n + m] = d;
+      if ((m + k) % SUB == 0 || r == 0) {
+        d0s[(size_t)((m + k) / SUB) * n + m] = d;
+        lins[(size_t)((m + k) / SUB) * n + m] = Lrow;
+      }
       if (k <= last) {
         Dc[r] = __drcp_rn(d);
         if (k < last) {
@@ -92,6 +97,7 @@ __global__ void k_op_build(int n, int C, const double* __restrict__ sqB, double*
         Dc[r] = 0.0;
         Lc[r] = 0.0;
       }
+      Lrow = Lc[r];
       if (m == 0) {
         L0[k] = Lc[r];
         dinv0[k] = Dc[r];
@@ -149,6 +155,19 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, e, r);
 }
 
+// sqrt of an exact integer-valued double (< 2^53): rsqrt seed, one Goldschmidt
+// step and a residual correction (~1 ulp).  Used for the block off-diagonal
+// e = -sqrt(B(i) B(k)) so the interior tiles read no factor tables per row.
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double y = x * r, h = 0.5 * r;
+  const double t = fma(-y, h, 0.5);
+  y = fma(y, t, y);
+  h = fma(h, t, h);
+  return fma(fma(-y, y, x), h, y);
+}
+
 // ---------------------------------------------------------------------------
 // chunk tiles: warp = 8 diagonals x 64 rows; lane (d = lane & 7,
 // s = lane >> 3) owns rows [16 s, 16 s + 16) of diagonal m0 + d.
@@ -159,6 +178,7 @@ struct SolveArgs {
   const double* sqB;
   const double* Bq;  // (j+1)(N-1-j), exact
   const double* d0s;
+  const double* lins;
   const double* lin;
   const double* L0;
   const double* dinv0;
@@ -231,6 +251,8 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   double2 v[SUB];
 #pragma unroll
   for (int r = 0; r < SUB; ++r) v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
+  const double2 ych = (FINAL && mok) ? __ldcg(A.yend + cm) : make_double2(0.0, 0.0);
+  const double2 xch = (FINAL && mok) ? __ldcg(A.xst + cm) : make_double2(0.0, 0.0);
 
   // 2. factor chain from the exact sub-chunk pivot (dpttrf order, fast rcp)
   if (has) {
@@ -281,8 +303,8 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
 
   double2 mu = make_double2(0.0, 0.0), gauge = make_double2(0.0, 0.0);
   if (!FAST && FINAL && m == 0) {
-    mu = A.m0mg[2 * b];
-    gauge = A.m0mg[2 * b + 1];
+    mu = __ldcg(A.m0mg + 2 * b);
+    gauge = __ldcg(A.m0mg + 2 * b + 1);
   }
   // 3. forward sweep with zero carry (laplacian.py:280-287) -> affine map
   double2 tb = make_double2(0.0, 0.0);
@@ -321,7 +343,6 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
     exm.a = make_double2(0.0, 0.0);
     exm.g = 1.0;
   }
-  const double2 ych = (FINAL && mok) ? A.yend[cm] : make_double2(0.0, 0.0);
   const double2 yin = make_double2(fma(exm.g, ych.x, exm.a.x), fma(exm.g, ych.y, exm.a.y));
   if (!FINAL && s == LPD - 1 && mok) A.yend[cm] = inc.a;  // chunk forward aggregate (zero carry)
   // 5. forward fix-up: y(r) += g(r) y_in, g(r) = prod(-L) from the segment start
@@ -368,7 +389,6 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
     rex.a = make_double2(0.0, 0.0);
     rex.g = 1.0;
   }
-  const double2 xch = (FINAL && mok) ? A.xst[cm] : make_double2(0.0, 0.0);
   const double2 xin = make_double2(fma(rex.g, xch.x, rex.a.x), fma(rex.g, xch.y, rex.a.y));
   if (!FINAL) {
     if (s == 0 && mok) A.xst[cm] = rinc.a;  // chunk backward aggregate (zero carries)
@@ -445,6 +465,94 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   }
 }
 
+
+
+// Pass-1 body of the interior tiles: one ascending loop runs the factor
+// chain, the zero-carry forward sweep and (by linearity) the zero-carry
+// backward start, so nothing is stored per row; the block entries come from
+// exact integer recurrences (B(j+1) = B(j) + N - 3 - 2j) and fast_sqrt
+// instead of table loads.  The shared-memory form was L1-bound here (ncu:
+// L1/TEX 93% busy at 47% of DRAM on per-row table loads and factor round
+// trips).
+__device__ __forceinline__ void agg_body(const SolveArgs& A, const double* __restrict__ w, int b, int c,
+                                         int m0, int lane) {
+  const int n = A.n;
+  const int i0 = c * SR;
+  const int dl = lane % DPW, s = lane / DPW;
+  const int m = m0 + dl;
+  const int ib = i0 + s * SUB;
+  const int k0 = ib - m;  // >= 1 on interior tiles
+  const size_t cm = (size_t)b * A.C * n + (size_t)c * n + m;
+  const int64_t wstride = (A.ldw + 1) * 2;
+  const double* wp = w + ((int64_t)ib * A.ldw + k0) * 2;
+
+  double2 v[SUB];
+#pragma unroll
+  for (int r = 0; r < SUB; ++r) v[r] = ld2(wp + r * wstride);
+
+  const size_t sub = (size_t)(ib / SUB) * n + m;
+  double qm1 = 1.0, q0 = A.d0s[sub];
+  const double Lin = A.lins[sub];
+  double dg = block_diag(n, m, k0);
+  double inc = 2.0 * (double)(n - 2 - 2 * k0 - m);
+  double bi = (ib + 1.0) * (double)(n - 1 - ib), dbi = (double)(n - 3 - 2 * ib);
+  double bk = (k0 + 1.0) * (double)(n - 1 - k0), dbk = (double)(n - 3 - 2 * k0);
+  // factor chain fused with the zero-carry forward sweep (laplacian.py:280-287);
+  // the segment's zero-carry backward start is accumulated on the way up:
+  // x(0) = sum_r P_r D_r y(r) + P_SUB x_in with P_r = prod_{j<r} (-L_j), and
+  // its response to the segment's incoming y is ks = sum_r P_r D_r g(r)
+  AffW fm;
+  fm.a = make_double2(0.0, 0.0);
+  fm.g = 1.0;
+  double2 bl = make_double2(0.0, 0.0);
+  double ks = 0.0, P = 1.0;
+  double Lp = Lin;
+#pragma unroll
+  for (int r = 0; r < SUB; ++r) {
+    const double di = qm1 * fast_rcp(q0);
+    const double e2 = bi * bk;
+    const double L = -fast_sqrt(e2) * di;
+    dg += inc;
+    inc -= 4.0;
+    const double q1 = fma(dg, q0, -e2 * qm1);
+    qm1 = q0;
+    q0 = q1;
+    bi += dbi;
+    dbi -= 2.0;
+    bk += dbk;
+    dbk -= 2.0;
+    fm.a = make_double2(fma(-Lp, fm.a.x, v[r].x), fma(-Lp, fm.a.y, v[r].y));
+    fm.g = -Lp * fm.g;
+    const double cf = P * di;
+    bl = make_double2(fma(cf, fm.a.x, bl.x), fma(cf, fm.a.y, bl.y));
+    ks = fma(cf, fm.g, ks);
+    P = -L * P;
+    Lp = L;
+  }
+  AffW incf = fm;
+#pragma unroll
+  for (int step = 1; step < LPD; step <<= 1) {
+    AffW o = aff_shfl(incf, max(lane - step * DPW, 0));
+    if (s >= step) incf = aff_compose(o, incf);
+  }
+  AffW exm = aff_shfl(incf, max(lane - DPW, 0));
+  if (s == 0) {
+    exm.a = make_double2(0.0, 0.0);
+    exm.g = 1.0;
+  }
+  // segment backward map with zero chunk carries: a = Back(y_loc + g exm.a)(0)
+  AffW bm;
+  bm.a = make_double2(fma(ks, exm.a.x, bl.x), fma(ks, exm.a.y, bl.y));
+  bm.g = P;
+#pragma unroll
+  for (int step = 1; step < LPD; step <<= 1) {
+    AffW o = aff_shfl(bm, min(lane + step * DPW, 31));
+    if (s + step <= LPD - 1) bm = aff_compose(o, bm);
+  }
+  if (s == LPD - 1) A.yend[cm] = incf.a;  // chunk forward aggregate (zero carry)
+  if (s == 0) A.xst[cm] = bm.a;           // chunk backward aggregate (zero carries)
+}
+
 // Interior tiles: chunks c < Cf (the chunk ends before row n-2), groups
 // g = 1 .. GPC*c-1 with GPC = SR/DPW groups per chunk height (all DPW
 // diagonals start before the chunk).  Count per chunk GPC*c-1, prefix
@@ -472,8 +580,14 @@ static int fast_ntiles(int cf) { return (int)fast_prefix(cf); }
 // One launch for a whole tile pass: blocks [0, gblocks) take the boundary
 // tiles (dispatched first, so their latency hides under the interior tiles
 // that follow), the rest the interior tiles.
+#ifndef SOLVE_MINB_AGG
+#define SOLVE_MINB_AGG 4
+#endif
+#ifndef SOLVE_MINB_FIN
+#define SOLVE_MINB_FIN 3
+#endif
 template <bool FINAL>
-__global__ void __launch_bounds__(SOLVE_WARPS * 32, 4)
+__global__ void __launch_bounds__(SOLVE_WARPS * 32, FINAL ? SOLVE_MINB_FIN : SOLVE_MINB_AGG)
     k_solve_merged(SolveArgs A, const int2* __restrict__ tiles, int count, int gblocks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = blockIdx.y;
@@ -495,7 +609,12 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, 4)
     if (t >= A.ntiles) return;
     int c, g;
     fast_tile_coords(t, c, g);
-    tile_body<FINAL, true>(A, w, p, b, c, g * DPW, lane, sm);
+    // pass 1: register body (no factor tables, no shared memory); pass 3:
+    // shared-memory factors (the register form needs > 168 registers there)
+    if (!FINAL)
+      agg_body(A, w, b, c, g * DPW, lane);
+    else
+      tile_body<true, true>(A, w, p, b, c, g * DPW, lane, sm);
   }
 }
 
@@ -824,7 +943,7 @@ static std::vector<int2> generic_tiles(int n) {
 static size_t op_bytes(int n, int C) {
   const size_t nsub = (size_t)(n + SUB - 1) / SUB;
   const size_t ngen = generic_tiles(n).size();
-  return sizeof(double) * ((size_t)4 * n + nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
+  return sizeof(double) * ((size_t)4 * n + 2 * nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
          sizeof(int2) * ngen + 512;
 }
 
@@ -856,6 +975,8 @@ int op_create(int n, int device, zt_operator** out) {
   q += n;
   op->d0 = q;
   q += (size_t)((n + SUB - 1) / SUB) * n;
+  op->lins = q;
+  q += (size_t)((n + SUB - 1) / SUB) * n;
   op->lin = q;
   q += (size_t)C * n;
   op->G = q;
@@ -875,7 +996,7 @@ int op_create(int n, int device, zt_operator** out) {
   }
   k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB, op->Bq);
   ZT_LAUNCHED();
-  k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lin, op->G, op->H, op->K, op->L0,
+  k_op_build<<<(n + 127) / 128, 128>>>(n, C, op->sqB, op->d0, op->lins, op->lin, op->G, op->H, op->K, op->L0,
                                         op->dinv0, op->m0x);
   ZT_LAUNCHED();
   int smem = SOLVE_WARPS * SR * DPW * (int)sizeof(double2);
@@ -907,6 +1028,7 @@ size_t solve_workspace_bytes(int n, int batch) {
   return one * batch;
 }
 
+
 static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64_t sw, double* p,
                             int64_t ldp, int64_t sp, int batch, void* ws, size_t ws_bytes,
                             cudaStream_t st) {
@@ -919,6 +1041,7 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
   A.sqB = op->sqB;
   A.Bq = op->Bq;
   A.d0s = op->d0;
+  A.lins = op->lins;
   A.lin = op->lin;
   A.L0 = op->L0;
   A.dinv0 = op->dinv0;
