@@ -65,7 +65,10 @@ int zgemm_update(int n, const double* amat, const double* p, const double* base,
 int skew_diff(int n, const double* a, double* c, cudaStream_t st);
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
-                  unsigned long long* cons, unsigned int* sync, int algo, double* planes, cudaStream_t st);
+                  unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
+                  cudaStream_t st);
+size_t zupdate_split_bytes(int n);
+int zupdate_sync_words(int n);
 size_t sum_plane_bytes(int n);
 int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                int64_t ldc, int algo, cudaStream_t st);
@@ -76,6 +79,7 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
 static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
 static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
 static bool g_planes = true; // fused 3M reads precomputed sum planes (ZT_SUM_PLANES=0 disables)
+static bool g_split = true;  // split-K tail in the fused update (ZT_SPLIT=0 disables)
 
 // ---- step workspace layout -------------------------------------------------
 struct StepWS {
@@ -88,6 +92,7 @@ struct StepWS {
   double* val;   // [0..2] validation residuals
   unsigned int* sync;  // fused update: tile counter + per-panel completion counts
   double* planes;      // 3M sum planes (P A/B layout, X B layout, a A layout)
+  double* split;       // split-K tail partial accumulators
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -96,8 +101,9 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
   const size_t mat = align_up((size_t)n * n * 16);
   const size_t sb = align_up(solve_workspace_bytes(n, 1));
   const size_t rb = align_up(resid_workspace_bytes(n));
-  const size_t yb = align_up(sizeof(unsigned int) * ((n + 63) / 64 + 1));
+  const size_t yb = align_up(sizeof(unsigned int) * zupdate_sync_words(n));
   const size_t pl = align_up(4 * sum_plane_bytes(n));
+  const size_t spl = align_up(zupdate_split_bytes(n));
   size_t off = 0;
   if (w) {
     w->p = reinterpret_cast<double*>(base + off);
@@ -109,8 +115,9 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
     w->val = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 64);
     w->sync = reinterpret_cast<unsigned int*>(base + off + 2 * mat + sb + rb + 256);
     w->planes = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb);
+    w->split = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl);
   }
-  return 2 * mat + sb + rb + 256 + yb + pl;
+  return 2 * mat + sb + rb + 256 + yb + pl + spl;
 }
 
 // small pinned host mailbox for the per-iteration read-back
@@ -182,7 +189,7 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   if (g_fused) {
     // GEMM-1 and GEMM-2 in one persistent launch (profiled as "gemm1")
     rc = zupdate_fused(n, w.p, x, w.a, base, xprev, wn, out, hh, qq, resid, cons, w.sync,
-                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, st);
+                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, g_split ? w.split : nullptr, st);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;
@@ -454,6 +461,7 @@ int zt_op_create(int n, int device, zt_op_t* op) {
   if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
   if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
+  if (const char* e = getenv("ZT_SPLIT")) g_split = std::string(e) != "0";
   return op_create(n, device, op);
 }
 int zt_op_destroy(zt_op_t op) { return op_destroy(op); }

@@ -465,7 +465,18 @@ struct FusedArgs {
   const double* pb1;
   double* pa2;
   const double* pb2;
+  // split-K tail: the last `split_s` GEMM-2 tiles run as `split_f` K-slices
+  // each (one work id per slice), so the last round of the persistent grid is
+  // a fraction of a tile instead of a partial wave of whole tiles; slices
+  // store their 3M accumulators to `split_acc` and the last slice to finish
+  // (per-tile counter `split_sem`) sums them and runs the update epilogue
+  int split_s, split_f;
+  unsigned int* split_sem;  // [split_s] (zeroed per launch)
+  double* split_acc;        // [split_s * split_f][NACC*4*WNB*2][consumer threads]
 };
+
+constexpr int SPLIT_MAX_PARTS = 320;
+constexpr int SPLIT_PART_DOUBLES = 3 * 4 * WNB * 2 * CONSUMER_WARPS * 32;
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
@@ -486,12 +497,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
   uint64_t* tq_empty = tq_full + 2;    // [2]
   __shared__ int tq[2];
   __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
+  __shared__ int split_last;
 
   const GemmArgs& g = f.g2;
   const int n = g.n;
   const int T = (n + BM - 1) / BM;
-  const int T1 = T * T, total = T1 + T * (T + 1) / 2;
+  const int L2 = T * (T + 1) / 2;
+  const int T1 = T * T, total = T1 + L2 + f.split_s * (f.split_f - 1);
   const int KT = (n + BK - 1) / BK;
+  // work id -> (GEMM-2 lower-tile index, K slice): ids past the unsplit
+  // GEMM-2 tiles are slices of the tail tiles
+  auto g2_unit = [&](int u, int& tile, int& part, int& sidx) {
+    const int full = L2 - f.split_s;
+    if (u < full) {
+      tile = u;
+      part = -1;
+      sidx = -1;
+    } else {
+      sidx = (u - full) / f.split_f;
+      part = (u - full) - sidx * f.split_f;
+      tile = full + sidx;
+    }
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -522,7 +549,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
       tq[slot] = id < total ? id : -1;
       mbar_arrive(&tq_full[slot]);
       if (id >= total) break;
-      int I, J;
+      int I, J, tl, part = -1, sidx = -1;
       const CUtensorMap *ma, *mb;
       const double *pla, *plb;
       if (id < T1) {
@@ -532,7 +559,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
         pla = f.pa1;
         plb = f.pb1;
       } else {
-        tile_of(id - T1, true, T, I, J);
+        g2_unit(id - T1, tl, part, sidx);
+        tile_of(tl, true, T, I, J);
         ma = &g.tma_a;
         mb = &g.tma_b;
         pla = f.pa2;
@@ -543,7 +571,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       const int kbt = KT;  // k blocks of 16
-      for (int kt = 0; kt < KT; ++kt, ++gs) {
+      const int k0 = part < 0 ? 0 : part * KT / f.split_f;
+      const int k1 = part < 0 ? KT : (part + 1) * KT / f.split_f;
+      for (int kt = k0; kt < k1; ++kt, ++gs) {
         const int s = gs % STAGES;
         mbar_wait(&empty[s], ((gs / STAGES) & 1) ^ 1);
         if (PL)
@@ -571,15 +601,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
     __syncwarp();
     if (lane == 0) mbar_arrive(&tq_empty[slot]);
     if (id < 0) break;
-    int I, J;
+    int I, J, tl = 0, part = -1, sidx = -1;
     const bool phase1 = id < T1;
-    if (phase1)
+    if (phase1) {
       tile_of(id, false, T, I, J);
-    else
-      tile_of(id - T1, true, T, I, J);
+    } else {
+      g2_unit(id - T1, tl, part, sidx);
+      tile_of(tl, true, T, I, J);
+    }
     Acc<ALGO> acc;
     acc.zero();
-    for (int kt = 0; kt < KT; ++kt, ++gs) {
+    const int k0 = part < 0 ? 0 : part * KT / f.split_f;
+    const int k1 = part < 0 ? KT : (part + 1) * KT / f.split_f;
+    for (int kt = k0; kt < k1; ++kt, ++gs) {
       const int s = gs % STAGES;
       mbar_wait(&full[s], (gs / STAGES) & 1);
       consume_stage<ALGO>(smem + s * SB, acc, wm, wn, lane);
@@ -613,6 +647,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
       asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
       if (threadIdx.x == 0) atomicAdd(f.done + I, 1u);
     } else {
+      if (part >= 0) {
+        // K slice of a tail tile: publish the partial accumulators; the last
+        // slice to arrive adds the others and runs the epilogue
+        constexpr int NV = Acc<ALGO>::NACC * 4 * WNB * 2;
+        const int tid = threadIdx.x;
+        double* mine = f.split_acc + (size_t)(sidx * f.split_f + part) * SPLIT_PART_DOUBLES;
+        const double* av = &acc.v[0][0][0][0];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) __stcg(mine + (size_t)q * (CONSUMER_WARPS * 32) + tid, av[q]);
+        __threadfence();
+        asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+        if (tid == 0) split_last = (atomicAdd(f.split_sem + sidx, 1u) == (unsigned)f.split_f - 1u);
+        asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+        const bool last = split_last;
+        asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+        if (!last) continue;
+        __threadfence();
+        double* aw = &acc.v[0][0][0][0];
+        for (int o = 0; o < f.split_f; ++o) {
+          if (o == part) continue;
+          const double* other = f.split_acc + (size_t)(sidx * f.split_f + o) * SPLIT_PART_DOUBLES;
+#pragma unroll
+          for (int q = 0; q < NV; ++q) aw[q] += __ldcg(other + (size_t)q * (CONSUMER_WARPS * 32) + tid);
+        }
+      }
       if (lane == 0) {
         // order this warp's epilogue reads of a after the producer's acquire
         while (ld_acquire(f.done + I) < (unsigned)T) __nanosleep(32);
@@ -775,9 +834,38 @@ size_t sum_plane_bytes(int n) {
   return (size_t)((n + 63) / 64) * 64 * ((n + 15) / 16) * 16 * sizeof(double);
 }
 
+size_t zupdate_split_bytes(int n) {
+  const int T = (n + BM - 1) / BM;
+  const int parts = std::min(SPLIT_MAX_PARTS, 4 * (T * (T + 1) / 2));
+  return sizeof(double) * (size_t)parts * SPLIT_PART_DOUBLES;
+}
+int zupdate_sync_words(int n) { return (n + BM - 1) / BM + 1 + SPLIT_MAX_PARTS; }
+
+// Split-K tail: with U work units on G resident CTAs the last round holds
+// r = U mod G whole tiles; splitting them into f K-slices makes it
+// ceil(f r / G) / f tiles long.  Pick the f in {2, 3, 4} that shortens it most.
+static void pick_split(int U, int G, int L2, int n, int& S, int& F) {
+  S = 0;
+  F = 1;
+  const int r = U % G;
+  if (r == 0 || G <= 1 || n < 256) return;
+  double best = 1.0;
+  const int cap = (int)(zupdate_split_bytes(n) / (sizeof(double) * SPLIT_PART_DOUBLES));
+  for (int fs = 2; fs <= 4; ++fs) {
+    if (r > L2 || r * fs > cap) continue;
+    const double len = (double)((fs * r + G - 1) / G) / fs;
+    if (len < best - 1e-9) {
+      best = len;
+      S = r;
+      F = fs;
+    }
+  }
+}
+
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
-                  unsigned long long* cons, unsigned int* sync, int algo, double* planes, cudaStream_t st) {
+                  unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
+                  cudaStream_t st) {
   FusedArgs f;
   memset(&f, 0, sizeof f);
   GemmArgs& g = f.g2;
@@ -834,7 +922,13 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
   const int T = (n + BM - 1) / BM;
   const int total = T * T + T * (T + 1) / 2;
   const int grid = std::min(total, dev < 16 ? g_sms[dev] : 148);
-  ZT_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (T + 1), st));
+  int S = 0, F = 1;
+  if (split) pick_split(total, grid, T * (T + 1) / 2, n, S, F);
+  f.split_s = S;
+  f.split_f = F;
+  f.split_sem = sync + 1 + T;
+  f.split_acc = split;
+  ZT_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (T + 1 + S), st));
   if (algo == ALGO_4M)
     k_zupdate<ALGO_4M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
   else if (algo == ALGO_3MS)

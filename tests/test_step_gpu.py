@@ -105,7 +105,9 @@ def test_consistency_and_comm_scale(zt):
     np.testing.assert_allclose(a, b, atol=1e-14)
 
 
-@pytest.mark.parametrize("n", (200, 512))
+# 1024 and 1280 run the fused update with a split-K tail (3 and 2 K-slices on
+# 148 SMs: 392 = 2*148 + 96 and 610 = 4*148 + 18 work units)
+@pytest.mark.parametrize("n", (200, 512, 1024, 1280))
 def test_step_vs_oracle_midsize(zt, n):
     w = zo.smooth_initial(n)
     ref = w

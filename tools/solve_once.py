@@ -11,7 +11,7 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 g = torch.Generator(device="cuda").manual_seed(0)
 a = torch.randn(8, n, n, dtype=torch.complex128, device="cuda", generator=g) / n
 w = 0.5 * (a - a.conj().transpose(1, 2))
-w -= torch.diagonal(w, dim1=1, dim2=2).mean(-1)[:, None, None] * torch.eye(n, device="cuda")
+w -= torch.diagonal(w, dim1=1, dim2=2).mean(-1)[:, None, None] * torch.eye(n, device="cuda", dtype=torch.complex128)
 op = zt.build_operator(n)
 for _ in range(reps):
     p = zt.solve_stream_batched(w, op)

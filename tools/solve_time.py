@@ -16,7 +16,7 @@ for n in [int(x) for x in (sys.argv[1:] or ["1024", "2048", "4096"])]:
     a = torch.randn(8, n, n, dtype=torch.complex128, device="cuda", generator=g) / n
     w = 0.5 * (a - a.conj().transpose(1, 2))
     del a
-    w -= torch.diagonal(w, dim1=1, dim2=2).mean(-1)[:, None, None] * torch.eye(n, device="cuda")
+    w -= torch.diagonal(w, dim1=1, dim2=2).mean(-1)[:, None, None] * torch.eye(n, device="cuda", dtype=torch.complex128)
     op = zt.build_operator(n)
     p = zt.solve_stream_batched(w, op)
     ref = torch.load(f"/tmp/ref_{n}.pt") if os.path.exists(f"/tmp/ref_{n}.pt") else None
