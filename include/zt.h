@@ -23,6 +23,9 @@
  *   zt_zgemm            integrator.py:127-128, 155-156  the numpy `@` products (OpenBLAS zgemm)
  *   zt_commutator /     integrator.py:127-129           (a - a^H) and the sandwich update
  *   zt_sandwich
+ *   zt_basis_vectors    basis.py:119-165 compute_basis    the quantized basis eigenvectors
+ *   zt_basis_extract    basis.py:319-331 extract          per-diagonal transforms
+ *   zt_basis_project    basis.py:276-316 project
  */
 #ifndef ZT_H_
 #define ZT_H_
@@ -133,6 +136,27 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
 int zt_commutator(int n, const double* p, const double* w, double* c, double* work, void* stream);
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work,
                 void* stream);
+
+/* Quantized spherical-harmonic basis (basis.py).
+ * Vectors for orders m0 <= m < m1 are stored like the reference's
+ * QuantizedBasis.vectors[m]: row-major (N - m) x n_l(m) doubles,
+ * n_l(m) = N - max(m, 1), columns l = max(m,1)..N-1, at vec + off[m]
+ * (device int64 offsets, indexed by absolute m).  Coefficients are complex
+ * (interleaved), order m at pos/neg + 2 * coff[m] (n_l(m) entries each).
+ *   zt_basis_vectors   compute_basis eigenvectors, sign rule of
+ *                      basis.py:110-114 (basis.py:119-165)
+ *   zt_basis_extract   w_lm = -i Tr(T_lm^H W) for both signs of m
+ *                      (basis.py:319-331)
+ *   zt_basis_project   W = sum i w_lm T_lm into the rows/columns of the
+ *                      m-diagonals; neg == NULL: skew completion of the
+ *                      lower triangle (basis.py:276-316) */
+int zt_basis_vectors(int n, int m0, int m1, const long long* off, double* vec, void* stream);
+int zt_basis_extract(int n, int m0, int m1, const long long* off, const long long* coff,
+                     const double* vec, const double* w, int64_t ldw, double* pos, double* neg,
+                     void* stream);
+int zt_basis_project(int n, int m0, int m1, const long long* off, const long long* coff,
+                     const double* vec, const double* pos, const double* neg, double* w,
+                     int64_t ldw, void* stream);
 
 /* Per-kernel device timing for the roofline report: when enabled, CUDA
  * events bracket the stream solve, GEMM-1 (a = P X) and GEMM-2 (update) of

@@ -5,6 +5,20 @@ Drop-in for the reference package's step / stream-solve API
 by hand-written sm_100a kernels in ``libzt.so`` (C ABI: include/zt.h).
 """
 
+from .basis import (
+    DeviceBasis,
+    HarmonicCoefficients,
+    QuantizedBasis,
+    compute_basis,
+    energy_spectrum,
+    extract,
+    hamiltonian_from_coeffs,
+    load_basis,
+    project,
+    save_basis,
+    threej,
+    wigner_basis_oracle,
+)
 from .diagnostics import hamiltonian
 from .driver import Checkpoint, DeviceRun, FileFormatError, read_checkpoint, write_checkpoint
 from .integrator import (
@@ -41,4 +55,6 @@ __all__ = [
     "apply_laplacian", "build_block", "build_operator", "skewness_residual", "solve_stream",
     "solve_stream_batched", "spectral_norm", "trace_residual", "validate_vorticity", "hamiltonian",
     "Checkpoint", "DeviceRun", "FileFormatError", "read_checkpoint", "write_checkpoint",
+    "DeviceBasis", "HarmonicCoefficients", "QuantizedBasis", "compute_basis", "energy_spectrum", "extract",
+    "hamiltonian_from_coeffs", "load_basis", "project", "save_basis", "threej", "wigner_basis_oracle",
 ]

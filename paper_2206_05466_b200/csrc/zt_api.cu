@@ -68,6 +68,11 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
                   cudaStream_t st);
 size_t zupdate_split_bytes(int n);
+int basis_vectors(int n, int m0, int m1, const long long* off, double* vec, cudaStream_t st);
+int basis_extract(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
+                  const double* w, int64_t ldw, double* pos, double* neg, cudaStream_t st);
+int basis_project(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
+                  const double* pos, const double* neg, double* w, int64_t ldw, cudaStream_t st);
 int zupdate_sync_words(int n);
 size_t sum_plane_bytes(int n);
 int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
@@ -581,6 +586,23 @@ int zt_commutator(int n, const double* p, const double* w, double* c, double* wo
   int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
   if (rc) return rc;
   return skew_diff(n, work, c, st);
+}
+
+int zt_basis_vectors(int n, int m0, int m1, const long long* off, double* vec, void* stream) {
+  if (!off || !vec) return fail(ZT_EINVAL, "zt_basis_vectors: bad argument");
+  return basis_vectors(n, m0, m1, off, vec, (cudaStream_t)stream);
+}
+
+int zt_basis_extract(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
+                     const double* w, int64_t ldw, double* pos, double* neg, void* stream) {
+  if (!off || !coff || !vec || !w || !pos || !neg || ldw < n) return fail(ZT_EINVAL, "zt_basis_extract: bad argument");
+  return basis_extract(n, m0, m1, off, coff, vec, w, ldw, pos, neg, (cudaStream_t)stream);
+}
+
+int zt_basis_project(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
+                     const double* pos, const double* neg, double* w, int64_t ldw, void* stream) {
+  if (!off || !coff || !vec || !pos || !w || ldw < n) return fail(ZT_EINVAL, "zt_basis_project: bad argument");
+  return basis_project(n, m0, m1, off, coff, vec, pos, neg, w, ldw, (cudaStream_t)stream);
 }
 
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work, void* stream) {

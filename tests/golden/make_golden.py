@@ -18,6 +18,11 @@ Contents (all complex128 C-order unless noted):
                     per-step iterations, C2/C3/H series
   known.npz         known answers: pinv-oracle P at N=5, casimirs of
                     i*diag(1,-1,0,0), blocks N=2 m=0 / N=3 m=1
+  basis.npz         per N in BASIS_NS: reference basis vectors (all m, the
+                    QuantizedBasis layout, concatenated), extract of
+                    random_admissible(N, default_rng(500+N), 1) (packed pos/neg),
+                    its energy spectrum, project of random real coefficients
+                    (test_basis.py:20-32 generator, default_rng(700+N))
   modes.npz         inputs of the reference's integrator property tests
                     (test_integrator.py) built with its spherical-harmonic basis
                     (out of scope here): single modes (N=8 l=4 m=1, N=9 l=2 m=0),
@@ -175,6 +180,36 @@ def modes():
     np.savez_compressed(os.path.join(OUT, "modes.npz"), **d)
 
 
+BASIS_NS = (2, 3, 5, 8, 9, 16, 17, 33, 48)
+
+
+def basis():
+    """Reference basis vectors (sign rule / oracle alignment), extract of an
+    admissible W, project of real coefficients, energy spectrum (basis.py)."""
+    from test_basis import random_real_field_coeffs
+    from zeitlin.basis import compute_basis, extract, project
+    from zeitlin.diagnostics import energy_spectrum
+
+    d = {}
+    for n in BASIS_NS:
+        b = compute_basis(n)
+        d[f"vec_{n}"] = np.concatenate([v.ravel() for v in b.vectors])
+        w = random_admissible(n, np.random.default_rng(500 + n), 1.0)
+        c = extract(w, b)
+        d[f"W_{n}"] = w
+        d[f"pos_{n}"] = np.concatenate(c.pos)
+        d[f"neg_{n}"] = np.concatenate(c.neg)
+        d[f"E_{n}"] = energy_spectrum(c)
+        cr = random_real_field_coeffs(n, np.random.default_rng(700 + n))
+        d[f"cpos_{n}"] = np.concatenate(cr.pos)
+        d[f"cneg_{n}"] = np.concatenate(cr.neg)
+        d[f"P_{n}"] = project(cr, b)
+    np.savez_compressed(os.path.join(OUT, "basis.npz"), **d)
+    from zeitlin.basis import save_basis
+
+    save_basis(os.path.join(OUT, "basis_n5.zeb"), compute_basis(5))  # formats.py:83-89
+
+
 def checkpoint():
     """A ZCK1 file written by the reference's own writer (formats.py:130-143)."""
     from zeitlin.formats import Checkpoint, write_checkpoint
@@ -186,6 +221,7 @@ def checkpoint():
 
 
 if __name__ == "__main__":
+    basis()
     checkpoint()
     modes()
     solve_small()

@@ -36,3 +36,24 @@ def test_reader_rejects_corruption(tmp_path):
         p.write_bytes(bad)
         with pytest.raises(FileFormatError):
             read_checkpoint(p, device="cpu")
+
+
+def test_basis_cache_matches_reference_format(tmp_path):
+    """ZEB1 basis cache (formats.py:83-113): a file written by the reference's
+    save_basis parses to its vectors, and writing them back is byte-identical."""
+    from paper_2206_05466_b200.basis import load_basis, save_basis
+    from paper_2206_05466_b200.driver import FileFormatError
+
+    src = os.path.join(GOLDEN, "basis_n5.zeb")
+    b = load_basis(src, device="cpu")
+    g = np.load(os.path.join(GOLDEN, "basis.npz"))
+    np.testing.assert_array_equal(b.data.numpy(), g["vec_5"])
+    out = tmp_path / "b.zeb"
+    save_basis(out, b)
+    assert out.read_bytes() == open(src, "rb").read()
+    raw = open(src, "rb").read()
+    for bad in (b"ZEB2" + raw[4:], raw[:-8], raw + b"\0"):
+        p = tmp_path / "bad.zeb"
+        p.write_bytes(bad)
+        with pytest.raises(FileFormatError):
+            load_basis(p, device="cpu")

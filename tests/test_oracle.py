@@ -7,7 +7,7 @@ trusted checker for the GPU parity tests.
 
 import numpy as np
 import pytest
-from conftest import relf
+from conftest import load_golden, relf
 
 from oracle import zeitlin_oracle as zo
 
@@ -110,3 +110,32 @@ def test_closed_form_ldlt_matches_dpttrf():
             kk = k[:-1]
             lex = -np.sqrt((n - 1 - kk - m) / (kk + m + 1)) * np.sqrt((kk + 1) / (n - 1 - kk))
             np.testing.assert_allclose(e, lex, rtol=4e-15)
+
+
+def _split_vectors(flat, n):
+    out, off = [], 0
+    for m in range(n):
+        sz = (n - m) * (n - max(m, 1))
+        out.append(flat[off:off + sz].reshape(n - m, n - max(m, 1)))
+        off += sz
+    return out
+
+
+@pytest.mark.parametrize("n", (2, 3, 5, 8, 9, 16, 17, 33, 48))
+def test_basis_oracle_pinned(n):
+    """The basis restatement reproduces the reference's vectors bit for bit
+    (3j-aligned signs at n <= 16, the sign rule above), and extract/project
+    its transforms (basis.py:119-165, 276-331)."""
+    g = load_golden("basis.npz")
+    ref = _split_vectors(g[f"vec_{n}"], n)
+    mine = zo.basis_vectors(n)
+    if n > 16:
+        for a, b in zip(mine, ref):
+            np.testing.assert_array_equal(a, b)
+    mine = zo.align_with(mine, ref)
+    for a, b in zip(mine, ref):
+        np.testing.assert_array_equal(a, b)
+    p, q = zo.extract(g[f"W_{n}"], ref)
+    np.testing.assert_array_equal(p, g[f"pos_{n}"])
+    np.testing.assert_array_equal(q, g[f"neg_{n}"])
+    np.testing.assert_array_equal(zo.project(g[f"cpos_{n}"], g[f"cneg_{n}"], ref), g[f"P_{n}"])
