@@ -407,15 +407,20 @@ _lidx_cache: dict = {}
 
 
 def energy_spectrum_packed(pos: torch.Tensor, neg: torch.Tensor, basis: DeviceBasis) -> torch.Tensor:
-    """energy_spectrum on the device from packed coefficients."""
+    """energy_spectrum on the device from packed coefficients.  Deterministic:
+    the |w_lm|^2 are scattered into a dense (m, l) table (unique indices) and
+    summed over m, so repeated runs give identical bits."""
     n = basis.n
     key = (n, pos.device)
     if key not in _lidx_cache:
         lidx, m1 = _degree_index(n)
-        _lidx_cache[key] = (torch.from_numpy(lidx).to(pos.device), torch.from_numpy(m1).to(pos.device))
-    lidx, m1 = _lidx_cache[key]
+        midx = np.concatenate([np.full(n - _l_start(m), m) for m in range(n)])
+        _lidx_cache[key] = tuple(torch.from_numpy(a).to(pos.device) for a in (lidx, m1, midx))
+    lidx, m1, midx = _lidx_cache[key]
     p = pos.abs() ** 2 + torch.where(m1, neg.abs() ** 2, torch.zeros_like(neg.real))
-    power = torch.zeros(n, dtype=torch.float64, device=pos.device).index_add_(0, lidx, p)
+    table = torch.zeros((n, n), dtype=torch.float64, device=pos.device)
+    table[midx, lidx] = p
+    power = table.sum(0)
     l = torch.arange(n, dtype=torch.float64, device=pos.device)
     out = torch.zeros_like(power)
     out[1:] = power[1:] / (2.0 * l[1:] * (l[1:] + 1.0))

@@ -17,10 +17,12 @@ device-to-host copy.  Runs are bitwise deterministic, so a run resumed from a
 checkpoint reproduces the uninterrupted run's checkpoints and diagnostics
 byte for byte (the reference's test_driver.py:231-248 contract).
 
-Out of scope here (they need the spherical-harmonic basis):
-the energy spectrum files, the basis-derived kinetic energy K (written as
-the trace-form energy, equal to it up to round-off per diagnostics.py:8-12),
-grid snapshots, the config file and CLI.
+With a device basis (`basis.compute_basis`) each sample
+also extracts the coefficients on the device and writes the reference's
+`spectrum_<step>.csv` (rows l, E_l) with K = sum_l E(l)
+(driver.py:357-372); without one, K is the trace-form energy H, equal to it
+up to round-off (diagnostics.py:8-12).  Out of scope: grid snapshots
+(rank 4), the config file and CLI.
 """
 
 from __future__ import annotations
@@ -33,6 +35,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
+from .basis import energy_spectrum_packed, extract_packed
 from .diagnostics import hamiltonian
 from .integrator import StepperState, casimirs, midpoint_step_raw
 from .laplacian import build_operator
@@ -113,7 +116,7 @@ class DeviceRun:
 
     def __init__(self, state: StepperState, output_dir, k_max: int = 3, sample_every: int = 10,
                  checkpoint_every: int = 100, seed: int = 0, rng_state: bytes = b"",
-                 baseline: np.ndarray | None = None):
+                 baseline: np.ndarray | None = None, basis=None):
         w = state.w if isinstance(state.w, torch.Tensor) else torch.from_numpy(np.asarray(state.w))
         if not w.is_cuda:
             w = w.to(torch.device("cuda", torch.cuda.current_device()))
@@ -133,6 +136,9 @@ class DeviceRun:
         self.diag_path = self.out / "diagnostics.csv"
         self.meta_path = self.out / "run_meta.json"
         self.iterations: list[int] = []
+        if basis is not None and basis.n != self.n:
+            raise ValueError(f"basis is for N={basis.n}, state has N={self.n}")
+        self.basis = basis
 
     # -- files ---------------------------------------------------------------
     def start(self) -> None:
@@ -147,7 +153,7 @@ class DeviceRun:
 
     @classmethod
     def resume(cls, checkpoint_path, output_dir, k_max=3, sample_every=10, checkpoint_every=100,
-               tol=1e-12, max_iter=10, comm_scale=1.0):
+               tol=1e-12, max_iter=10, comm_scale=1.0, basis=None):
         """Resume from a ZCK1 checkpoint and the run's run_meta.json (driver.py:300-334)."""
         out = Path(output_dir)
         meta_path, diag_path = out / "run_meta.json", out / "diagnostics.csv"
@@ -166,7 +172,7 @@ class DeviceRun:
         st = StepperState(w=cp.w, h=h, time=cp.time, step_index=cp.step_index, tol=tol,
                           max_iter=max_iter, comm_scale=comm_scale)
         run = cls(st, out, k_max=k_max, sample_every=sample_every, checkpoint_every=checkpoint_every,
-                  seed=cp.seed, rng_state=cp.rng_state, baseline=baseline)
+                  seed=cp.seed, rng_state=cp.rng_state, baseline=baseline, basis=basis)
         # drop diagnostics rows after the resume point (driver.py:241-252)
         lines = run.diag_path.read_text().splitlines()
         kept = [lines[0]] + [ln for ln in lines[1:]
@@ -178,7 +184,14 @@ class DeviceRun:
         """On-device Casimirs and energy at the current state (driver.py:357-376)."""
         ck = casimirs(self.w, self.k_max)
         h_val = hamiltonian(self.w, self.op)
-        row = [format_float(self.state.time), format_float(h_val), format_float(h_val)]
+        k_val = h_val
+        if self.basis is not None:
+            pos, neg = extract_packed(self.w, self.basis)
+            energy = energy_spectrum_packed(pos, neg, self.basis).cpu().numpy()
+            k_val = float(energy.sum())
+            lines = ["l,E_l"] + [f"{l},{format_float(energy[l])}" for l in range(1, self.n)]
+            _atomic_write(self.out / f"spectrum_{self.state.step_index:08d}.csv", ("\n".join(lines) + "\n").encode())
+        row = [format_float(self.state.time), format_float(h_val), format_float(k_val)]
         row += [format_float(v) for v in casimir_drift(self.baseline, ck)]
         with open(self.diag_path, "a", encoding="utf-8") as fh:
             fh.write(",".join(row) + "\n")

@@ -74,3 +74,31 @@ def test_resume_truncates_later_rows_and_checks_config(tmp_path):
         DeviceRun.resume(cp, tmp_path / "o", k_max=3)
     with pytest.raises(ValueError):
         DeviceRun.resume(cp, tmp_path / "missing", k_max=3)
+
+
+def test_run_with_device_basis_writes_spectra(tmp_path):
+    """With a device basis the run writes spectrum_<step>.csv (driver.py:368-372)
+    and K = sum_l E(l), equal to the trace-form H (diagnostics.py:8-12); the
+    resumed run still reproduces every file byte for byte."""
+    from paper_2206_05466_b200 import DeviceRun, StepperState, compute_basis
+
+    g = load_golden("cfg4_n64.npz")
+    b = compute_basis(64)
+
+    def go(out, steps):
+        run = DeviceRun(StepperState(w=torch.from_numpy(g["W0"]).cuda(), h=0.005), out, k_max=3,
+                        sample_every=10, checkpoint_every=10, seed=1, basis=b)
+        run.start()
+        run.advance(steps)
+
+    go(tmp_path / "a", 20)
+    rows = [r.split(",") for r in (tmp_path / "a" / "diagnostics.csv").read_text().splitlines()[1:]]
+    for r in rows:
+        assert float(r[2]) == pytest.approx(float(r[1]), rel=1e-12)
+    sp = (tmp_path / "a" / "spectrum_00000020.csv").read_text().splitlines()
+    assert sp[0] == "l,E_l" and len(sp) == 64 and sp[1].startswith("1,")
+    go(tmp_path / "b", 10)
+    DeviceRun.resume(tmp_path / "b" / "checkpoint_00000010.zck", tmp_path / "b", k_max=3, sample_every=10,
+                     checkpoint_every=10, basis=b).advance(20)
+    for f in ("diagnostics.csv", "spectrum_00000020.csv", "checkpoint_00000020.zck"):
+        assert (tmp_path / "b" / f).read_bytes() == (tmp_path / "a" / f).read_bytes(), f
