@@ -25,7 +25,6 @@ struct zt_operator {
   double* m0x = nullptr;  // m = 0 per-chunk constant-RHS responses
   int2* gen_tiles = nullptr;  // (chunk, group) of the boundary tiles
   int ngen = 0;
-  int2* g0_tiles = nullptr;   // (chunk, 0): diagonals 0..7 (the resident path's complement)
   void* block = nullptr;  // single allocation holding every table
 };
 

@@ -767,362 +767,6 @@ __global__ void __launch_bounds__(MAXT) k_solve_carry(int n, int C, const double
   }
 }
 
-// ---------------------------------------------------------------------------
-// Single-read solve for the diagonals m >= 8: one thread-block cluster per
-// group of RG = 4 consecutive diagonals and matrix.  The Q CTAs of the
-// cluster split the group's rows; each CTA stages its rows of W in shared
-// memory once (cp.async, 64 B per row: W[i][i-m0-3 .. i-m0]), runs the
-// factor chain + zero-carry forward sweep per 16-row thread segment (the
-// factors stay in registers), composes the segment maps per diagonal, and
-// the CTAs exchange their aggregate maps through distributed shared memory
-// (one cluster barrier).  Every CTA then resolves its own carries and
-// finishes from shared memory: W is read from HBM exactly once and P
-// written once (24 N^2 bytes instead of the 3-pass path's 32 N^2), one
-// launch, no carry tables.  Diagonals 0..7 (including the singular,
-// deflated m = 0 block) take the 3-pass tile path on a forked stream.
-// ---------------------------------------------------------------------------
-constexpr int RG = 4;                            // diagonals per resident group
-constexpr int RSTRIDE = SUB * RG * 16 + 64;       // bytes per 16-row segment block (padded: bank halves)
-constexpr int RSMEM_EXTRA = (8 * RG * 4 + RG * 8 + RG * 4 + 8 * RG * 7) * 8;  // scan/exchange scratch
-
-struct ResArgs {
-  int n, Q, segmax, g0, ngroups;
-  const double* d0s;
-  const double* lins;
-  const double* sqB;
-  const double* Bq;
-  const double* w;
-  int64_t ldw, sw;
-  double* p;
-  int64_t ldp, sp;
-};
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ double ld_dsmem(const double* local, uint32_t rank) {
-  uint32_t a = smem_u32(local), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
-  return v;
-}
-
-__global__ void __launch_bounds__(256) k_solve_resident(ResArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n = A.n, Q = A.Q;
-  const int q = (int)cluster_rank();
-  const int g = A.g0 + blockIdx.x / Q;
-  const int b = blockIdx.y;
-  const int m0 = g * RG;
-  const int t = threadIdx.x;
-  unsigned char* tile = smem_raw;                                            // segmax * RSTRIDE
-  double* maps = reinterpret_cast<double*>(smem_raw + A.segmax * RSTRIDE);   // warp totals [8][RG][4]
-  double* agg = maps + 8 * RG * 4;  // [RG][8]: A(2) G X(2) H K
-  double* car = agg + RG * 8;       // [RG][4]: y_in(2), x_in(2); then [8][RG][7] gathered aggregates
-  const double* w = A.w + (size_t)b * A.sw * 2;
-  double* p = A.p + (size_t)b * A.sp * 2;
-
-  const int S0 = m0 / SUB, S1 = (n + SUB - 1) / SUB;
-  const int per = (S1 - S0 + Q - 1) / Q;
-  const int sb = S0 + q * per;
-  const int J = max(0, min(S1, sb + per) - sb);
-  const int r0 = sb * SUB;  // first row of this CTA
-
-  // ---- stage this CTA's rows (zero-fill entries outside the lower triangle)
-  {
-    const uint32_t sbase = smem_u32(tile);
-    for (int idx = t; idx < J * SUB * RG; idx += blockDim.x) {
-      const int rl = idx / RG, e = idx % RG;
-      const int i = r0 + rl;
-      const int col = i - m0 - (RG - 1) + e;  // diagonal m0 + 3 - e
-      const bool ok = i < n && col >= 0;
-      const double* src = ok ? w + ((size_t)i * A.ldw + col) * 2 : w;
-      const uint32_t dst = sbase + (rl / SUB) * RSTRIDE + (rl % SUB) * (RG * 16) + e * 16;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-    __syncthreads();
-  }
-
-  // ---- phase 1: thread (d, j) owns rows [16 s, 16 s + 16) of diagonal m0 + d
-  const int d = t % RG, j = t / RG;
-  const int m = m0 + d;
-  const int s = sb + j;
-  const int ib = s * SUB;
-  const int len = n - m;
-  const int rs = max(0, m - ib), re = min(SUB - 1, n - 1 - ib);
-  const bool has = j < J && m < n && rs <= re;
-  double2* mine = reinterpret_cast<double2*>(tile + j * RSTRIDE) + (RG - 1 - d);  // row r at mine[r * RG]
-  double Lr[SUB], Dr[SUB];
-  AffW fm;
-  fm.a = make_double2(0.0, 0.0);
-  fm.g = 1.0;
-  double2 bl = make_double2(0.0, 0.0);
-  double ks = 0.0, P = 1.0;
-  double Lin = 0.0;
-  if (has) {
-    const size_t sub = (size_t)(ib / SUB) * n + m;
-    int k = ib + rs - m;
-    double qm1 = 1.0, q0 = A.d0s[sub];
-    Lin = A.lins[sub];
-    double dg = block_diag(n, m, k);
-    double inc = 2.0 * (double)(n - 2 - 2 * k - m);
-    const double* sqi = A.sqB + ib + rs;
-    const double* sqk = A.sqB + k;
-    const double* bqi = A.Bq + ib + rs;
-    const double* bqk = A.Bq + k;
-    double Lp = Lin;
-#pragma unroll
-    for (int r = 0; r < SUB; ++r) {
-      Lr[r] = 0.0;
-      Dr[r] = 0.0;
-      if (r >= rs && r <= re) {
-        const int rr = r - rs;
-        const int kk = k + rr;
-        const double di = qm1 * fast_rcp(q0);
-        double L = 0.0;
-        if (kk < len - 1) {
-          L = (-sqi[rr] * sqk[rr]) * di;
-          const double e2 = bqi[rr] * bqk[rr];
-          dg += inc;
-          inc -= 4.0;
-          const double q1 = fma(dg, q0, -e2 * qm1);
-          qm1 = q0;
-          q0 = q1;
-        }
-        const double2 bb = mine[r * RG];
-        if (kk == 0) {  // diagonal start: no coupling from above
-          fm.a = bb;
-          fm.g = 0.0;
-        } else {
-          fm.a = make_double2(fma(-Lp, fm.a.x, bb.x), fma(-Lp, fm.a.y, bb.y));
-          fm.g = -Lp * fm.g;
-        }
-        mine[r * RG] = fm.a;  // y with zero carry into the segment
-        const double cf = P * di;
-        bl = make_double2(fma(cf, fm.a.x, bl.x), fma(cf, fm.a.y, bl.y));
-        ks = fma(cf, fm.g, ks);
-        P = -L * P;
-        Lr[r] = L;
-        Dr[r] = di;
-        Lp = L;
-      }
-    }
-  }
-  // ---- compose the segment maps of each diagonal across the CTA: warp
-  // shuffles within a warp (lane = 4 j' + d, 8 segments), shared memory across
-  // warps.  Forward: y_end = a + g y_in.  Backward, with the segment's y_in
-  // written through the forward prefix (y_in(j) = yA + yG Y, Y = the CTA's
-  // incoming y): x_start(j) = c + k Y + P x_start(j+1).
-  const int lane = t & 31, wid = t >> 5, nw = (blockDim.x + 31) >> 5;
-  const int jl = lane / RG;  // segment within the warp
-  AffW f = fm;
-  if (!(j < J)) {
-    f.a = make_double2(0.0, 0.0);
-    f.g = 1.0;
-  }
-  AffW fi = f;  // inclusive forward scan within the warp
-#pragma unroll
-  for (int o = 1; o < 32 / RG; o <<= 1) {
-    AffW u = aff_shfl(fi, max(lane - o * RG, 0));
-    if (jl >= o) fi = aff_compose(u, fi);
-  }
-  double* wagg = maps;  // [nw][RG][3] forward warp totals, then [nw][RG][4] backward
-  if (jl == 32 / RG - 1) {
-    double* o = wagg + (wid * RG + d) * 3;
-    o[0] = fi.a.x;
-    o[1] = fi.a.y;
-    o[2] = fi.g;
-  }
-  __syncthreads();
-  AffW pre;  // exclusive prefix of this segment within the CTA
-  pre.a = make_double2(0.0, 0.0);
-  pre.g = 1.0;
-  for (int ww = 0; ww < wid; ++ww) {
-    const double* o = wagg + (ww * RG + d) * 3;
-    AffW u;
-    u.a = make_double2(o[0], o[1]);
-    u.g = o[2];
-    pre = aff_compose(pre, u);
-  }
-  {
-    AffW ex = aff_shfl(fi, max(lane - RG, 0));
-    if (jl >= 1) pre = aff_compose(pre, ex);
-  }
-  const AffW ctaf = aff_compose(pre, f);  // the CTA forward total at the last segment slot
-  // backward maps (c, k, P)
-  double2 c = make_double2(fma(ks, pre.a.x, bl.x), fma(ks, pre.a.y, bl.y));
-  double kc = ks * pre.g, pc = P;
-  if (!(j < J)) {
-    c = make_double2(0.0, 0.0);
-    kc = 0.0;
-    pc = 1.0;
-  }
-  // inclusive suffix scan within the warp: (c,k,P)_j o (c,k,P)_{j+1} ...
-  double2 sc = c;
-  double sk = kc, sp = pc;
-#pragma unroll
-  for (int o = 1; o < 32 / RG; o <<= 1) {
-    const int src = min(lane + o * RG, 31);
-    const double ux = __shfl_sync(0xffffffff, sc.x, src), uy = __shfl_sync(0xffffffff, sc.y, src);
-    const double uk = __shfl_sync(0xffffffff, sk, src), up = __shfl_sync(0xffffffff, sp, src);
-    if (jl + o < 32 / RG) {
-      sc = make_double2(fma(sp, ux, sc.x), fma(sp, uy, sc.y));
-      sk = fma(sp, uk, sk);
-      sp = sp * up;
-    }
-  }
-  __syncthreads();  // forward warp totals consumed
-  if (jl == 0) {
-    double* o = wagg + (wid * RG + d) * 4;
-    o[0] = sc.x;
-    o[1] = sc.y;
-    o[2] = sk;
-    o[3] = sp;
-  }
-  __syncthreads();
-  // exclusive suffix: the rest of my warp, then the later warps
-  double2 xc = make_double2(0.0, 0.0);
-  double xk = 0.0, xp = 1.0;
-  {
-    const int src = min(lane + RG, 31);
-    const double ux = __shfl_sync(0xffffffff, sc.x, src), uy = __shfl_sync(0xffffffff, sc.y, src);
-    const double uk = __shfl_sync(0xffffffff, sk, src), up = __shfl_sync(0xffffffff, sp, src);
-    if (jl + 1 < 32 / RG) {
-      xc = make_double2(ux, uy);
-      xk = uk;
-      xp = up;
-    }
-  }
-  for (int ww = wid + 1; ww < nw; ++ww) {
-    const double* o = wagg + (ww * RG + d) * 4;
-    xc = make_double2(fma(xp, o[0], xc.x), fma(xp, o[1], xc.y));
-    xk = fma(xp, o[2], xk);
-    xp = xp * o[3];
-  }
-  // CTA totals: forward from the last segment slot, backward from j = 0
-  if (j == nw * (32 / RG) - 1) {
-    agg[d * 8 + 0] = ctaf.a.x;
-    agg[d * 8 + 1] = ctaf.a.y;
-    agg[d * 8 + 2] = ctaf.g;
-  }
-  if (j == 0) {
-    // full-CTA backward total = warp-0 inclusive suffix composed with later warps
-    double2 tc = sc;
-    double tk = sk, tp = sp;
-    for (int ww = 1; ww < nw; ++ww) {
-      const double* o = wagg + (ww * RG + d) * 4;
-      tc = make_double2(fma(tp, o[0], tc.x), fma(tp, o[1], tc.y));
-      tk = fma(tp, o[2], tk);
-      tp = tp * o[3];
-    }
-    agg[d * 8 + 3] = tc.x;
-    agg[d * 8 + 4] = tc.y;
-    agg[d * 8 + 5] = tp;
-    agg[d * 8 + 6] = tk;
-  }
-  cluster_sync_all();  // every CTA's aggregates are visible cluster-wide
-  // gather the Q aggregates (one remote round trip, in parallel), then chain
-  double* rem = car + RG * 4;  // [Q][RG][7]
-  if (t < RG * Q) {
-    const int dd = t % RG, qq = t / RG;
-#pragma unroll
-    for (int e = 0; e < 7; ++e) rem[(qq * RG + dd) * 7 + e] = ld_dsmem(agg + dd * 8 + e, qq);
-  }
-  cluster_arrive();  // remote reads done; wait before exit
-  __syncthreads();
-  if (t < RG) {
-    double yx = 0.0, yy = 0.0, myx = 0.0, myy = 0.0;
-    double yin_x[8], yin_y[8];
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      if (qq < Q) {
-        yin_x[qq] = yx;
-        yin_y[qq] = yy;
-        if (qq == q) {
-          myx = yx;
-          myy = yy;
-        }
-        const double* r = rem + (qq * RG + t) * 7;
-        const double nx = fma(r[2], yx, r[0]), ny = fma(r[2], yy, r[1]);
-        yx = nx;
-        yy = ny;
-      }
-    }
-    double xx = 0.0, xy = 0.0;
-#pragma unroll
-    for (int qq = 7; qq >= 0; --qq) {
-      if (qq < Q && qq > q) {
-        const double* r = rem + (qq * RG + t) * 7;
-        const double nx = r[3] + r[5] * xx + r[6] * yin_x[qq];
-        const double ny = r[4] + r[5] * xy + r[6] * yin_y[qq];
-        xx = nx;
-        xy = ny;
-      }
-    }
-    car[t * 4 + 0] = myx;
-    car[t * 4 + 1] = myy;
-    car[t * 4 + 2] = xx;
-    car[t * 4 + 3] = xy;
-  }
-  __syncthreads();
-  // ---- phase 2: true carries, fix-up, backward sweep (laplacian.py:288-300)
-  if (has) {
-    const double cyx = car[d * 4 + 0], cyy = car[d * 4 + 1], cxx = car[d * 4 + 2], cxy = car[d * 4 + 3];
-    const double2 yin = make_double2(fma(pre.g, cyx, pre.a.x), fma(pre.g, cyy, pre.a.y));
-    const double2 xin = make_double2(xc.x + xk * cyx + xp * cxx, xc.y + xk * cyy + xp * cxy);
-    double gg = 1.0, Lp = Lin;
-#pragma unroll
-    for (int rr = 0; rr < SUB; ++rr) {
-      if (rr >= rs && rr <= re) {
-        gg = (ib + rr - m == 0) ? 0.0 : -Lp * gg;
-        const double2 y = mine[rr * RG];
-        mine[rr * RG] = make_double2(fma(gg, yin.x, y.x), fma(gg, yin.y, y.y));
-        Lp = Lr[rr];
-      }
-    }
-    const int64_t pstride = (A.ldp + 1) * 2;
-    double* pp = p + ((int64_t)ib * A.ldp + (ib - m)) * 2;
-    double2 x = xin;
-#pragma unroll
-    for (int rr = SUB - 1; rr >= 0; --rr) {
-      if (rr >= rs && rr <= re) {
-        const double2 y = mine[rr * RG];
-        x = make_double2(fma(-Lr[rr], x.x, Dr[rr] * y.x), fma(-Lr[rr], x.y, Dr[rr] * y.y));
-        st2(pp + rr * pstride, make_double2(-x.x, -x.y));  // P[i][i-m] = -x
-        mine[rr * RG] = x;
-      }
-    }
-  }
-  __syncthreads();
-  // ---- strict upper by skew reflection, P[i-m][i] = conj(x): output row j'
-  // takes columns j'+m0 .. j'+m0+3 from rows j'+m0+e of diagonal m0+e
-  {
-    const int rows = J * SUB;
-    const int jlo = r0 - m0 - (RG - 1), jhi = r0 + rows - m0;
-    for (int idx = t; idx < (jhi - jlo) * RG; idx += blockDim.x) {
-      const int jr = jlo + idx / RG, e = idx % RG;
-      const int mm = m0 + e;
-      const int i = jr + mm;
-      const int rl = i - r0;
-      if (rl < 0 || rl >= rows || i >= n || jr < 0 || mm >= n) continue;
-      const double2 xv =
-          *(reinterpret_cast<const double2*>(tile + (rl / SUB) * RSTRIDE + (rl % SUB) * (RG * 16)) + (RG - 1 - e));
-      st2(p + ((size_t)jr * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
-    }
-  }
-  cluster_wait();
-}
-
 __device__ __forceinline__ void tile_coords(int t, int& c, int& g) {
   c = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((c + 1) * (c + 2) / 2 <= t) ++c;
@@ -1300,7 +944,7 @@ static size_t op_bytes(int n, int C) {
   const size_t nsub = (size_t)(n + SUB - 1) / SUB;
   const size_t ngen = generic_tiles(n).size();
   return sizeof(double) * ((size_t)4 * n + 2 * nsub * n + (size_t)4 * C * n + (size_t)M0X * C) +
-         sizeof(int2) * (ngen + C) + 512;
+         sizeof(int2) * ngen + 512;
 }
 
 int op_create(int n, int device, zt_operator** out) {
@@ -1349,10 +993,6 @@ int op_create(int n, int device, zt_operator** out) {
     op->gen_tiles = reinterpret_cast<int2*>(reinterpret_cast<uintptr_t>(q + 1) & ~(uintptr_t)7);
     op->ngen = (int)gt.size();
     cudaMemcpy(op->gen_tiles, gt.data(), sizeof(int2) * gt.size(), cudaMemcpyHostToDevice);
-    std::vector<int2> g0(C);
-    for (int c = 0; c < C; ++c) g0[c] = make_int2(c, 0);
-    op->g0_tiles = op->gen_tiles + gt.size();
-    cudaMemcpy(op->g0_tiles, g0.data(), sizeof(int2) * C, cudaMemcpyHostToDevice);
   }
   k_op_sqrt_table<<<(n + 255) / 256, 256>>>(n, op->sqB, op->Bq);
   ZT_LAUNCHED();
@@ -1364,7 +1004,6 @@ int op_create(int n, int device, zt_operator** out) {
   cudaFuncSetAttribute(k_solve_merged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_solve_merged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_apply_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
-  cudaFuncSetAttribute(k_solve_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   e = cudaDeviceSynchronize();
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
@@ -1431,63 +1070,6 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
     ZT_LAUNCHED();
     return ZT_OK;
   };
-  static int resident = -1;
-  if (resident < 0) {
-    const char* e = getenv("ZT_SOLVE_RESIDENT");
-    resident = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (resident && n >= 64 && n <= 8192) {
-    // diagonals >= 8: one cluster per 4-diagonal group, W read once
-    ResArgs R;
-    R.n = n;
-    R.Q = std::max(1, std::min(8, n / 512));
-    const int S1 = (n + SUB - 1) / SUB;
-    R.segmax = (S1 + R.Q - 1) / R.Q;
-    R.g0 = 8 / RG;
-    R.ngroups = (n - 8 + RG - 1) / RG;
-    R.d0s = op->d0;
-    R.lins = op->lins;
-    R.sqB = op->sqB;
-    R.Bq = op->Bq;
-    R.w = w;
-    R.ldw = ldw;
-    R.sw = sw;
-    R.p = p;
-    R.ldp = ldp;
-    R.sp = sp;
-    const int rsmem = R.segmax * RSTRIDE + RSMEM_EXTRA;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(R.Q * R.ngroups, batch);
-    cfg.blockDim = dim3(((RG * R.segmax + 31) / 32) * 32);
-    cfg.dynamicSmemBytes = rsmem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = R.Q;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    ZT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_solve_resident, R));
-    ZT_LAUNCHED();
-    // diagonals 0..7 (incl. the deflated m = 0 block): the 3-pass tile path
-    A.ntiles = 0;
-    const int t0 = (C + SOLVE_WARPS - 1) / SOLVE_WARPS;
-    k_solve_merged<false><<<dim3(t0, batch), SOLVE_WARPS * 32, smem, st>>>(A, op->g0_tiles, C, t0);
-    ZT_LAUNCHED();
-    const int seg0 = std::max(8, (C + CE - 1) / CE);
-    if (seg0 <= 16)
-      k_solve_carry<512><<<dim3(1, batch), 32 * seg0, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x, A.yend,
-                                                               A.xst, A.m0acc, A.m0mg);
-    else
-      k_solve_carry<1024><<<dim3(1, batch), 32 * seg0, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x, A.yend,
-                                                                A.xst, A.m0acc, A.m0mg);
-    ZT_LAUNCHED();
-    k_solve_merged<true><<<dim3(t0, batch), SOLVE_WARPS * 32, smem, st>>>(A, op->g0_tiles, C, t0);
-    ZT_LAUNCHED();
-    ZT_CUDA_CHECK(cudaGetLastError());
-    return ZT_OK;
-  }
   int rc = pass(false);
   if (rc) return rc;
   const int seg = std::max(8, (C + CE - 1) / CE);  // chunk segments per carry block
