@@ -35,7 +35,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-from .basis import energy_spectrum_packed, extract_packed
+from .basis import HarmonicCoefficients, energy_spectrum_packed, extract_packed, project_packed
 from .diagnostics import hamiltonian
 from .integrator import StepperState, casimirs, midpoint_step_raw
 from .laplacian import build_operator
@@ -108,6 +108,44 @@ def casimir_drift(c0: np.ndarray, ck: np.ndarray) -> np.ndarray:
     base = np.asarray(c0, dtype=np.float64)[1:]
     denom = np.where(np.abs(base) < CASIMIR_BASELINE_FLOOR, 1.0, np.abs(base))
     return np.abs(np.asarray(ck, dtype=np.float64)[1:] - base) / denom
+
+
+def random_initial_condition(cfg, basis, rng: np.random.Generator | None = None) -> torch.Tensor:
+    """driver.py:196-225: band-limited random field, unit spectral norm.
+
+    `cfg` needs n, l_min, l_max, seed (the reference's SimConfig works).
+    Magnitudes uniform in [0.8, 1.2], uniform random phase (m = 0: real with
+    a random sign), drawn m ascending then l ascending so a seed pins the
+    coefficients bitwise; negative orders from the reality condition.  The
+    field is assembled on the device with the device basis; above N = 16 the
+    basis phase convention may differ from the reference's LAPACK-rounding
+    signs (basis.py:27-30), so the same seed gives the same coefficients but
+    not necessarily the same matrix there.
+    """
+    from .laplacian import spectral_norm
+
+    n, l_min, l_max = cfg.n, cfg.l_min, cfg.l_max
+    if l_max >= n:
+        raise ValueError(f"l_max={l_max} must be below n={n}")
+    if rng is None:
+        rng = np.random.default_rng(cfg.seed)
+    coeffs = HarmonicCoefficients.zeros(n)
+    for m in range(l_max + 1):
+        lo = max(l_min, m, 1)
+        if lo > l_max:
+            continue
+        count = l_max - lo + 1
+        amps = rng.uniform(0.8, 1.2, count)
+        if m == 0:
+            vals = amps * np.where(rng.random(count) < 0.5, -1.0, 1.0) + 0j
+        else:
+            vals = amps * np.exp(2j * np.pi * rng.random(count))
+        first = lo - max(m, 1)
+        coeffs.pos[m][first:first + count] = vals
+    coeffs.enforce_reality()
+    pos, _ = coeffs.packed(basis.data.device)
+    w = project_packed(pos, None, basis)
+    return w / spectral_norm(w)
 
 
 class DeviceRun:

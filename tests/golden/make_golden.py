@@ -23,6 +23,8 @@ Contents (all complex128 C-order unless noted):
                     random_admissible(N, default_rng(500+N), 1) (packed pos/neg),
                     its energy spectrum, project of random real coefficients
                     (test_basis.py:20-32 generator, default_rng(700+N))
+  init.npz          driver.random_initial_condition(SimConfig(n, seed, l_min,
+                    l_max), compute_basis(n)) at N = 9, 12, 16 (oracle-aligned)
   modes.npz         inputs of the reference's integrator property tests
                     (test_integrator.py) built with its spherical-harmonic basis
                     (out of scope here): single modes (N=8 l=4 m=1, N=9 l=2 m=0),
@@ -210,6 +212,18 @@ def basis():
     save_basis(os.path.join(OUT, "basis_n5.zeb"), compute_basis(5))  # formats.py:83-89
 
 
+def initial_conditions():
+    """driver.random_initial_condition at oracle-aligned sizes (basis signs match)."""
+    from zeitlin.basis import compute_basis
+    from zeitlin.driver import SimConfig, random_initial_condition
+
+    d = {}
+    for n, seed, lo, hi in ((12, 5, 2, 6), (16, 20260809, 1, 15), (9, 3, 2, 8)):
+        cfg = SimConfig(n=n, steps=0, seed=seed, l_min=lo, l_max=hi)
+        d[f"W_{n}_{seed}_{lo}_{hi}"] = random_initial_condition(cfg, compute_basis(n))
+    np.savez_compressed(os.path.join(OUT, "init.npz"), **d)
+
+
 def checkpoint():
     """A ZCK1 file written by the reference's own writer (formats.py:130-143)."""
     from zeitlin.formats import Checkpoint, write_checkpoint
@@ -221,6 +235,7 @@ def checkpoint():
 
 
 if __name__ == "__main__":
+    initial_conditions()
     basis()
     checkpoint()
     modes()
