@@ -26,6 +26,7 @@
  *   zt_basis_vectors    basis.py:119-165 compute_basis    the quantized basis eigenvectors
  *   zt_basis_extract    basis.py:319-331 extract          per-diagonal transforms
  *   zt_basis_project    basis.py:276-316 project
+ *   zt_grid_eval        diagnostics.py:113-187 evaluate_on_grid
  */
 #ifndef ZT_H_
 #define ZT_H_
@@ -157,6 +158,13 @@ int zt_basis_extract(int n, int m0, int m1, const long long* off, const long lon
 int zt_basis_project(int n, int m0, int m1, const long long* off, const long long* coff,
                      const double* vec, const double* pos, const double* neg, double* w,
                      int64_t ldw, void* stream);
+
+/* Grid rendering (diagnostics.py:113-187): the real
+ * field sum_lm w_lm Y_lm on theta_i = i pi / (nlat-1), phi_j = 2 pi j / nlon
+ * is the real part of the complex nlat x nlon `field`; `work` holds
+ * (nlat + nlon) x (lmax + 1) complex. */
+int zt_grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, const double* pos,
+                 double* work, double* field, void* stream);
 
 /* Per-kernel device timing for the roofline report: when enabled, CUDA
  * events bracket the stream solve, GEMM-1 (a = P X) and GEMM-2 (update) of

@@ -11,6 +11,7 @@ from .basis import (
     QuantizedBasis,
     compute_basis,
     energy_spectrum,
+    evaluate_on_grid,
     extract,
     hamiltonian_from_coeffs,
     load_basis,
@@ -20,7 +21,16 @@ from .basis import (
     wigner_basis_oracle,
 )
 from .diagnostics import hamiltonian
-from .driver import Checkpoint, DeviceRun, FileFormatError, read_checkpoint, write_checkpoint
+from .driver import (
+    Checkpoint,
+    DeviceRun,
+    FileFormatError,
+    random_initial_condition,
+    read_checkpoint,
+    read_grid,
+    write_checkpoint,
+    write_grid,
+)
 from .integrator import (
     FixedPointError,
     StepInfo,
@@ -57,4 +67,5 @@ __all__ = [
     "Checkpoint", "DeviceRun", "FileFormatError", "read_checkpoint", "write_checkpoint",
     "DeviceBasis", "HarmonicCoefficients", "QuantizedBasis", "compute_basis", "energy_spectrum", "extract",
     "hamiltonian_from_coeffs", "load_basis", "project", "save_basis", "threej", "wigner_basis_oracle",
+    "evaluate_on_grid", "random_initial_condition", "read_grid", "write_grid",
 ]

@@ -51,6 +51,7 @@ SIGNATURES = {
     "zt_basis_vectors": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "zt_basis_extract": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp]),
     "zt_basis_project": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp]),
+    "zt_grid_eval": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
     "zt_launch_count": (_c_i64, []),
     "zt_profile_enable": (_c_int, [_c_int]),
     "zt_profile_read": (_c_int, [_vp, _vp, _c_int]),

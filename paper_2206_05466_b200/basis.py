@@ -54,6 +54,8 @@ __all__ = [
     "save_basis",
     "load_basis",
     "QuantizedBasis",
+    "evaluate_on_grid",
+    "evaluate_on_grid_packed",
 ]
 
 BASIS_MAGIC = b"ZEB1"  # formats.py:44-48
@@ -396,6 +398,37 @@ def energy_spectrum(coeffs: HarmonicCoefficients) -> np.ndarray:
     power = np.bincount(lidx, weights=p, minlength=n)
     deg = np.arange(1, n, dtype=np.float64)
     return np.concatenate([[0.0], power[1:] / (2.0 * deg * (deg + 1.0))])
+
+
+def evaluate_on_grid_packed(n: int, pos: torch.Tensor, n_lat: int, n_lon: int, l_max: int | None = None) -> torch.Tensor:
+    """Real field sum_lm w_lm Y_lm on the equiangular grid from packed device
+    coefficients (m >= 0 part; real fields, diagnostics.py:133-187)."""
+    if n_lat < 2 or n_lon < 2:
+        raise ValueError(f"grid must be at least 2 x 2, got {n_lat} x {n_lon}")
+    l_max = n - 1 if l_max is None else l_max
+    if not 1 <= l_max <= n - 1:
+        raise ValueError(f"l_max={l_max} out of range 1..{n - 1}")
+    dev = pos.device
+    _, _, coff = _layout(n)
+    coff_dev = torch.from_numpy(coff).to(dev)
+    work = torch.empty((n_lat + n_lon) * (l_max + 1), dtype=torch.complex128, device=dev)
+    field = torch.empty((n_lat, n_lon), dtype=torch.complex128, device=dev)
+    check(lib.zt_grid_eval(n, l_max, n_lat, n_lon, coff_dev.data_ptr(), pos.data_ptr(), work.data_ptr(),
+                           field.data_ptr(), _stream_ptr(dev)))
+    return field.real.contiguous()
+
+
+def evaluate_on_grid(coeffs: HarmonicCoefficients, n_lat: int, n_lon: int, l_max: int | None = None,
+                     reality_tol: float = 1e-12, device=None) -> np.ndarray:
+    """diagnostics.py:151-187: the field on theta_i = i pi/(n_lat-1), phi_j =
+    2 pi j/n_lon (numpy out); the coefficients must describe a real field."""
+    dev_ = coeffs.reality_violation()
+    if dev_ > reality_tol * max(1.0, coeffs.max_abs()):
+        raise ValueError(f"coefficients violate the reality condition (deviation {dev_:.3e}); "
+                         "grid sampling is defined for real fields")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    pos, _ = coeffs.packed(dev)
+    return evaluate_on_grid_packed(coeffs.n, pos, n_lat, n_lon, l_max).cpu().numpy()
 
 
 def hamiltonian_from_coeffs(coeffs: HarmonicCoefficients) -> float:

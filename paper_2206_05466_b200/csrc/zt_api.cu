@@ -69,6 +69,8 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
                   cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int basis_vectors(int n, int m0, int m1, const long long* off, double* vec, cudaStream_t st);
+int grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, const double* pos, double* work,
+              double* field, cudaStream_t st);
 int basis_extract(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
                   const double* w, int64_t ldw, double* pos, double* neg, cudaStream_t st);
 int basis_project(int n, int m0, int m1, const long long* off, const long long* coff, const double* vec,
@@ -586,6 +588,12 @@ int zt_commutator(int n, const double* p, const double* w, double* c, double* wo
   int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
   if (rc) return rc;
   return skew_diff(n, work, c, st);
+}
+
+int zt_grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, const double* pos, double* work,
+                 double* field, void* stream) {
+  if (!coff || !pos || !work || !field) return fail(ZT_EINVAL, "zt_grid_eval: bad argument");
+  return grid_eval(n, lmax, nlat, nlon, coff, pos, work, field, (cudaStream_t)stream);
 }
 
 int zt_basis_vectors(int n, int m0, int m1, const long long* off, double* vec, void* stream) {

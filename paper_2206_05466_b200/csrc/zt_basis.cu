@@ -289,3 +289,87 @@ int basis_project(int n, int m0, int m1, const long long* off, const long long* 
 }
 
 }  // namespace zt
+
+namespace zt {
+
+// ---------------------------------------------------------------------------
+// Grid rendering (diagnostics.py:113-187): G[i][m] =
+// sum_l w_lm Pbar_lm(cos theta_i), one thread per (theta_i, m), the fully
+// normalised associated-Legendre recurrence evaluated in the reference's
+// operation order (no FMA contraction); the azimuthal sum is a complex GEMM
+// with the phase table e^{i m phi_j} (weight 2 for m >= 1).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_grid_legendre(int n, int lmax, int nlat, const long long* __restrict__ coff,
+                                                       const double* __restrict__ pos, double* __restrict__ g,
+                                                       int64_t ldg) {
+  const int m = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nlat || m > lmax) return;
+  const double step = 3.141592653589793 / (double)(nlat - 1);
+  const double th = (i == nlat - 1) ? 3.141592653589793 : __dmul_rn((double)i, step);  // np.linspace
+  const double ct = cos(th), st = sin(th);
+  double pmm = 1.0 / sqrt(4.0 * 3.141592653589793);
+  for (int q = 1; q <= m; ++q) {
+    const double s = -sqrt((2.0 * q + 1.0) / (2.0 * q));
+    pmm = __dmul_rn(__dmul_rn(s, st), pmm);
+  }
+  const double* cm = pos + 2 * (size_t)coff[m];
+  const int lo = max(m, 1);
+  double gr = 0.0, gi = 0.0;
+  auto add = [&](int l, double p) {
+    if (lo <= l && l <= lmax) {
+      gr = __dadd_rn(gr, __dmul_rn(cm[2 * (l - lo)], p));
+      gi = __dadd_rn(gi, __dmul_rn(cm[2 * (l - lo) + 1], p));
+    }
+  };
+  double pprev = pmm;
+  add(m, pprev);
+  if (m + 1 <= lmax) {
+    double pcur = __dmul_rn(__dmul_rn(sqrt(2.0 * m + 3.0), ct), pmm);
+    add(m + 1, pcur);
+    const int top = min(lmax, n - 1);
+    for (int l = m + 2; l <= top; ++l) {
+      const double ll = (double)l * l - (double)m * m;
+      const double a = sqrt((4.0 * l * l - 1.0) / ll);
+      const double b = sqrt(((2.0 * l + 1.0) * (l - 1.0 + m) * (l - 1.0 - m)) / ((2.0 * l - 3.0) * ll));
+      const double pn = __dsub_rn(__dmul_rn(__dmul_rn(a, ct), pcur), __dmul_rn(b, pprev));
+      add(l, pn);
+      pprev = pcur;
+      pcur = pn;
+    }
+  }
+  g[((size_t)i * ldg + m) * 2] = gr;
+  g[((size_t)i * ldg + m) * 2 + 1] = gi;
+}
+
+__global__ void k_grid_phases(int lmax, int nlon, double* __restrict__ ph) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (j >= nlon || m > lmax) return;
+  const double phi = (2.0 * 3.141592653589793 * (double)j) / (double)nlon;
+  double s, c;
+  sincos((double)m * phi, &s, &c);
+  const double wgt = m == 0 ? 1.0 : 2.0;
+  ph[((size_t)m * nlon + j) * 2] = c * wgt;
+  ph[((size_t)m * nlon + j) * 2 + 1] = s * wgt;
+}
+
+int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+               int64_t ldc, int algo, cudaStream_t st);
+
+// field (complex, nlat x nlon; the caller keeps the real part) from the
+// m >= 0 coefficients; work = nlat x (lmax+1) + (lmax+1) x nlon complex
+int grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, const double* pos, double* work,
+              double* field, cudaStream_t st) {
+  if (n < 2 || lmax < 1 || lmax > n - 1 || nlat < 2 || nlon < 2) return fail(ZT_EINVAL, "grid_eval: bad sizes");
+  double* g = work;
+  double* ph = work + (size_t)nlat * (lmax + 1) * 2;
+  k_grid_legendre<<<dim3((nlat + 127) / 128, lmax + 1), 128, 0, st>>>(n, lmax, nlat, coff, pos, g, lmax + 1);
+  ZT_LAUNCHED();
+  k_grid_phases<<<dim3((nlon + 127) / 128, lmax + 1), 128, 0, st>>>(lmax, nlon, ph);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return zgemm_rect(nlat, nlon, lmax + 1, g, lmax + 1, ph, nlon, field, nlon, 0, st);
+}
+
+}  // namespace zt

@@ -20,9 +20,10 @@ byte for byte (the reference's test_driver.py:231-248 contract).
 With a device basis (`basis.compute_basis`) each sample
 also extracts the coefficients on the device and writes the reference's
 `spectrum_<step>.csv` (rows l, E_l) with K = sum_l E(l)
-(driver.py:357-372); without one, K is the trace-form energy H, equal to it
-up to round-off (diagnostics.py:8-12).  Out of scope: grid snapshots
-(rank 4), the config file and CLI.
+(driver.py:357-372) and, with `write_grid`, the ZGD1 grid snapshot of the
+field (rank 4, driver.py:373-375); without one, K is the trace-form energy H,
+equal to it up to round-off (diagnostics.py:8-12).  Out of scope: the config
+file and CLI.
 """
 
 from __future__ import annotations
@@ -35,12 +36,19 @@ from pathlib import Path
 import numpy as np
 import torch
 
-from .basis import HarmonicCoefficients, energy_spectrum_packed, extract_packed, project_packed
+from .basis import (
+    HarmonicCoefficients,
+    energy_spectrum_packed,
+    evaluate_on_grid_packed,
+    extract_packed,
+    project_packed,
+)
 from .diagnostics import hamiltonian
 from .integrator import StepperState, casimirs, midpoint_step_raw
 from .laplacian import build_operator
 
 CHECKPOINT_MAGIC = b"ZCK1"
+GRID_MAGIC = b"ZGD1"
 FORMAT_VERSION = 1
 CASIMIR_BASELINE_FLOOR = 1e-14  # diagnostics.py:38-40
 
@@ -102,6 +110,34 @@ def read_checkpoint(path, device=None) -> Checkpoint:
     return Checkpoint(step_index=step, time=time, n=n, seed=seed, rng_state=rng_state, w=w)
 
 
+def write_grid(path, field: np.ndarray, time: float) -> None:
+    """ZGD1 snapshot (formats.py:163-168): header, then n_lat x n_lon <f8."""
+    if field.ndim != 2:
+        raise ValueError(f"grid field must be 2-D, got shape {field.shape}")
+    n_lat, n_lon = field.shape
+    header = GRID_MAGIC + struct.pack("<IId", n_lat, n_lon, time)
+    _atomic_write(Path(path), header + np.ascontiguousarray(field, dtype="<f8").tobytes())
+
+
+def read_grid(path) -> tuple[np.ndarray, float]:
+    """ZGD1 reader (formats.py:171-181)."""
+    with open(path, "rb") as fh:
+        if fh.read(4) != GRID_MAGIC:
+            raise FileFormatError(f"{path}: bad magic, expected {GRID_MAGIC!r}")
+        head = fh.read(16)
+        if len(head) != 16:
+            raise FileFormatError("truncated file while reading header")
+        n_lat, n_lon, time = struct.unpack("<IId", head)
+        if n_lat < 2 or n_lon < 2:
+            raise FileFormatError(f"{path}: invalid grid shape {n_lat} x {n_lon}")
+        raw = fh.read(8 * n_lat * n_lon)
+        if len(raw) != 8 * n_lat * n_lon:
+            raise FileFormatError("truncated file while reading grid samples")
+        if fh.read(1):
+            raise FileFormatError(f"{path}: trailing bytes after grid samples")
+    return np.frombuffer(raw, dtype="<f8").reshape(n_lat, n_lon).copy(), time
+
+
 def casimir_drift(c0: np.ndarray, ck: np.ndarray) -> np.ndarray:
     """diagnostics.py:86-110 for one sample: |C_k - C_k(0)| / |C_k(0)|, k >= 2,
     absolute error where the baseline is below 1e-14."""
@@ -154,7 +190,7 @@ class DeviceRun:
 
     def __init__(self, state: StepperState, output_dir, k_max: int = 3, sample_every: int = 10,
                  checkpoint_every: int = 100, seed: int = 0, rng_state: bytes = b"",
-                 baseline: np.ndarray | None = None, basis=None):
+                 baseline: np.ndarray | None = None, basis=None, write_grid: bool = False):
         w = state.w if isinstance(state.w, torch.Tensor) else torch.from_numpy(np.asarray(state.w))
         if not w.is_cuda:
             w = w.to(torch.device("cuda", torch.cuda.current_device()))
@@ -177,6 +213,7 @@ class DeviceRun:
         if basis is not None and basis.n != self.n:
             raise ValueError(f"basis is for N={basis.n}, state has N={self.n}")
         self.basis = basis
+        self.write_grid = write_grid and basis is not None
 
     # -- files ---------------------------------------------------------------
     def start(self) -> None:
@@ -191,7 +228,7 @@ class DeviceRun:
 
     @classmethod
     def resume(cls, checkpoint_path, output_dir, k_max=3, sample_every=10, checkpoint_every=100,
-               tol=1e-12, max_iter=10, comm_scale=1.0, basis=None):
+               tol=1e-12, max_iter=10, comm_scale=1.0, basis=None, write_grid=False):
         """Resume from a ZCK1 checkpoint and the run's run_meta.json (driver.py:300-334)."""
         out = Path(output_dir)
         meta_path, diag_path = out / "run_meta.json", out / "diagnostics.csv"
@@ -210,7 +247,7 @@ class DeviceRun:
         st = StepperState(w=cp.w, h=h, time=cp.time, step_index=cp.step_index, tol=tol,
                           max_iter=max_iter, comm_scale=comm_scale)
         run = cls(st, out, k_max=k_max, sample_every=sample_every, checkpoint_every=checkpoint_every,
-                  seed=cp.seed, rng_state=cp.rng_state, baseline=baseline, basis=basis)
+                  seed=cp.seed, rng_state=cp.rng_state, baseline=baseline, basis=basis, write_grid=write_grid)
         # drop diagnostics rows after the resume point (driver.py:241-252)
         lines = run.diag_path.read_text().splitlines()
         kept = [lines[0]] + [ln for ln in lines[1:]
@@ -229,6 +266,11 @@ class DeviceRun:
             k_val = float(energy.sum())
             lines = ["l,E_l"] + [f"{l},{format_float(energy[l])}" for l in range(1, self.n)]
             _atomic_write(self.out / f"spectrum_{self.state.step_index:08d}.csv", ("\n".join(lines) + "\n").encode())
+            if self.write_grid:
+                # driver.py:355, 373-375: l_render = min(N-1, 512) on a 2L x 4L grid
+                lr = min(self.n - 1, 512)
+                field = evaluate_on_grid_packed(self.n, pos, 2 * lr, 4 * lr, l_max=lr).cpu().numpy()
+                write_grid(self.out / f"grid_{self.state.step_index:08d}.bin", field, self.state.time)
         row = [format_float(self.state.time), format_float(h_val), format_float(k_val)]
         row += [format_float(v) for v in casimir_drift(self.baseline, ck)]
         with open(self.diag_path, "a", encoding="utf-8") as fh:

@@ -23,6 +23,9 @@ Contents (all complex128 C-order unless noted):
                     random_admissible(N, default_rng(500+N), 1) (packed pos/neg),
                     its energy spectrum, project of random real coefficients
                     (test_basis.py:20-32 generator, default_rng(700+N))
+  grids.npz         diagnostics.evaluate_on_grid of random real coefficients at
+                    (N, n_lat, n_lon, l_max) = (16, 9, 14, -), (40, 33, 64, 20),
+                    (100, 50, 80, 99)
   init.npz          driver.random_initial_condition(SimConfig(n, seed, l_min,
                     l_max), compute_basis(n)) at N = 9, 12, 16 (oracle-aligned)
   modes.npz         inputs of the reference's integrator property tests
@@ -224,6 +227,23 @@ def initial_conditions():
     np.savez_compressed(os.path.join(OUT, "init.npz"), **d)
 
 
+def grids():
+    """diagnostics.evaluate_on_grid of random real coefficients (input pinned)."""
+    from test_basis import random_real_field_coeffs
+    from zeitlin.diagnostics import evaluate_on_grid
+
+    d = {}
+    for n, nlat, nlon, lmax in ((16, 9, 14, None), (40, 33, 64, 20), (100, 50, 80, 99)):
+        c = random_real_field_coeffs(n, np.random.default_rng(900 + n))
+        d[f"pos_{n}"] = np.concatenate(c.pos)
+        d[f"neg_{n}"] = np.concatenate(c.neg)
+        d[f"grid_{n}"] = evaluate_on_grid(c, nlat, nlon, l_max=lmax)
+    np.savez_compressed(os.path.join(OUT, "grids.npz"), **d)
+    from zeitlin.formats import write_grid
+
+    write_grid(os.path.join(OUT, "grid_n16.zgd"), d["grid_16"], 0.375)  # formats.py:163-168
+
+
 def checkpoint():
     """A ZCK1 file written by the reference's own writer (formats.py:130-143)."""
     from zeitlin.formats import Checkpoint, write_checkpoint
@@ -235,6 +255,7 @@ def checkpoint():
 
 
 if __name__ == "__main__":
+    grids()
     initial_conditions()
     basis()
     checkpoint()

@@ -143,3 +143,22 @@ def test_packed_spectrum_and_errors(B):
         B.extract(np.zeros((n + 1, n + 1), dtype=complex), b)
     with pytest.raises(ValueError):
         B.wigner_basis_oracle(17)
+
+
+@pytest.mark.parametrize("n,nlat,nlon,lmax", ((16, 9, 14, None), (40, 33, 64, 20), (100, 50, 80, 99)))
+def test_evaluate_on_grid_matches_reference(B, n, nlat, nlon, lmax):
+    """diagnostics.py:113-187 on the device from the same coefficients."""
+    g = load_golden("grids.npz")
+    _, _, coff = B._layout(n)
+    c = B.HarmonicCoefficients.zeros(n)
+    p, q = g[f"pos_{n}"], g[f"neg_{n}"]
+    c.pos = [p[coff[m]:coff[m + 1]] for m in range(n)]
+    c.neg = [q[coff[m]:coff[m + 1]] for m in range(n)]
+    field = B.evaluate_on_grid(c, nlat, nlon, l_max=lmax)
+    ref = g[f"grid_{n}"]
+    assert field.shape == ref.shape
+    np.testing.assert_allclose(field, ref, atol=1e-12 * np.max(np.abs(ref)), rtol=0)
+    bad = c.copy()
+    bad.neg[1] = bad.neg[1] + 1.0
+    with pytest.raises(ValueError, match="reality"):
+        B.evaluate_on_grid(bad, nlat, nlon)

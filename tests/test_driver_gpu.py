@@ -87,7 +87,7 @@ def test_run_with_device_basis_writes_spectra(tmp_path):
 
     def go(out, steps):
         run = DeviceRun(StepperState(w=torch.from_numpy(g["W0"]).cuda(), h=0.005), out, k_max=3,
-                        sample_every=10, checkpoint_every=10, seed=1, basis=b)
+                        sample_every=10, checkpoint_every=10, seed=1, basis=b, write_grid=True)
         run.start()
         run.advance(steps)
 
@@ -99,6 +99,10 @@ def test_run_with_device_basis_writes_spectra(tmp_path):
     assert sp[0] == "l,E_l" and len(sp) == 64 and sp[1].startswith("1,")
     go(tmp_path / "b", 10)
     DeviceRun.resume(tmp_path / "b" / "checkpoint_00000010.zck", tmp_path / "b", k_max=3, sample_every=10,
-                     checkpoint_every=10, basis=b).advance(20)
-    for f in ("diagnostics.csv", "spectrum_00000020.csv", "checkpoint_00000020.zck"):
+                     checkpoint_every=10, basis=b, write_grid=True).advance(20)
+    from paper_2206_05466_b200.driver import read_grid
+
+    field, t = read_grid(tmp_path / "a" / "grid_00000020.bin")
+    assert field.shape == (126, 252) and t == pytest.approx(0.1, abs=1e-15)
+    for f in ("diagnostics.csv", "spectrum_00000020.csv", "grid_00000020.bin", "checkpoint_00000020.zck"):
         assert (tmp_path / "b" / f).read_bytes() == (tmp_path / "a" / f).read_bytes(), f

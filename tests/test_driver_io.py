@@ -57,3 +57,22 @@ def test_basis_cache_matches_reference_format(tmp_path):
         p.write_bytes(bad)
         with pytest.raises(FileFormatError):
             load_basis(p, device="cpu")
+
+
+def test_grid_snapshot_matches_reference_format(tmp_path):
+    """ZGD1 grid files (formats.py:163-181) both ways."""
+    from paper_2206_05466_b200.driver import FileFormatError, read_grid, write_grid
+
+    src = os.path.join(GOLDEN, "grid_n16.zgd")
+    field, t = read_grid(src)
+    np.testing.assert_array_equal(field, np.load(os.path.join(GOLDEN, "grids.npz"))["grid_16"])
+    assert t == 0.375
+    out = tmp_path / "g.zgd"
+    write_grid(out, field, t)
+    assert out.read_bytes() == open(src, "rb").read()
+    raw = open(src, "rb").read()
+    for bad in (b"ZGD2" + raw[4:], raw[:-8], raw + b"\0"):
+        p = tmp_path / "bad.zgd"
+        p.write_bytes(bad)
+        with pytest.raises(FileFormatError):
+            read_grid(p)
