@@ -190,7 +190,8 @@ def load_fp64_peak():
 
 def run_sharded(args):
     """Row-block sharded step (paper_2206_05466_b200/sharded.py): the same cfg
-    workload split over the ranks (strong scaling), NCCL collectives."""
+    workload split over the ranks (strong scaling); collectives fused into the
+    GEMM epilogues as peer stores (default) or NCCL calls (--transport nccl)."""
     import torch
     import torch.distributed as dist
 
@@ -215,7 +216,17 @@ def run_sharded(args):
     n = args.n
     h = H if n == N else 0.0025
     be = DeviceBackend(n, dev)
-    st = ShardedStepper(n, be, force_collectives=True)
+    transport = args.transport
+    if transport == "p2p":
+        try:
+            from paper_2206_05466_b200.sharded import PeerShardedStepper
+
+            st = PeerShardedStepper(n, be)
+        except Exception as exc:  # no symmetric memory / peer access on this box
+            print(f"[bench] p2p transport unavailable ({exc!r}); using NCCL collectives", file=sys.stderr)
+            transport = "nccl"
+    if transport == "nccl":
+        st = ShardedStepper(n, be, force_collectives=True)
     r = torch.from_numpy(cfg4_initial_numpy(n)).to(dev)
     w0 = zt.solve_stream(r, be.op)
     w0 = w0 / torch.linalg.norm(w0)
@@ -282,7 +293,11 @@ def run_sharded(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"row-block sharded midpoint step, N={n}, h={h}", "N": n, "h": h,
                    "iterations_per_step": sorted(set(iters)), "parallelism": f"rowblock{world}",
-                   "collectives": "NCCL all_gather(X) + all_to_all(a tiles) + all_reduce(max residual) per update",
+                   "transport": transport,
+                   "collectives": ("all-gather of X and all-to-all of a fused into the GEMM epilogues as NVLink "
+                                   "peer stores (torch symmetric memory), rank barrier + NCCL all_reduce(max "
+                                   "residual) per update") if transport == "p2p" else
+                                  "NCCL all_gather(X) + all_to_all(a tiles) + all_reduce(max residual) per update",
                    "l2": "no flush: per-step working set > 126 MB L2"},
         "roofline": {"bound": "tensor", "kernel": "whole sharded step (all ranks)", "achieved": achieved,
                      "peak": peak * world, "unit": "TFLOP/s", "frac": achieved / (peak * world),
@@ -498,6 +513,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="row-block sharded step over the ranks (default when WORLD_SIZE > 1)")
+    ap.add_argument("--transport", choices=("p2p", "nccl"), default="p2p",
+                    help="sharded step: collectives fused into the GEMM epilogues as peer-memory stores "
+                         "(p2p, torch symmetric memory) or NCCL all-gather / all-to-all (nccl)")
     ap.add_argument("--replicas", action="store_true",
                     help="with WORLD_SIZE > 1: independent replicas per rank instead of sharding")
     ap.add_argument("--n", type=int, default=N, help="matrix size for --sharded (cfg 5: 4096, 8192)")

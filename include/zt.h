@@ -138,6 +138,39 @@ int zt_commutator(int n, const double* p, const double* w, double* c, double* wo
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work,
                 void* stream);
 
+/* Peer-memory variants of the sharded step (rank r0 / mloc = N / G): the
+ * collectives are stores in the GEMM epilogues to NVLink peer-mapped buffers
+ * (`peers`: device array of npeer pointers, one per rank, e.g. from
+ * torch symmetric memory), visible to the peers after the kernel completes
+ * and a rank barrier.
+ *   zt_zgemm_rect_scatter      a_R = P_R X; column block h of a_R also to
+ *                              rank h's N x mloc buffer a[:, R_h] (all-to-all)
+ *   zt_zgemm_update_rows_peer  the row-block update with (a^H)_R read from
+ *                              this rank's a[:, R] buffer; the new rows also
+ *                              to every rank's N x N iterate (all-gather)
+ *   zt_rows_broadcast          a row block into every rank's N x N buffer
+ *   zt_zgemm_rect_mirror       C = A B and -conj(C^T) into `mirror` (the
+ *                              partner rank's rows of the skew-Hermitian
+ *                              b = a P, so each block pair is computed once);
+ *                              mirror == NULL and m == n: a diagonal block,
+ *                              lower tiles only, mirrored in place
+ *   zt_update_rows_ew          the row-block update from a precomputed b_R,
+ *                              residual, new rows broadcast to every rank */
+int zt_zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
+                          double* c, int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc,
+                          void* stream);
+int zt_zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* p, const double* acol, int mloc,
+                              const double* base, const double* xprev, double* out, int64_t ld, double hh,
+                              double qq, unsigned long long* resid, const unsigned long long* peers, int npeer,
+                              int r0, void* stream);
+int zt_rows_broadcast(int m, int n, const double* rows, int64_t ld, const unsigned long long* peers, int npeer,
+                      int r0, void* stream);
+int zt_zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
+                         double* c, int64_t ldc, double* mirror, int64_t ld_mirror, void* stream);
+int zt_update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
+                      const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                      unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, void* stream);
+
 /* Quantized spherical-harmonic basis (basis.py).
  * Vectors for orders m0 <= m < m1 are stored like the reference's
  * QuantizedBasis.vectors[m]: row-major (N - m) x n_l(m) doubles,

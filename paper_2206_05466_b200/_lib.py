@@ -52,6 +52,18 @@ SIGNATURES = {
     "zt_basis_extract": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp]),
     "zt_basis_project": (_c_int, [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp]),
     "zt_grid_eval": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp]),
+    "zt_zgemm_rect_scatter": (
+        _c_int, [_c_int, _c_int, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_int, _c_int, _c_int, _vp]),
+    "zt_zgemm_update_rows_peer": (
+        _c_int,
+        [_c_int, _c_int, _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_i64, _c_dbl, _c_dbl, _vp, _vp, _c_int, _c_int, _vp],
+    ),
+    "zt_rows_broadcast": (_c_int, [_c_int, _c_int, _vp, _c_i64, _vp, _c_int, _c_int, _vp]),
+    "zt_zgemm_rect_mirror": (_c_int, [_c_int, _c_int, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp]),
+    "zt_update_rows_ew": (
+        _c_int,
+        [_c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_dbl, _vp, _vp, _c_int, _c_int, _vp],
+    ),
     "zt_launch_count": (_c_i64, []),
     "zt_profile_enable": (_c_int, [_c_int]),
     "zt_profile_read": (_c_int, [_vp, _vp, _c_int]),

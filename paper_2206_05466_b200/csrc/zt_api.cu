@@ -68,6 +68,20 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
                   cudaStream_t st);
 size_t zupdate_split_bytes(int n);
+int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                       int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc, int algo,
+                       cudaStream_t st);
+int zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* p, const double* acol, int mloc,
+                           const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                           unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, int algo,
+                           cudaStream_t st);
+int rows_broadcast(int m, int n, const double* rows, int64_t ld, const unsigned long long* peers, int npeer, int r0,
+                   cudaStream_t st);
+int zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                      int64_t ldc, double* mirror, int64_t ld_mirror, int algo, cudaStream_t st);
+int update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
+                   const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                   unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, cudaStream_t st);
 int basis_vectors(int n, int m0, int m1, const long long* off, double* vec, cudaStream_t st);
 int grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, const double* pos, double* work,
               double* field, cudaStream_t st);
@@ -594,6 +608,44 @@ int zt_grid_eval(int n, int lmax, int nlat, int nlon, const long long* coff, con
                  double* field, void* stream) {
   if (!coff || !pos || !work || !field) return fail(ZT_EINVAL, "zt_grid_eval: bad argument");
   return grid_eval(n, lmax, nlat, nlon, coff, pos, work, field, (cudaStream_t)stream);
+}
+
+int zt_zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
+                          double* c, int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc,
+                          void* stream) {
+  if (!a || !b || !c || !peers) return fail(ZT_EINVAL, "zt_zgemm_rect_scatter: bad argument");
+  return zgemm_rect_scatter(m, n, k, a, lda, b, ldb, c, ldc, peers, npeer, r0, mloc, g_algo, (cudaStream_t)stream);
+}
+
+int zt_zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* p, const double* acol, int mloc,
+                              const double* base, const double* xprev, double* out, int64_t ld, double hh,
+                              double qq, unsigned long long* resid, const unsigned long long* peers, int npeer,
+                              int r0, void* stream) {
+  if (!a_rows || !p || !acol || !base || !out || (npeer && !peers))
+    return fail(ZT_EINVAL, "zt_zgemm_update_rows_peer: bad argument");
+  return zgemm_update_rows_peer(m, n, a_rows, p, acol, mloc, base, xprev, out, ld, hh, qq, resid, peers, npeer, r0,
+                                g_algo, (cudaStream_t)stream);
+}
+
+int zt_zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
+                         double* c, int64_t ldc, double* mirror, int64_t ld_mirror, void* stream) {
+  if (!a || !b || !c) return fail(ZT_EINVAL, "zt_zgemm_rect_mirror: bad argument");
+  return zgemm_rect_mirror(m, n, k, a, lda, b, ldb, c, ldc, mirror, ld_mirror, g_algo, (cudaStream_t)stream);
+}
+
+int zt_update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
+                      const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                      unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, void* stream) {
+  if (!a_rows || !acol || !b_rows || !base || !out || (npeer && !peers))
+    return fail(ZT_EINVAL, "zt_update_rows_ew: bad argument");
+  return update_rows_ew(m, n, a_rows, acol, mloc, b_rows, base, xprev, out, ld, hh, qq, resid, peers, npeer, r0,
+                        (cudaStream_t)stream);
+}
+
+int zt_rows_broadcast(int m, int n, const double* rows, int64_t ld, const unsigned long long* peers, int npeer,
+                      int r0, void* stream) {
+  if (!rows || !peers) return fail(ZT_EINVAL, "zt_rows_broadcast: bad argument");
+  return rows_broadcast(m, n, rows, ld, peers, npeer, r0, (cudaStream_t)stream);
 }
 
 int zt_basis_vectors(int n, int m0, int m1, const long long* off, double* vec, void* stream) {

@@ -99,6 +99,24 @@ struct GemmArgs {
   double hh, qq;       // new = base + hh (a - a^H) + qq b
   unsigned long long* resid;  // max |new - xprev| bits
   unsigned long long* cons;   // max |base - hh(a-a^H) + qq b - wn| bits
+  // peer-memory collectives fused into the epilogue (sharded step): `peers`
+  // holds npeer device pointers (one per rank, NVLink peer-mapped).
+  //   EPI_STORE: element (i, j) of this rank's row block (global row r0 + i)
+  //     also goes to rank h = j / mloc's N x mloc buffer a[:, R_h] at
+  //     (r0 + i, j - h mloc) -- the all-to-all behind (a^H)_R;
+  //   EPI_ROWS: every output element also goes to each rank's N x N iterate
+  //     at (r0 + i, j) -- the all-gather of the next iterate;
+  //     with `acol` set, (a^H)_R[i][j] = conj(acol[j][i]) (acol: N x mloc).
+  const unsigned long long* peers;
+  int npeer, r0, mloc;
+  const double* acol;
+  // EPI_STORE: also -conj(C^T) into `mirror` (ld_mirror), e.g. the partner
+  // rank's rows of a skew-Hermitian product
+  double* mirror;
+  int64_t ld_mirror;
+  // EPI_STORE on a square skew-Hermitian block: lower tiles only, the strict
+  // upper tiles stored as -conj of the lower ones
+  int lower;
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -228,9 +246,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const Acc<ALGO>
         if (gi >= mrows || gj >= n) continue;
         if (EPI == EPI_STORE) {
           st2(g.c + ((size_t)gi * g.ldc + gj) * 2, make_double2(cr, ci));
+          if (g.npeer) {
+            const int h = gj / g.mloc;
+            double* dst = reinterpret_cast<double*>(g.peers[h]);
+            st2(dst + ((size_t)(g.r0 + gi) * g.mloc + (gj - h * g.mloc)) * 2, make_double2(cr, ci));
+          }
+          if (g.mirror) st2(g.mirror + ((size_t)gj * g.ld_mirror + gi) * 2, make_double2(-cr, ci));
+          if (g.lower && I != J) st2(g.c + ((size_t)gj * g.ldc + gi) * 2, make_double2(-cr, ci));
         } else if (EPI == EPI_ROWS) {
           const size_t o = ((size_t)gi * g.ld + gj) * 2;
-          const double2 aij = ld2_plain(g.amat + o), ahij = ld2_plain(g.ah + o);
+          const double2 aij = ld2_plain(g.amat + o);
+          double2 ahij;
+          if (g.acol) {
+            const double2 t = ld2_plain(g.acol + ((size_t)gj * g.mloc + gi) * 2);
+            ahij = make_double2(t.x, -t.y);
+          } else {
+            ahij = ld2_plain(g.ah + o);
+          }
           const double2 dij = csub(aij, ahij);  // (a - a^H) on this row block
           const double2 base = ld2_plain(g.base + o);
           const double2 nw = cadd(cadd(base, rmul(g.hh, dij)), rmul(g.qq, make_double2(cr, ci)));
@@ -239,6 +271,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& g, const Acc<ALGO>
             rmax = nanmax(rmax, hypot(nw.x - xp.x, nw.y - xp.y));
           }
           st2(g.out + o, nw);
+          for (int h = 0; h < g.npeer; ++h)
+            st2(reinterpret_cast<double*>(g.peers[h]) + ((size_t)(g.r0 + gi) * g.n + gj) * 2, nw);
         } else {
           const size_t oij = ((size_t)gi * g.ld + gj) * 2, oji = ((size_t)gj * g.ld + gi) * 2;
           const double2 aij = ld2_plain(g.amat + oij), aji = ld2_plain(g.amat + oji);
@@ -346,7 +380,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
   const int mrows = g.m;
   const int T = (n + BM - 1) / BM;
   int I, J;
-  if (EPI == EPI_UPDATE) {
+  if (EPI == EPI_UPDATE || (EPI == EPI_STORE && g.lower)) {
     tile_of(blockIdx.x, true, T, I, J);
   } else {
     // grouped rasterisation over a (ceil(m/64) x ceil(n/64)) tile grid
@@ -396,6 +430,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant
   }
   double rmax = 0.0, cmax = 0.0;
   epilogue_tile<ALGO, EPI>(g, acc, I, J, wm, wn, lane, rmax, cmax);
+  if (g.npeer || g.mirror) __threadfence_system();  // peer stores visible before the rank barrier
   if (EPI != EPI_STORE) reduce_max_atomic(rmax, cmax, g.resid, g.cons, red_res, red_cons);
 }
 
@@ -796,6 +831,184 @@ int zgemm_rect(int m, int n, int k, const double* a, int64_t lda, const double* 
   const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, nt, st);
   return launch<ALGO_3M, EPI_STORE>(g, nt, st);
+}
+
+// Rectangular product whose epilogue also scatters the result's column
+// blocks into the ranks' a[:, R_h] buffers (fused all-to-all).
+int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                       int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc, int algo,
+                       cudaStream_t st) {
+  if (m < 1 || n < 1 || k < 1 || npeer < 1 || mloc < 1 || n != npeer * mloc)
+    return fail(ZT_EINVAL, "zgemm_rect_scatter: bad sizes");
+  GemmArgs g{};
+  g.n = n;
+  g.m = m;
+  g.k = k;
+  g.a = a;
+  g.lda = lda;
+  g.b = b;
+  g.ldb = ldb;
+  g.c = c;
+  g.ldc = ldc;
+  g.peers = peers;
+  g.npeer = npeer;
+  g.r0 = r0;
+  g.mloc = mloc;
+  const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, nt, st);
+  return launch<ALGO_3M, EPI_STORE>(g, nt, st);
+}
+
+// Row-block update reading (a^H)_R from this rank's a[:, R] buffer and
+// broadcasting the new rows into every rank's N x N iterate (fused all-gather).
+int zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* p, const double* acol, int mloc,
+                           const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                           unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, int algo,
+                           cudaStream_t st) {
+  if (m < 1 || n < 1 || npeer < 0 || !acol) return fail(ZT_EINVAL, "zgemm_update_rows_peer: bad arguments");
+  GemmArgs g{};
+  g.n = n;
+  g.m = m;
+  g.k = n;
+  g.a = a_rows;
+  g.lda = ld;
+  g.b = p;
+  g.ldb = n;
+  g.amat = a_rows;
+  g.acol = acol;
+  g.mloc = mloc;
+  g.base = base;
+  g.xprev = xprev;
+  g.out = out;
+  g.ld = ld;
+  g.hh = hh;
+  g.qq = qq;
+  g.resid = resid;
+  g.peers = peers;
+  g.npeer = npeer;
+  g.r0 = r0;
+  const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  if (algo == ALGO_4M) return launch<ALGO_4M, EPI_ROWS>(g, nt, st);
+  return launch<ALGO_3M, EPI_ROWS>(g, nt, st);
+}
+
+// C = A B (m x n, inner k) and -conj(C^T) into `mirror` (n x m, ld_mirror):
+// one skew-Hermitian block product for this rank and its partner.
+int zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
+                      int64_t ldc, double* mirror, int64_t ld_mirror, int algo, cudaStream_t st) {
+  if (m < 1 || n < 1 || k < 1) return fail(ZT_EINVAL, "zgemm_rect_mirror: sizes must be positive");
+  if (!mirror && m == n) {
+    // a diagonal block of the skew-Hermitian product: lower tiles + mirror in place
+    GemmArgs g{};
+    g.n = n;
+    g.m = m;
+    g.k = k;
+    g.a = a;
+    g.lda = lda;
+    g.b = b;
+    g.ldb = ldb;
+    g.c = c;
+    g.ldc = ldc;
+    g.lower = 1;
+    const int T = (n + BM - 1) / BM;
+    if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, T * (T + 1) / 2, st);
+    return launch<ALGO_3M, EPI_STORE>(g, T * (T + 1) / 2, st);
+  }
+  GemmArgs g{};
+  g.n = n;
+  g.m = m;
+  g.k = k;
+  g.a = a;
+  g.lda = lda;
+  g.b = b;
+  g.ldb = ldb;
+  g.c = c;
+  g.ldc = ldc;
+  g.mirror = mirror;
+  g.ld_mirror = ld_mirror;
+  const int nt = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  if (algo == ALGO_4M) return launch<ALGO_4M, EPI_STORE>(g, nt, st);
+  return launch<ALGO_3M, EPI_STORE>(g, nt, st);
+}
+
+// Elementwise row-block update from a precomputed b_R (the skew-balanced
+// sharded GEMM-2): new = base + hh (a_R - conj(acol)^T) + qq b_R, residual
+// max |new - xprev|, new rows also into every rank's N x N iterate.
+__global__ void __launch_bounds__(256) k_update_rows_ew(int m, int n, const double* __restrict__ a_rows,
+                                                        const double* __restrict__ acol, int mloc,
+                                                        const double* __restrict__ b_rows,
+                                                        const double* __restrict__ base, const double* xprev,
+                                                        double* out, int64_t ld, double hh, double qq,
+                                                        unsigned long long* resid,
+                                                        const unsigned long long* __restrict__ peers, int npeer,
+                                                        int r0) {
+  __shared__ double2 tile[32][33];
+  const int bj = blockIdx.x * 32, bi = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // (a^H)_R[i][j] = conj(acol[j][i]): stage the transposed 32 x 32 block
+  for (int r = ty; r < 32; r += 8) {
+    const int j = bj + r, i = bi + tx;
+    tile[r][tx] = (j < n && i < m) ? ld2(acol + ((size_t)j * mloc + i) * 2) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double rmax = 0.0;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi + r, j = bj + tx;
+    if (i >= m || j >= n) continue;
+    const size_t o = ((size_t)i * ld + j) * 2;
+    const double2 aij = ld2(a_rows + o), t = tile[tx][r];
+    const double2 d = make_double2(__dsub_rn(aij.x, t.x), __dadd_rn(aij.y, t.y));  // a - conj(acol^T)
+    const double2 bb = ld2(b_rows + o);
+    const double2 nw = cadd(cadd(ld2(base + o), rmul(hh, d)), rmul(qq, bb));
+    if (xprev) {
+      const double2 xp = *reinterpret_cast<const double2*>(xprev + o);
+      rmax = nanmax(rmax, hypot(nw.x - xp.x, nw.y - xp.y));
+    }
+    st2(out + o, nw);
+    for (int h = 0; h < npeer; ++h) st2(reinterpret_cast<double*>(peers[h]) + ((size_t)(r0 + i) * n + j) * 2, nw);
+  }
+  if (npeer) __threadfence_system();
+  if (resid) {
+    unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(rmax));
+    if (rmax != rmax) bits = 0x7ff8000000000000ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffff, bits, off));
+    if (tx == 0) atomicMax(resid, bits);
+  }
+}
+
+int update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
+                   const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
+                   unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, cudaStream_t st) {
+  if (m < 1 || n < 1) return fail(ZT_EINVAL, "update_rows_ew: bad sizes");
+  dim3 grid((n + 31) / 32, (m + 31) / 32);
+  k_update_rows_ew<<<grid, 256, 0, st>>>(m, n, a_rows, acol, mloc, b_rows, base, xprev, out, ld, hh, qq, resid,
+                                         peers, npeer, r0);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+// Copy a row block into every rank's N x N buffer at rows r0.. (seeds the
+// gathered iterate with W_n at the start of a sharded step).
+__global__ void k_rows_broadcast(int m, int n, const double* __restrict__ rows, int64_t ld,
+                                 const unsigned long long* __restrict__ peers, int npeer, int r0) {
+  const size_t total = (size_t)m * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = e / n, j = e % n;
+    const double2 v = ld2(rows + (i * ld + j) * 2);
+    for (int h = 0; h < npeer; ++h) st2(reinterpret_cast<double*>(peers[h]) + ((r0 + i) * (size_t)n + j) * 2, v);
+  }
+  __threadfence_system();
+}
+
+int rows_broadcast(int m, int n, const double* rows, int64_t ld, const unsigned long long* peers, int npeer, int r0,
+                   cudaStream_t st) {
+  if (m < 1 || n < 1 || npeer < 1) return fail(ZT_EINVAL, "rows_broadcast: bad sizes");
+  k_rows_broadcast<<<592, 256, 0, st>>>(m, n, rows, ld, peers, npeer, r0);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
 }
 
 // Row-block update of the sharded step: b = a_R P (m x n, inner n);

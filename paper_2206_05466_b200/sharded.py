@@ -165,3 +165,214 @@ class ShardedStepper:
         wt, k, r = self.fixed_point(w_rows, h, tol, max_iter)
         out, _ = self._update(wt, wt, 0.5 * h, -0.25 * h * h, residual=False)
         return out, k, r
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory variant: the two data-path collectives are fused into the GEMM
+# epilogues as NVLink stores into the other ranks' buffers.
+#
+#   all-gather of the iterate  -> the update epilogue writes every new row of
+#                                 X_R into each rank's N x N iterate buffer
+#                                 (zt_zgemm_update_rows_peer), overlapped with
+#                                 the GEMM-2 tiles that produce them;
+#   all-to-all for (a^H)_R     -> the GEMM-1 epilogue writes column block h of
+#                                 a_R into rank h's N x (N/G) buffer a[:, R_h]
+#                                 (zt_zgemm_rect_scatter), which the update
+#                                 epilogue reads transposed.
+#
+# GEMM-2 is balanced over the skew symmetry of b = a P = P X P: of every
+# pair of off-diagonal blocks b[R_g, R_h], b[R_h, R_g] = -b[R_g, R_h]^H only
+# one is multiplied (rank g for h = g+1 .. g+G/2-1 mod G, the G/2 pair split
+# in halves), and its epilogue stores -conj(block^T) straight into the
+# partner's b rows (zt_zgemm_rect_mirror) -- (G+1)/2 instead of G blocks of
+# m x m x N per rank, the work of the single-GPU lower-tile scheme.
+#
+# Per fixed-point update a rank runs: solve on its gathered iterate ->
+# GEMM-1 + scatter -> barrier -> GEMM-2 blocks + mirror -> barrier ->
+# elementwise update + broadcast -> all-reduce(max) of the residual (which
+# also orders the broadcast before the next solve).  `peer_midpoint_step` holds the algorithm once for a list of
+# ranks: one rank per process on a real NVSwitch box (torch symmetric memory
+# for the peer pointers), or G virtual ranks on one GPU executed phase by
+# phase (tests: no kernel ever waits on another rank's kernel).
+# ---------------------------------------------------------------------------
+
+
+class PeerRank:
+    """One rank's buffers and kernels for the peer-fused sharded step."""
+
+    def __init__(self, n: int, world: int, rank: int, backend: DeviceBackend, xfull: torch.Tensor,
+                 acol: torch.Tensor, xptrs: torch.Tensor, aptrs: torch.Tensor, brows: torch.Tensor,
+                 bptrs: list[int]):
+        if n % world:
+            raise ValueError(f"N={n} must be divisible by the number of ranks {world}")
+        self.n, self.world, self.rank = n, world, rank
+        self.m = n // world
+        self.r0 = rank * self.m
+        self.be = backend
+        self.xfull, self.acol = xfull, acol  # this rank's N x N iterate, N x m block a[:, R]
+        self.xptrs, self.aptrs = xptrs, aptrs  # int64 device arrays: every rank's buffers
+        self.brows, self.bptrs = brows, bptrs  # this rank's m x N rows of b; every rank's (host ints)
+        self._flag = torch.zeros(1, dtype=torch.int64, device=backend.device)
+
+    def _s(self):
+        return self.be._stream(self.be.device)
+
+    def seed(self, w_rows: torch.Tensor) -> None:
+        lib = self.be._lib
+        lib.check(lib.lib.zt_rows_broadcast(self.m, self.n, w_rows.data_ptr(), self.n, self.xptrs.data_ptr(),
+                                            self.world, self.r0, self._s()))
+
+    def phase1(self, validate: bool) -> None:
+        """P = lap^-1 X on the gathered iterate; a_R = P_R X with the column
+        blocks scattered to their owners."""
+        lib = self.be._lib
+        if validate:
+            self.be.validate(self.xfull)
+        self.p = self.be.solve(self.xfull)
+        self.a_rows = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
+        lib.check(lib.lib.zt_zgemm_rect_scatter(
+            self.m, self.n, self.n, self.p[self.r0:].data_ptr(), self.n, self.xfull.data_ptr(), self.n,
+            self.a_rows.data_ptr(), self.n, self.aptrs.data_ptr(), self.world, self.r0, self.m, self._s()))
+
+    def blocks(self):
+        """GEMM-2 blocks this rank multiplies: (row0, nrows, col0, ncols, partner
+        or None) in local rows / global columns (see the header)."""
+        g, G, m = self.rank, self.world, self.m
+        out = [(0, m, g * m, m, None)]
+        for d in range(1, G):
+            h = (g + d) % G
+            if 2 * d < G:
+                out.append((0, m, h * m, m, h))
+            elif 2 * d == G:
+                half = m // 2
+                if g < h:  # all my rows x the first half of h's columns
+                    out.append((0, m, h * m, half, h))
+                else:      # the second half of my rows x all of h's columns
+                    out.append((half, m - half, h * m, m, h))
+        return out
+
+    def phase2a(self):
+        """b = a_R P on this rank's share of blocks, mirrors to the partners."""
+        lib, n = self.be._lib, self.n
+        esz = 16
+        for r0, nr, c0, nc, h in self.blocks():
+            a_ptr = self.a_rows.data_ptr() + r0 * n * esz
+            b_ptr = self.p.data_ptr() + c0 * esz
+            c_ptr = self.brows.data_ptr() + (r0 * n + c0) * esz
+            if h is None:
+                mir = None
+            else:  # partner rows (c0 - h m) .., columns r0_g + r0 ..
+                mir = self.bptrs[h] + ((c0 - h * self.m) * n + self.r0 + r0) * esz
+            lib.check(lib.lib.zt_zgemm_rect_mirror(nr, nc, n, a_ptr, n, b_ptr, n, c_ptr, n, mir, n, self._s()))
+
+    def phase2b(self, base_rows, xprev_rows, hh: float, qq: float):
+        """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, broadcast to every rank."""
+        lib = self.be._lib
+        out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
+        self._flag.zero_()
+        lib.check(lib.lib.zt_update_rows_ew(
+            self.m, self.n, self.a_rows.data_ptr(), self.acol.data_ptr(), self.m, self.brows.data_ptr(),
+            base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
+            self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
+        bits = int(self._flag.item())
+        return out, torch.tensor([bits], dtype=torch.int64).view(torch.float64).item()
+
+    def phase2(self, base_rows, xprev_rows, hh: float, qq: float):
+        """Unbalanced alternative: full rows of b per rank, fused update epilogue."""
+        lib = self.be._lib
+        out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
+        self._flag.zero_()
+        lib.check(lib.lib.zt_zgemm_update_rows_peer(
+            self.m, self.n, self.a_rows.data_ptr(), self.p.data_ptr(), self.acol.data_ptr(), self.m,
+            base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
+            self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
+        bits = int(self._flag.item())
+        return out, torch.tensor([bits], dtype=torch.int64).view(torch.float64).item()
+
+
+def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda: None,
+                       allreduce_max=lambda v: v):
+    """integrator.py:96-171 over row blocks with peer-fused collectives.
+    `ranks` / `w_rows`: the ranks this process drives and their rows of W_n.
+    Returns (rows of W_{n+1}, iterations, residual)."""
+    from .integrator import FixedPointError
+
+    if h < 0.0:
+        raise ValueError(f"time-step must be nonnegative, got {h}")
+    if tol <= 0.0:
+        raise ValueError(f"tolerance must be positive, got {tol}")
+    if max_iter < 1:
+        raise ValueError(f"max_iter must be at least 1, got {max_iter}")
+    hh, qq = 0.5 * h, 0.25 * h * h
+    for rk, w in zip(ranks, w_rows):
+        rk.seed(w)
+    barrier()
+    x = list(w_rows)
+    r = math.inf
+    for k in range(1, max_iter + 1):
+        for rk in ranks:
+            rk.phase1(validate=(k == 1))
+        barrier()
+        for rk in ranks:
+            rk.phase2a()
+        barrier()
+        new, res = [], []
+        for rk, xr, wr in zip(ranks, x, w_rows):
+            nx, rr = rk.phase2b(wr, xr, hh, qq)
+            new.append(nx)
+            res.append(math.inf if rr != rr else rr)
+        r = allreduce_max(max(res))  # also orders the broadcast before the next solve
+        x = new
+        if r <= tol:
+            break
+    else:
+        raise FixedPointError(
+            f"fixed-point iteration did not reach tol={tol:.1e} in {max_iter} iterations "
+            f"(last residual {r:.3e})", residual=r, iterations=max_iter)
+    for rk in ranks:
+        rk.phase1(validate=False)
+    barrier()
+    for rk in ranks:
+        rk.phase2a()
+    barrier()
+    out = [rk.phase2b(xr, None, hh, -qq)[0] for rk, xr in zip(ranks, x)]
+    barrier()
+    return out, k, r
+
+
+class PeerShardedStepper:
+    """One process per GPU: peer buffers from torch symmetric memory, the rank
+    barrier from its signal pads, the residual all-reduce over NCCL."""
+
+    def __init__(self, n: int, backend: DeviceBackend, group=None):
+        import torch.distributed._symmetric_memory as symm
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if n % self.world:
+            raise ValueError(f"N={n} must be divisible by the number of ranks {self.world}")
+        dev = backend.device
+        m = n // self.world
+        xfull = symm.empty((n, n), dtype=torch.complex128, device=dev)
+        acol = symm.empty((n, m), dtype=torch.complex128, device=dev)
+        brows = symm.empty((m, n), dtype=torch.complex128, device=dev)
+        name = self.group.group_name
+        self._hx = symm.rendezvous(xfull, name)
+        self._ha = symm.rendezvous(acol, name)
+        self._hb = symm.rendezvous(brows, name)
+        xptrs = torch.tensor(self._hx.buffer_ptrs, dtype=torch.int64, device=dev)
+        aptrs = torch.tensor(self._ha.buffer_ptrs, dtype=torch.int64, device=dev)
+        self.r = PeerRank(n, self.world, self.rank, backend, xfull, acol, xptrs, aptrs, brows,
+                          list(self._hb.buffer_ptrs))
+        self.n, self.m, self.r0 = n, m, self.r.r0
+
+    def _allreduce_max(self, v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=self.r.be.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def midpoint_step(self, w_rows, h, tol=1e-12, max_iter=10):
+        out, k, r = peer_midpoint_step([self.r], [w_rows], h, tol, max_iter,
+                                       barrier=self._hx.barrier, allreduce_max=self._allreduce_max)
+        return out[0], k, r

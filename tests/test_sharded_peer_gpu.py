@@ -1,0 +1,101 @@
+"""Peer-fused sharded step (sharded.py: collectives as epilogue stores into
+the other ranks' buffers).  G virtual ranks on one GPU run the algorithm
+phase by phase (every kernel's inputs are complete before it starts; no rank
+waits on another), and must reproduce the single-GPU step; the symmetric-
+memory path runs on a one-rank NCCL group."""
+
+import numpy as np
+import pytest
+import torch
+from conftest import relf
+
+from oracle import zeitlin_oracle as zo
+
+pytestmark = pytest.mark.gpu
+
+
+def _virtual_ranks(n, world, dev):
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerRank
+
+    be = DeviceBackend(n, dev)
+    m = n // world
+    xf = [torch.zeros((n, n), dtype=torch.complex128, device=dev) for _ in range(world)]
+    ac = [torch.zeros((n, m), dtype=torch.complex128, device=dev) for _ in range(world)]
+    br = [torch.full((m, n), float("nan"), dtype=torch.complex128, device=dev) for _ in range(world)]
+    xp = torch.tensor([t.data_ptr() for t in xf], dtype=torch.int64, device=dev)
+    ap = torch.tensor([t.data_ptr() for t in ac], dtype=torch.int64, device=dev)
+    bp = [t.data_ptr() for t in br]
+    return [PeerRank(n, world, g, be, xf[g], ac[g], xp, ap, br[g], bp) for g in range(world)]
+
+
+@pytest.mark.parametrize("n,world", ((256, 2), (512, 4), (384, 3), (512, 8), (640, 5), (768, 6)))
+def test_virtual_ranks_match_single_gpu(n, world):
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+    from paper_2206_05466_b200.laplacian import build_operator
+    from paper_2206_05466_b200.sharded import peer_midpoint_step
+
+    dev = torch.device("cuda:0")
+    w = torch.from_numpy(zo.smooth_initial(n)).to(dev)
+    ranks = _virtual_ranks(n, world, dev)
+    m = n // world
+    rows = [w[g * m:(g + 1) * m].contiguous() for g in range(world)]
+    ref = w
+    op = build_operator(n, dev)
+    for _ in range(3):
+        rows, k, r = peer_midpoint_step(ranks, rows, 0.005)
+        ref, kr, _, _ = midpoint_step_raw(ref, 0.005, 1e-12, 10, op)
+        assert k == kr
+    got = torch.cat(rows).cpu().numpy()
+    assert relf(got, ref.cpu().numpy()) <= 1e-13
+    # the gathered iterate on every rank equals the full new state, and the
+    # balanced GEMM-2 blocks tile b_R exactly (b rows started as NaN)
+    for rk in ranks:
+        assert relf(rk.xfull.cpu().numpy(), got) == 0.0
+        assert not torch.isnan(torch.view_as_real(rk.brows)).any()
+    work = [sum(nr * nc for _, nr, _, nc, _ in rk.blocks()) for rk in ranks]
+    m = n // world
+    assert max(work) == min(work) == m * m * (world + 1) // 2
+
+
+def test_virtual_ranks_errors_and_nonconvergence():
+    from paper_2206_05466_b200.integrator import FixedPointError
+    from paper_2206_05466_b200.sharded import peer_midpoint_step
+
+    dev = torch.device("cuda:0")
+    n, world = 128, 2
+    ranks = _virtual_ranks(n, world, dev)
+    w = torch.from_numpy(zo.random_admissible(n, np.random.default_rng(1), 1.0)).to(dev)
+    rows = [w[:64].contiguous(), w[64:].contiguous()]
+    with pytest.raises(ValueError):
+        peer_midpoint_step(ranks, rows, -1.0)
+    with pytest.raises(FixedPointError) as e:
+        peer_midpoint_step(ranks, rows, 0.5, max_iter=1)
+    assert e.value.iterations == 1 and e.value.residual > 1e-14
+
+
+def test_symmetric_memory_path_one_rank():
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper
+
+    dev = torch.device("cuda:0")
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
+        s.close()
+        dist.init_process_group("nccl", device_id=dev)
+    try:
+        n = 256
+        be = DeviceBackend(n, dev)
+        st = PeerShardedStepper(n, be)
+        w = torch.from_numpy(zo.smooth_initial(n)).to(dev)
+        out, k, _ = st.midpoint_step(w.clone(), 0.005)
+        ref, kr, _, _ = midpoint_step_raw(w, 0.005, 1e-12, 10, be.op)
+        assert k == kr and relf(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+    finally:
+        dist.destroy_process_group()
