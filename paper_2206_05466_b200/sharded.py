@@ -188,9 +188,10 @@ class ShardedStepper:
 # m x m x N per rank, the work of the single-GPU lower-tile scheme.
 #
 # Per fixed-point update a rank runs: solve on its gathered iterate ->
-# GEMM-1 + scatter -> barrier -> GEMM-2 blocks + mirror -> barrier ->
-# elementwise update + broadcast -> all-reduce(max) of the residual (which
-# also orders the broadcast before the next solve).  `peer_midpoint_step` holds the algorithm once for a list of
+# GEMM-1 + scatter -> GEMM-2 blocks + mirror -> barrier -> elementwise update
+# + broadcast -> all-reduce(max) of the residual (which also orders the
+# broadcast before the next solve and the next scatter after this update's
+# reads).  `peer_midpoint_step` holds the algorithm once for a list of
 # ranks: one rank per process on a real NVSwitch box (torch symmetric memory
 # for the peer pointers), or G virtual ranks on one GPU executed phase by
 # phase (tests: no kernel ever waits on another rank's kernel).
@@ -310,9 +311,10 @@ def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda:
     x = list(w_rows)
     r = math.inf
     for k in range(1, max_iter + 1):
+        # phase 2a needs only local a_R and P; the barrier after it covers both
+        # the a scatter (phase 1) and the b mirrors (phase 2a)
         for rk in ranks:
             rk.phase1(validate=(k == 1))
-        barrier()
         for rk in ranks:
             rk.phase2a()
         barrier()
@@ -331,7 +333,6 @@ def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda:
             f"(last residual {r:.3e})", residual=r, iterations=max_iter)
     for rk in ranks:
         rk.phase1(validate=False)
-    barrier()
     for rk in ranks:
         rk.phase2a()
     barrier()
