@@ -66,7 +66,8 @@ int skew_diff(int n, const double* a, double* c, cudaStream_t st);
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
-                  cudaStream_t st);
+                  cudaStream_t st, int gemm1_only = 0);
+int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                        int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc, int algo,
@@ -162,6 +163,7 @@ static double bits_to_double(unsigned long long b) {
 static bool g_prof = false;
 struct ProfSlot {
   cudaEvent_t ev[4];
+  int final_update = 0;  // 1: [solve, a = P W~ (GEMM-1 only), W_n + h (a - a^H)]
 };
 static std::vector<ProfSlot> g_slots;
 static size_t g_used = 0;
@@ -170,7 +172,7 @@ static int64_t g_prof_cnt[3] = {0, 0, 0};
 
 static thread_local bool t_capturing = false;
 
-static void prof_mark(int which, cudaStream_t st) {
+static void prof_mark(int which, cudaStream_t st, int final_update = 0) {
   if (!g_prof || t_capturing) return;
   if (which == 0) {
     if (g_used == g_slots.size()) {
@@ -179,17 +181,25 @@ static void prof_mark(int which, cudaStream_t st) {
       g_slots.push_back(s);
     }
     ++g_used;
+    g_slots[g_used - 1].final_update = final_update;
   }
   cudaEventRecord(g_slots[g_used - 1].ev[which], st);
 }
 
 static void prof_collect() {
   if (!g_prof) return;
+  // slots: [0] stream solve, [1] full update (GEMM-1 + GEMM-2 + epilogue, or
+  // GEMM-1 alone when unfused), [2] GEMM-2 (unfused) or the step's final
+  // update (GEMM-1 only + the commutator pass)
   for (size_t i = 0; i < g_used; ++i) {
     cudaEventSynchronize(g_slots[i].ev[3]);
+    const bool fin = g_slots[i].final_update;
     for (int k = 0; k < 3; ++k) {
+      if (fin && k == 1) continue;
       float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, g_slots[i].ev[k], g_slots[i].ev[k + 1]) == cudaSuccess) {
+      const cudaEvent_t e0 = g_slots[i].ev[k], e1 = (fin && k == 2) ? g_slots[i].ev[3] : g_slots[i].ev[k + 1];
+      const cudaEvent_t s0 = (fin && k == 2) ? g_slots[i].ev[1] : e0;
+      if (cudaEventElapsedTime(&ms, s0, e1) == cudaSuccess) {
         g_prof_ms[k] += ms;
         g_prof_cnt[k] += 1;
       }
@@ -219,6 +229,29 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   if (rc) return rc;
   prof_mark(2, st);
   rc = zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, g_algo, st);
+  prof_mark(3, st);
+  return rc;
+}
+
+// The step's last update without GEMM-2 (see k_final_commutator): solve,
+// a = P W~, W_{n+1} = W_n + h (a - a^H), in place over W~.  ZT_FINAL_SANDWICH=1
+// (or a consistency request) keeps the reference's sandwich form.
+static bool g_final_comm = true;
+static int final_update(zt_operator* op, double* x, const double* wn, double h, StepWS& w, cudaStream_t st) {
+  const int n = op->n;
+  prof_mark(0, st, 1);
+  int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
+  if (rc) return rc;
+  prof_mark(1, st);
+  if (g_fused) {
+    rc = zupdate_fused(n, w.p, x, w.a, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, nullptr, w.sync,
+                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, nullptr, st, 1);
+  } else {
+    rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
+  }
+  if (rc) return rc;
+  prof_mark(2, st);
+  rc = final_commutator(n, w.a, wn, h, x, st);
   prof_mark(3, st);
   return rc;
 }
@@ -350,8 +383,13 @@ static int build_step_graph(GraphEntry& e, StepWS& w) {
   }
   int64_t c2 = g_launches.load();
   if (!rc && e.cons) rc = cudaMemsetAsync(w.flags + 1, 0, sizeof(unsigned long long), cs) ? ZT_ECUDA : ZT_OK;
-  if (!rc)
-    rc = update(op, x, x, nullptr, e.cons ? e.wn : nullptr, x, hh, -qq, w, nullptr, e.cons ? w.flags + 1 : nullptr, cs);
+  if (!rc) {
+    if (!e.cons && g_final_comm)
+      rc = final_update(op, x, e.wn, e.h, w, cs);
+    else
+      rc = update(op, x, x, nullptr, e.cons ? e.wn : nullptr, x, hh, -qq, w, nullptr, e.cons ? w.flags + 1 : nullptr,
+                  cs);
+  }
   int64_t c3 = g_launches.load();
   cudaError_t ce = cudaStreamEndCapture(cs, &graph);
   t_capturing = false;
@@ -483,6 +521,7 @@ int zt_op_create(int n, int device, zt_op_t* op) {
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
   if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
   if (const char* e = getenv("ZT_SPLIT")) g_split = std::string(e) != "0";
+  if (const char* e = getenv("ZT_FINAL_SANDWICH")) g_final_comm = std::string(e) == "0";
   return op_create(n, device, op);
 }
 int zt_op_destroy(zt_op_t op) { return op_destroy(op); }
@@ -585,8 +624,11 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
   // final update (integrator.py:154-158): W_{n+1} = W~ + (h/2)(a - a^H) - (h^2/4) a P~
   const double hh = 0.5 * h_eff, q = 0.25 * h_eff * h_eff;
   if (consistency) ZT_CUDA_CHECK(cudaMemsetAsync(w.flags + 1, 0, sizeof(unsigned long long), st));
-  rc = update(op, w_next, w_next, nullptr, consistency ? wn : nullptr, w_next, hh, -q, w, nullptr,
-              consistency ? w.flags + 1 : nullptr, st);
+  if (!consistency && g_final_comm)
+    rc = final_update(op, w_next, wn, h_eff, w, st);
+  else
+    rc = update(op, w_next, w_next, nullptr, consistency ? wn : nullptr, w_next, hh, -q, w, nullptr,
+                consistency ? w.flags + 1 : nullptr, st);
   if (rc) return rc;
   prof_collect();
   if (consistency) {
