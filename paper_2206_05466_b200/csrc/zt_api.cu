@@ -678,7 +678,7 @@ int zt_zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, cons
 int zt_update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
                       const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
                       unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, void* stream) {
-  if (!a_rows || !acol || !b_rows || !base || !out || (npeer && !peers))
+  if (!a_rows || !acol || !base || !out || (npeer && !peers))
     return fail(ZT_EINVAL, "zt_update_rows_ew: bad argument");
   return update_rows_ew(m, n, a_rows, acol, mloc, b_rows, base, xprev, out, ld, hh, qq, resid, peers, npeer, r0,
                         (cudaStream_t)stream);

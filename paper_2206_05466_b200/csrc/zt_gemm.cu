@@ -959,7 +959,7 @@ __global__ void __launch_bounds__(256) k_update_rows_ew(int m, int n, const doub
     const size_t o = ((size_t)i * ld + j) * 2;
     const double2 aij = ld2(a_rows + o), t = tile[tx][r];
     const double2 d = make_double2(__dsub_rn(aij.x, t.x), __dadd_rn(aij.y, t.y));  // a - conj(acol^T)
-    const double2 bb = ld2(b_rows + o);
+    const double2 bb = b_rows ? ld2(b_rows + o) : make_double2(0.0, 0.0);  // null: no b term
     const double2 nw = cadd(cadd(ld2(base + o), rmul(hh, d)), rmul(qq, bb));
     if (xprev) {
       const double2 xp = *reinterpret_cast<const double2*>(xprev + o);

@@ -266,13 +266,15 @@ class PeerRank:
                 mir = self.bptrs[h] + ((c0 - h * self.m) * n + self.r0 + r0) * esz
             lib.check(lib.lib.zt_zgemm_rect_mirror(nr, nc, n, a_ptr, n, b_ptr, n, c_ptr, n, mir, n, self._s()))
 
-    def phase2b(self, base_rows, xprev_rows, hh: float, qq: float):
-        """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, broadcast to every rank."""
+    def phase2b(self, base_rows, xprev_rows, hh: float, qq: float, with_b: bool = True):
+        """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, broadcast to every rank
+        (with_b=False: no b term, the final update W_n + h (a - a^H))."""
         lib = self.be._lib
         out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
         self._flag.zero_()
         lib.check(lib.lib.zt_update_rows_ew(
-            self.m, self.n, self.a_rows.data_ptr(), self.acol.data_ptr(), self.m, self.brows.data_ptr(),
+            self.m, self.n, self.a_rows.data_ptr(), self.acol.data_ptr(), self.m,
+            self.brows.data_ptr() if with_b else None,
             base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
             self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
         bits = int(self._flag.item())
@@ -331,12 +333,12 @@ def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda:
         raise FixedPointError(
             f"fixed-point iteration did not reach tol={tol:.1e} in {max_iter} iterations "
             f"(last residual {r:.3e})", residual=r, iterations=max_iter)
+    # final update W_n + h (a - a^H) at a = P~ W~ (the sandwich form's
+    # (h^2/4) a P terms cancel at the fixed point; zt_api.cu final_update)
     for rk in ranks:
         rk.phase1(validate=False)
-    for rk in ranks:
-        rk.phase2a()
     barrier()
-    out = [rk.phase2b(xr, None, hh, -qq)[0] for rk, xr in zip(ranks, x)]
+    out = [rk.phase2b(wr, None, h, 0.0, with_b=False)[0] for rk, wr in zip(ranks, w_rows)]
     barrier()
     return out, k, r
 
