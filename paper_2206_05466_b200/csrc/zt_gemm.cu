@@ -370,8 +370,9 @@ template <int ALGO, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zgemm(const __grid_constant__ GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 128B swizzle needs 1024B-aligned boxes
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // offset (not an integer cast) keeps the shared address space visible to
+  // the compiler: fragment loads become LDS, not generic LD
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   __shared__ unsigned long long red_res[CONSUMER_WARPS], red_cons[CONSUMER_WARPS];
@@ -525,8 +526,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr bool PL = (ALGO == ALGO_3MS);
   constexpr int SB = STAGE_BYTES + (PL ? SUM_STAGE_BYTES : 0);
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // offset (not an integer cast) keeps the shared address space visible to
+  // the compiler: fragment loads become LDS, not generic LD
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
   uint64_t* empty = full + STAGES;
   uint64_t* tq_full = empty + STAGES;  // [2]
