@@ -504,7 +504,7 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-update launch at
 # N=2048 from the committed `ncu --set full` capture (profiles/r01_ncu_summary.md)
-TRAFFIC_FUSED = 1300.208e6 + 174.946e6  # ncu --set full, one k_zupdate launch (profiles/r01_ncu_summary.md)
+TRAFFIC_FUSED = 1289.324e6 + 164.925e6  # ncu --set full, one k_zupdate launch (profiles/r01_ncu_summary.md)
 
 
 def main():
