@@ -38,7 +38,7 @@ def main():
     os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
     s.close()
     import torch.distributed as dist
-    from paper_2206_05466_b200.sharded import DeviceBackend, ShardedStepper
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper, ShardedStepper
 
     dist.init_process_group("nccl", device_id=dev)
     for n in args.n:
@@ -87,21 +87,23 @@ def main():
                              "drift": {"C2": abs(c1[1] - c0[1]) / abs(c0[1]), "C3": abs(c1[2] - c0[2]) / abs(c0[2]),
                                        "H": abs(h1 - h0) / abs(h0)}}
         del cur, spare
-        # the sharded code path on a one-rank group (collectives executed)
+        # the sharded code paths on a one-rank group (collectives / peer stores executed)
         be = DeviceBackend(n, dev)
-        st = ShardedStepper(n, be, force_collectives=True)
-        rows = w0.clone()
-        rows, _, _ = st.midpoint_step(rows, H, TOL, MAX_ITER)
-        torch.cuda.synchronize()
         ns = max(2, min(args.steps, 10))
-        e0.record()
-        for _ in range(ns):
-            rows, k, _ = st.midpoint_step(rows, H, TOL, MAX_ITER)
-        e1.record()
-        torch.cuda.synchronize()
-        rec["sharded_path_g1"] = {"ms_per_step": e0.elapsed_time(e1) / ns, "steps": ns}
+        for name, st in (("sharded_peer_g1", PeerShardedStepper(n, be)),
+                         ("sharded_nccl_g1", ShardedStepper(n, be, force_collectives=True))):
+            rows = w0.clone()
+            rows, _, _ = st.midpoint_step(rows, H, TOL, MAX_ITER)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(ns):
+                rows, k, _ = st.midpoint_step(rows, H, TOL, MAX_ITER)
+            e1.record()
+            torch.cuda.synchronize()
+            rec[name] = {"ms_per_step": e0.elapsed_time(e1) / ns, "steps": ns}
+            del st
         print(json.dumps(rec), flush=True)
-        del rows, w0, be, st
+        del rows, w0, be
         torch.cuda.empty_cache()
     dist.destroy_process_group()
 
