@@ -267,7 +267,7 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
       // (B(j) = (j+1)(N-1-j)), so the loop-carried chain is one FMA per row
       // and the reciprocals are off the chain.  |q| <= d_max^16 < 1e150.
       int k = ib + rs - m;
-      double qm1 = 1.0, q0 = A.d0s[(size_t)(ib / SUB) * n + m];
+      double qm1 = 1.0, q0 = __ldg(A.d0s + (size_t)(ib / SUB) * n + m);
       double dg = block_diag(n, m, k);
       double inc = 2.0 * (double)(n - 2 - 2 * k - m);  // diag(k+1) - diag(k), exact
       const double* sqi = A.sqB + ib + rs;
@@ -282,9 +282,9 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
           const double di = qm1 * rq;  // 1 / d_k
           double L = 0.0;
           if (FAST ? !(lastrow && r == SUB - 1) : (k + rr < len - 1)) {
-            const double e = -sqi[rr] * sqk[rr];
+            const double e = -__ldg(sqi + rr) * __ldg(sqk + rr);
             L = e * di;
-            const double e2 = bqi[rr] * bqk[rr];
+            const double e2 = __ldg(bqi + rr) * __ldg(bqk + rr);
             dg += inc;
             inc -= 4.0;
             const double q1 = fma(dg, q0, -e2 * qm1);
@@ -299,7 +299,7 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   __syncwarp();
   // coupling into my first row: previous chunk (table) or my s-1 neighbour
   double Lin = 0.0;
-  if (has) Lin = (s == 0) ? A.lin[(size_t)c * n + m] : sm[(s * SUB - 1) * DPW + dl].x;
+  if (has) Lin = (s == 0) ? __ldg(A.lin + (size_t)c * n + m) : sm[(s * SUB - 1) * DPW + dl].x;
 
   double2 mu = make_double2(0.0, 0.0), gauge = make_double2(0.0, 0.0);
   if (!FAST && FINAL && m == 0) {
@@ -491,8 +491,8 @@ __device__ __forceinline__ void agg_body(const SolveArgs& A, const double* __res
   for (int r = 0; r < SUB; ++r) v[r] = ld2(wp + r * wstride);
 
   const size_t sub = (size_t)(ib / SUB) * n + m;
-  double qm1 = 1.0, q0 = A.d0s[sub];
-  const double Lin = A.lins[sub];
+  double qm1 = 1.0, q0 = __ldg(A.d0s + sub);
+  const double Lin = __ldg(A.lins + sub);
   double dg = block_diag(n, m, k0);
   double inc = 2.0 * (double)(n - 2 - 2 * k0 - m);
   double bi = (ib + 1.0) * (double)(n - 1 - ib), dbi = (double)(n - 3 - 2 * ib);
