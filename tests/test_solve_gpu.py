@@ -126,3 +126,24 @@ def test_batched_solve_cfg2_shape(zt, n):
     p = zt.solve_stream_batched(dev(np.stack(ws))).cpu().numpy()
     for k in range(3):
         assert relf(p[k], zo.solve_stream(ws[k])) <= 1e-12
+
+
+@pytest.mark.parametrize("n", (2048, 4096))
+def test_cfg2_full_size_batch(zt, n):
+    """BASELINE cfg 2 at full size: 8 successive random_admissible(N, rng(0),
+    1/N) draws.  Matrix 0 against the oracle; every matrix through the
+    size-independent round trip lap(P) = W (test_laplacian.py:116-124) and
+    bit-identical to its own single-matrix solve."""
+    rng = np.random.default_rng(0)
+    ws = np.stack([zo.random_admissible(n, rng, 1.0 / n) for _ in range(8)])
+    wd = dev(ws)
+    op = zt.build_operator(n)
+    p = zt.solve_stream_batched(wd, op)
+    assert relf(p[0].cpu().numpy(), zo.solve_stream(ws[0])) <= 1e-12
+    for k in range(8):
+        back = zt.apply_laplacian(p[k], op=op)
+        assert float((back - wd[k]).norm() / wd[k].norm()) <= 1e-10
+        if k in (0, 7):
+            assert torch.equal(zt.solve_stream(wd[k], op), p[k])
+    del p, wd
+    torch.cuda.empty_cache()
