@@ -162,3 +162,29 @@ def test_long_run_structure_full_size(zt, n):
     assert zt.skewness_residual(x) <= 1e-13
     assert zt.trace_residual(x) <= 1e-13
     assert abs(zt.casimirs(x, 2)[1] - c2_0) <= 1e-12 * abs(c2_0)
+
+
+@pytest.mark.parametrize("n", (2048, 4096))
+def test_cfg3_commutator_and_sandwich_full_size(zt, n):
+    """BASELINE cfg 3 at full size (P then W from random_admissible(N, rng(0),
+    1/N), h = 0.01): C = a - a^H and S = W - (h/2)(a - a^H) - (h^2/4) a P with
+    a = P W (integrator.py:127-129) against numpy/OpenBLAS, relF <= 1e-14;
+    C exactly skew-Hermitian."""
+    from paper_2206_05466_b200 import _lib
+
+    h = 0.01
+    rng = np.random.default_rng(0)
+    pn = zo.random_admissible(n, rng, 1.0 / n)
+    wn = zo.random_admissible(n, rng, 1.0 / n)
+    P, W = dev(pn), dev(wn)
+    C, S, work = torch.empty_like(P), torch.empty_like(P), torch.empty_like(P)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib.zt_commutator(n, P.data_ptr(), W.data_ptr(), C.data_ptr(), work.data_ptr(), s))
+    _lib.check(_lib.lib.zt_sandwich(n, P.data_ptr(), W.data_ptr(), h, S.data_ptr(), work.data_ptr(), s))
+    a = pn @ wn
+    cref = a - a.conj().T
+    c = C.cpu().numpy()
+    assert relf(c, cref) <= 1e-14
+    assert np.array_equal(c, -c.conj().T)
+    sref = wn - 0.5 * h * cref - 0.25 * h * h * (a @ pn)
+    assert relf(S.cpu().numpy(), sref) <= 1e-14
