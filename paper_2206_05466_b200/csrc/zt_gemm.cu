@@ -449,9 +449,10 @@ __device__ __forceinline__ size_t a_plane_index(int r, int k, int kbt) {
 }
 
 __global__ void __launch_bounds__(256) k_sum_planes(int n, const double* __restrict__ p, const double* __restrict__ x,
-                                                    int64_t ld, double* pa, double* pb, double* xb) {
+                                                    int64_t ld, double* pa, double* pb, double* xb, int skip_pb) {
   // blockIdx.y: 0 -> P in A layout, 1 -> P in B layout, 2 -> X in B layout
-  const int which = blockIdx.y;
+  // (skip_pb: GEMM-1 only, grid.y = 2 maps 1 -> X)
+  const int which = (skip_pb && blockIdx.y == 1) ? 2 : blockIdx.y;
   const int kbt = (n + 15) / 16, cbt = (n + 63) / 64;
   const int ntiles = (which == 0) ? cbt * kbt : kbt * cbt;
   const int tile = blockIdx.x;
@@ -1156,7 +1157,7 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
     f.pa2 = aa;
     f.pb2 = pb;
     const int kbt = (n + 15) / 16, cbt = (n + 63) / 64;
-    k_sum_planes<<<dim3(kbt * cbt, 3), 256, 0, st>>>(n, p, x, n, pa, pb, xb);
+    k_sum_planes<<<dim3(kbt * cbt, gemm1_only ? 2 : 3), 256, 0, st>>>(n, p, x, n, pa, pb, xb, gemm1_only);
     ZT_LAUNCHED();
   }
   int dev;
