@@ -28,7 +28,7 @@ def _virtual_ranks(n, world, dev):
     return [PeerRank(n, world, g, be, xf[g], ac[g], xp, ap, br[g], bp) for g in range(world)]
 
 
-@pytest.mark.parametrize("n,world", ((256, 2), (512, 4), (384, 3), (512, 8), (640, 5), (768, 6)))
+@pytest.mark.parametrize("n,world", ((256, 2), (512, 4), (384, 3), (512, 8), (640, 5), (768, 6), (300, 3), (200, 4), (210, 6)))
 def test_virtual_ranks_match_single_gpu(n, world):
     from paper_2206_05466_b200.integrator import midpoint_step_raw
     from paper_2206_05466_b200.laplacian import build_operator
@@ -54,7 +54,8 @@ def test_virtual_ranks_match_single_gpu(n, world):
         assert not torch.isnan(torch.view_as_real(rk.brows)).any()
     work = [sum(nr * nc for _, nr, _, nc, _ in rk.blocks()) for rk in ranks]
     m = n // world
-    assert max(work) == min(work) == m * m * (world + 1) // 2
+    # (G+1)/2 blocks each; odd m splits the G/2 pair into m//2 and m - m//2
+    assert max(work) - min(work) <= m and abs(sum(work) / world - m * m * (world + 1) / 2) <= m
 
 
 def test_virtual_ranks_errors_and_nonconvergence():
