@@ -256,7 +256,15 @@ class PeerRank:
         """b = a_R P on this rank's share of blocks, mirrors to the partners."""
         lib, n = self.be._lib, self.n
         esz = 16
-        for r0, nr, c0, nc, h in self.blocks():
+        blocks = self.blocks()
+        # the blocks are small at large G (m x m x N each, often under one wave
+        # of tiles): run them on side streams so they share the SMs
+        main = torch.cuda.current_stream(self.be.device)
+        streams = self._side_streams(len(blocks))
+        ready = torch.cuda.Event()
+        ready.record(main)
+        done = []
+        for (r0, nr, c0, nc, h), sstream in zip(blocks, streams):
             a_ptr = self.a_rows.data_ptr() + r0 * n * esz
             b_ptr = self.p.data_ptr() + c0 * esz
             c_ptr = self.brows.data_ptr() + (r0 * n + c0) * esz
@@ -264,7 +272,20 @@ class PeerRank:
                 mir = None
             else:  # partner rows (c0 - h m) .., columns r0_g + r0 ..
                 mir = self.bptrs[h] + ((c0 - h * self.m) * n + self.r0 + r0) * esz
-            lib.check(lib.lib.zt_zgemm_rect_mirror(nr, nc, n, a_ptr, n, b_ptr, n, c_ptr, n, mir, n, self._s()))
+            sstream.wait_event(ready)
+            lib.check(lib.lib.zt_zgemm_rect_mirror(nr, nc, n, a_ptr, n, b_ptr, n, c_ptr, n, mir, n,
+                                                   sstream.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(sstream)
+            done.append(ev)
+        for ev in done:
+            main.wait_event(ev)
+
+    def _side_streams(self, k: int):
+        pool = getattr(self, "_pool", None)
+        if pool is None or len(pool) < k:
+            pool = self._pool = [torch.cuda.Stream(device=self.be.device) for _ in range(max(k, 4))]
+        return pool[:k]
 
     def phase2b(self, base_rows, xprev_rows, hh: float, qq: float, with_b: bool = True):
         """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, broadcast to every rank
