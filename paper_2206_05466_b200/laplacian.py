@@ -76,7 +76,16 @@ def _to_device(w):
 
 
 def _out(t: torch.Tensor, as_numpy: bool):
-    return t.cpu().numpy() if as_numpy else t
+    """Device result -> the caller's type.  numpy results land in pinned host
+    memory (torch's caching host allocator recycles the blocks once the caller
+    drops them), so the copy runs at full DMA rate without page faults, and a
+    result fed back as the next input is pinned too (direct DMA on the way in)."""
+    if not as_numpy:
+        return t
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
 
 
 _ws_local = threading.local()
