@@ -20,15 +20,23 @@ from .basis import (
     threej,
     wigner_basis_oracle,
 )
-from .diagnostics import hamiltonian
+from .diagnostics import CASIMIR_BASELINE_FLOOR, DiagnosticsRecord, casimir_drift, hamiltonian
 from .driver import (
+    EXIT_CONFIG,
+    EXIT_IO,
+    EXIT_OK,
+    EXIT_SOLVER,
     Checkpoint,
+    ConfigError,
     DeviceRun,
     FileFormatError,
+    SimConfig,
+    SolverError,
     random_initial_condition,
     read_checkpoint,
     read_grid,
     write_checkpoint,
+    run,
     write_grid,
 )
 from .integrator import (
@@ -68,4 +76,6 @@ __all__ = [
     "DeviceBasis", "HarmonicCoefficients", "QuantizedBasis", "compute_basis", "energy_spectrum", "extract",
     "hamiltonian_from_coeffs", "load_basis", "project", "save_basis", "threej", "wigner_basis_oracle",
     "evaluate_on_grid", "random_initial_condition", "read_grid", "write_grid",
+    "CASIMIR_BASELINE_FLOOR", "DiagnosticsRecord", "casimir_drift", "EXIT_OK", "EXIT_CONFIG", "EXIT_SOLVER",
+    "EXIT_IO", "ConfigError", "SimConfig", "SolverError", "run",
 ]

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import json
 import struct
+import sys
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -43,18 +44,80 @@ from .basis import (
     extract_packed,
     project_packed,
 )
-from .diagnostics import hamiltonian
-from .integrator import StepperState, casimirs, midpoint_step_raw
+from .diagnostics import casimir_drift, hamiltonian
+from .integrator import FixedPointError, StepperState, casimirs, default_time_step, midpoint_step_raw
 from .laplacian import build_operator
 
 CHECKPOINT_MAGIC = b"ZCK1"
 GRID_MAGIC = b"ZGD1"
 FORMAT_VERSION = 1
-CASIMIR_BASELINE_FLOOR = 1e-14  # diagnostics.py:38-40
 
 
 class FileFormatError(ValueError):
     """formats.py:49-50."""
+
+
+EXIT_OK = 0      # driver.py:61-64: run() exit codes
+EXIT_CONFIG = 2
+EXIT_SOLVER = 3
+EXIT_IO = 4
+
+
+class ConfigError(ValueError):
+    """Invalid or inconsistent run configuration (driver.py:67-68)."""
+
+
+class SolverError(RuntimeError):
+    """The inner iteration failed during a run; carries the step index (driver.py:71-72)."""
+
+
+@dataclass
+class SimConfig:
+    """Run parameters (driver.py:75-122); ``h=None`` selects the advective-limit
+    default.  ``threads`` and ``deterministic`` are accepted: device runs are
+    bitwise deterministic at any setting."""
+
+    n: int
+    steps: int
+    h: float | None = None
+    tol: float = 1e-12
+    max_iter: int = 10
+    seed: int = 0
+    l_min: int = 2
+    l_max: int = 20
+    sample_every: int = 5000
+    checkpoint_every: int = 10000
+    output_dir: str = "out"
+    threads: int = 0
+    comm_scale: float = 1.0
+    k_max: int = 5
+    deterministic: bool = False
+    write_grid: bool = True
+    basis_cache: str | None = None
+
+    def validate(self) -> None:
+        checks = (
+            (self.n >= 2, f"n must be at least 2, got {self.n}"),
+            (self.steps >= 0, f"steps must be nonnegative, got {self.steps}"),
+            (self.h is None or self.h > 0.0, f"h must be positive, got {self.h}"),
+            (2 <= self.l_min <= self.l_max <= self.n - 1,
+             f"need 2 <= l_min <= l_max <= n-1, got l_min={self.l_min}, l_max={self.l_max}, n={self.n}"),
+            (self.tol > 0.0, f"tol must be positive, got {self.tol}"),
+            (self.max_iter >= 1, f"max_iter must be at least 1, got {self.max_iter}"),
+            (self.sample_every >= 1 and self.checkpoint_every >= 1,
+             "sample_every and checkpoint_every must be at least 1"),
+            (0 <= self.seed < 2**64, f"seed must fit in 64 bits, got {self.seed}"),
+            (2 <= self.k_max <= self.n, f"k_max={self.k_max} out of range 2..{self.n}"),
+            (self.threads >= 0, f"threads must be nonnegative, got {self.threads}"),
+            (self.comm_scale > 0.0, f"comm_scale must be positive, got {self.comm_scale}"),
+        )
+        for ok, msg in checks:
+            if not ok:
+                raise ConfigError(msg)
+
+
+def _log(msg: str) -> None:
+    print(f"[zeitlin] {msg}", file=sys.stderr, flush=True)
 
 
 def format_float(x: float) -> str:
@@ -138,12 +201,10 @@ def read_grid(path) -> tuple[np.ndarray, float]:
     return np.frombuffer(raw, dtype="<f8").reshape(n_lat, n_lon).copy(), time
 
 
-def casimir_drift(c0: np.ndarray, ck: np.ndarray) -> np.ndarray:
+def _drift_row(c0: np.ndarray, ck: np.ndarray) -> np.ndarray:
     """diagnostics.py:86-110 for one sample: |C_k - C_k(0)| / |C_k(0)|, k >= 2,
     absolute error where the baseline is below 1e-14."""
-    base = np.asarray(c0, dtype=np.float64)[1:]
-    denom = np.where(np.abs(base) < CASIMIR_BASELINE_FLOOR, 1.0, np.abs(base))
-    return np.abs(np.asarray(ck, dtype=np.float64)[1:] - base) / denom
+    return casimir_drift([(0.0, c0), (0.0, ck)])[1].casimir_rel_err
 
 
 def random_initial_condition(cfg, basis, rng: np.random.Generator | None = None) -> torch.Tensor:
@@ -162,7 +223,7 @@ def random_initial_condition(cfg, basis, rng: np.random.Generator | None = None)
 
     n, l_min, l_max = cfg.n, cfg.l_min, cfg.l_max
     if l_max >= n:
-        raise ValueError(f"l_max={l_max} must be below n={n}")
+        raise ConfigError(f"l_max={l_max} must be below n={n}")
     if rng is None:
         rng = np.random.default_rng(cfg.seed)
     coeffs = HarmonicCoefficients.zeros(n)
@@ -214,6 +275,7 @@ class DeviceRun:
             raise ValueError(f"basis is for N={basis.n}, state has N={self.n}")
         self.basis = basis
         self.write_grid = write_grid and basis is not None
+        self.log = False
 
     # -- files ---------------------------------------------------------------
     def start(self) -> None:
@@ -233,17 +295,17 @@ class DeviceRun:
         out = Path(output_dir)
         meta_path, diag_path = out / "run_meta.json", out / "diagnostics.csv"
         if not meta_path.exists():
-            raise ValueError(f"resume requires {meta_path} from the original run directory")
+            raise ConfigError(f"resume requires {meta_path} from the original run directory")
         if not diag_path.exists():
             raise FileFormatError(f"{diag_path}: missing diagnostics file for resume")
         meta = json.loads(meta_path.read_text())
-        cp = read_checkpoint(checkpoint_path)
+        cp = checkpoint_path if isinstance(checkpoint_path, Checkpoint) else read_checkpoint(checkpoint_path)
         if meta.get("n") != cp.n or meta.get("seed") != cp.seed:
-            raise ValueError(f"{meta_path} does not match checkpoint (N={cp.n}, seed={cp.seed})")
+            raise ConfigError(f"{meta_path} does not match checkpoint (N={cp.n}, seed={cp.seed})")
         h = float.fromhex(meta["h"])
         baseline = np.array([float.fromhex(s) for s in meta["casimir_baseline"]])
         if baseline.size != k_max:
-            raise ValueError(f"{meta_path} stores k_max={baseline.size}, asked for {k_max}")
+            raise ConfigError(f"{meta_path} stores k_max={baseline.size}, asked for {k_max}")
         st = StepperState(w=cp.w, h=h, time=cp.time, step_index=cp.step_index, tol=tol,
                           max_iter=max_iter, comm_scale=comm_scale)
         run = cls(st, out, k_max=k_max, sample_every=sample_every, checkpoint_every=checkpoint_every,
@@ -272,7 +334,7 @@ class DeviceRun:
                 field = evaluate_on_grid_packed(self.n, pos, 2 * lr, 4 * lr, l_max=lr).cpu().numpy()
                 write_grid(self.out / f"grid_{self.state.step_index:08d}.bin", field, self.state.time)
         row = [format_float(self.state.time), format_float(h_val), format_float(k_val)]
-        row += [format_float(v) for v in casimir_drift(self.baseline, ck)]
+        row += [format_float(v) for v in _drift_row(self.baseline, ck)]
         with open(self.diag_path, "a", encoding="utf-8") as fh:
             fh.write(",".join(row) + "\n")
         return h_val
@@ -289,14 +351,91 @@ class DeviceRun:
         st = self.state
         h_eff = st.h * st.comm_scale
         while st.step_index < steps:
-            nxt, k, _, _ = midpoint_step_raw(self.w, h_eff, st.tol, st.max_iter, self.op, out=self.spare)
+            try:
+                nxt, k, _, _ = midpoint_step_raw(self.w, h_eff, st.tol, st.max_iter, self.op, out=self.spare)
+            except FixedPointError as exc:  # driver.py:394-399
+                raise SolverError(f"step {st.step_index + 1}: {exc} (residual {exc.residual:.3e})") from exc
             self.w, self.spare = nxt, self.w
             st.time = st.time + st.h
             st.step_index += 1
             self.iterations.append(k)
             final = st.step_index == steps
             if st.step_index % self.sample_every == 0 or final:
-                self.sample()
+                h_val = self.sample()
+                if self.log:
+                    _log(f"step {st.step_index}/{steps} t={st.time:.6g} H={h_val:.9e} iters={k}")
             if st.step_index % self.checkpoint_every == 0 or final:
                 self.checkpoint()
         st.w = self.w
+
+
+def run(cfg: SimConfig, resume: str | None = None) -> int:
+    """driver.py:259-281: execute a run; returns a process exit code (0 ok,
+    2 configuration, 3 solver, 4 I/O).  The loop is `DeviceRun` (W stays in
+    HBM; samples and checkpoints computed on the device)."""
+    try:
+        cfg.validate()
+    except ConfigError as exc:
+        _log(f"configuration error: {exc}")
+        return EXIT_CONFIG
+    try:
+        _run_inner(cfg, resume)
+    except ConfigError as exc:
+        _log(f"configuration error: {exc}")
+        return EXIT_CONFIG
+    except (SolverError, FixedPointError) as exc:
+        _log(f"solver failure: {exc}")
+        return EXIT_SOLVER
+    except (OSError, FileFormatError) as exc:
+        _log(f"I/O failure: {exc}")
+        return EXIT_IO
+    return EXIT_OK
+
+
+def _run_inner(cfg: SimConfig, resume: str | None) -> None:
+    """driver.py:284-410 on the device."""
+    from .basis import compute_basis, load_basis
+
+    out = Path(cfg.output_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    meta_path = out / "run_meta.json"
+    lap = build_operator(cfg.n)
+    if cfg.basis_cache:
+        basis = load_basis(cfg.basis_cache)
+        if basis.n != cfg.n:
+            raise ConfigError(f"basis cache is for N={basis.n}, configuration asks for N={cfg.n}")
+    else:
+        basis = compute_basis(cfg.n)
+    common = dict(k_max=cfg.k_max, sample_every=cfg.sample_every, checkpoint_every=cfg.checkpoint_every,
+                  basis=basis, write_grid=cfg.write_grid)
+    if resume is not None:
+        cp = read_checkpoint(resume)
+        if cp.n != cfg.n:
+            raise ConfigError(f"checkpoint is for N={cp.n}, configuration asks for N={cfg.n}")
+        if cp.seed != cfg.seed:
+            raise ConfigError(f"checkpoint seed {cp.seed} differs from configured {cfg.seed}")
+        if not meta_path.exists():
+            raise ConfigError(f"resume requires {meta_path} from the original run directory")
+        meta = json.loads(meta_path.read_text())
+        if meta.get("n") != cfg.n or meta.get("seed") != cfg.seed:
+            raise ConfigError(f"{meta_path} does not match this configuration")
+        h = float.fromhex(meta["h"])
+        if cfg.h is not None and cfg.h != h:
+            raise ConfigError(f"configured h={cfg.h} differs from the original run's h={h}; "
+                              "a resumed run must keep its time-step")
+        if len(meta["casimir_baseline"]) != cfg.k_max:
+            raise ConfigError(f"{meta_path} stores k_max={len(meta['casimir_baseline'])}, configured {cfg.k_max}")
+        dr = DeviceRun.resume(cp, out, tol=cfg.tol, max_iter=cfg.max_iter, comm_scale=cfg.comm_scale,
+                              **common)
+        _log(f"resumed from {resume} at step {cp.step_index} (t={cp.time:g})")
+    else:
+        rng = np.random.default_rng(cfg.seed)
+        w0 = random_initial_condition(cfg, basis, rng)
+        h = cfg.h if cfg.h is not None else default_time_step(w0, lap)
+        st = StepperState(w=w0, h=h, tol=cfg.tol, max_iter=cfg.max_iter, comm_scale=cfg.comm_scale)
+        blob = json.dumps(rng.bit_generator.state).encode("utf-8")
+        dr = DeviceRun(st, out, seed=cfg.seed, rng_state=blob, **common)
+        _log(f"N={cfg.n} steps={cfg.steps} h={h:g} seed={cfg.seed}")
+        dr.start()
+    dr.log = True
+    dr.advance(cfg.steps)

@@ -34,6 +34,10 @@ Contents (all complex128 C-order unless noted):
                     normalized states (N=32, N=16, N=8, N=128), the rigid-rotation
                     state (N=16) and the basis matrix T_{5,3} used to extract the
                     advected coefficient, plus the reference's own results
+  runs.npz          driver.run(SimConfig(...)) output directories for the
+                    test_driver.py configurations RUNS (text of diagnostics.csv,
+                    run_meta.json and the final spectrum csv as uint8 arrays,
+                    the final checkpoint's W and the final grid field)
 """
 
 from __future__ import annotations
@@ -254,7 +258,38 @@ def checkpoint():
     np.save(os.path.join(OUT, "ck_n8_w.npy"), w)
 
 
+#: (name, SimConfig kwargs): test_driver.py:176-248 configurations
+RUNS = (
+    ("resume", dict(n=12, steps=40, h=1e-3, l_min=2, l_max=6, sample_every=10, checkpoint_every=20, seed=7)),
+    ("auto_h", dict(n=8, steps=2, l_max=5, seed=1)),
+    ("cadence", dict(n=8, steps=25, h=1e-3, l_max=5, sample_every=10, checkpoint_every=20, seed=1)),
+    ("grid", dict(n=10, steps=5, h=1e-3, l_max=6, sample_every=5, seed=4)),
+)
+
+
+def runs():
+    """The reference's run loop end to end (driver.py:259-410)."""
+    import tempfile
+    from pathlib import Path
+
+    from zeitlin.driver import SimConfig, run
+    from zeitlin.formats import read_checkpoint, read_grid
+
+    d = {}
+    for name, kw in RUNS:
+        with tempfile.TemporaryDirectory() as tmp:
+            assert run(SimConfig(output_dir=tmp, **kw)) == 0
+            out, last = Path(tmp), kw["steps"]
+            for key, fname in (("diag", "diagnostics.csv"), ("meta", "run_meta.json"),
+                               ("spec", f"spectrum_{last:08d}.csv")):
+                d[f"{name}_{key}"] = np.frombuffer((out / fname).read_bytes(), dtype=np.uint8)
+            d[f"{name}_w"] = read_checkpoint(out / f"checkpoint_{last:08d}.zck").w
+            d[f"{name}_grid"], _ = read_grid(out / f"grid_{last:08d}.bin")
+    np.savez_compressed(os.path.join(OUT, "runs.npz"), **d)
+
+
 if __name__ == "__main__":
+    runs()
     grids()
     initial_conditions()
     basis()

@@ -76,3 +76,42 @@ def test_grid_snapshot_matches_reference_format(tmp_path):
         p.write_bytes(bad)
         with pytest.raises(FileFormatError):
             read_grid(p)
+
+
+@pytest.mark.parametrize("kwargs", [
+    dict(n=1, steps=1), dict(n=8, steps=-1), dict(n=8, steps=1, h=0.0), dict(n=8, steps=1, l_min=1),
+    dict(n=8, steps=1, l_max=8), dict(n=8, steps=1, l_min=6, l_max=5), dict(n=8, steps=1, tol=0.0),
+    dict(n=8, steps=1, max_iter=0), dict(n=8, steps=1, sample_every=0), dict(n=8, steps=1, k_max=1),
+    dict(n=8, steps=1, seed=-1), dict(n=8, steps=1, comm_scale=0.0), dict(n=8, steps=1, threads=-1),
+])
+def test_simconfig_validate_rejects(kwargs):
+    """test_driver.py:91-109 (driver.py:97-122)."""
+    from paper_2206_05466_b200.driver import ConfigError, SimConfig
+
+    with pytest.raises(ConfigError):
+        SimConfig(**{"l_max": 5, **kwargs}).validate()
+    SimConfig(n=8, steps=1, l_max=5).validate()
+
+
+def test_invalid_config_exits_2(tmp_path):
+    """test_driver.py:111-113: validation precedes any device work."""
+    from paper_2206_05466_b200.driver import EXIT_CONFIG, SimConfig, run
+
+    assert run(SimConfig(n=8, steps=1, l_max=20, output_dir=str(tmp_path))) == EXIT_CONFIG
+    assert not any(tmp_path.iterdir())
+
+
+def test_casimir_drift_records():
+    """diagnostics.py:86-110: relative drift against the first entry, absolute
+    below the 1e-14 baseline floor (flagged)."""
+    from paper_2206_05466_b200 import DiagnosticsRecord, casimir_drift
+
+    assert casimir_drift([]) == []
+    c0 = np.array([0.0, -2.0, 1e-16, 4.0])
+    recs = casimir_drift([(0.0, c0), (0.5, np.array([0.0, -2.0 + 2e-12, 3e-16, 4.0]))])
+    assert all(isinstance(r, DiagnosticsRecord) for r in recs)
+    assert recs[1].time == 0.5 and recs[1].casimir_abs_fallback == (3,)
+    np.testing.assert_allclose(recs[1].casimir_rel_err, [1e-12, 2e-16, 0.0], rtol=1e-3, atol=1e-30)
+    np.testing.assert_array_equal(recs[0].casimir_rel_err, [0.0, 0.0, 0.0])
+    with pytest.raises(ValueError):
+        casimir_drift([(0.0, np.array([1.0]))])
