@@ -41,6 +41,33 @@ constexpr int LPD = 64 / SUB;   // lanes per diagonal
 constexpr int DPW = 32 / LPD;  // diagonals per warp tile
 constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
+
+// L2 residency between the passes: pass 1 reads W with evict_last so pass 3's
+// re-read hits L2 when the batch runs one matrix (or diagonal group) at a time;
+// pass 3 reads W for the last time (evict_first) and streams P out.
+#ifndef SOLVE_L2HINT
+#define SOLVE_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld2_pol(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st2_pol(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
 constexpr int TR = 32;  // rows per apply tile / diagonals per apply tile
 constexpr int M0X = 5;  // m = 0 per-chunk responses: Y1, X1, S1, SH, SK
 
@@ -250,7 +277,15 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
   // 1. loads (16 rows; each instruction covers 4 rows x 128 B)
   double2 v[SUB];
 #pragma unroll
+#if SOLVE_L2HINT
+  const uint64_t wpol = FINAL ? pol_first() : pol_last();
+  const uint64_t ppol = pol_first();
+  for (int r = 0; r < SUB; ++r) v[r] = (has && ROW_OK(r)) ? ld2_pol(wp + r * wstride, wpol) : make_double2(0.0, 0.0);
+#define PST(ptr, val) st2_pol(ptr, val, ppol)
+#else
   for (int r = 0; r < SUB; ++r) v[r] = (has && ROW_OK(r)) ? ld2(wp + r * wstride) : make_double2(0.0, 0.0);
+#define PST(ptr, val) st2(ptr, val)
+#endif
   const double2 ych = (FINAL && mok) ? __ldcg(A.yend + cm) : make_double2(0.0, 0.0);
   const double2 xch = (FINAL && mok) ? __ldcg(A.xst + cm) : make_double2(0.0, 0.0);
 
@@ -432,10 +467,10 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
         const double2 x = make_double2(fma(hh, xin.x, v[r].x), fma(hh, xin.y, v[r].y));
         if (!FAST && m == 0) {
           // zero-mean gauge (laplacian.py:293-298): P[i][i] = -(x - g)
-          st2(pp + r * pstride, make_double2(-(x.x - gauge.x), -(x.y - gauge.y)));
+          PST(pp + r * pstride, make_double2(-(x.x - gauge.x), -(x.y - gauge.y)));
         } else {
           // lower triangle: P[i][i-m] = -x (laplacian.py:299-300)
-          st2(pp + r * pstride, make_double2(-x.x, -x.y));
+          PST(pp + r * pstride, make_double2(-x.x, -x.y));
         }
         v[r] = x;
       }
@@ -460,9 +495,10 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
     const int i = i0 + r;
     if (uok && tt < SR && r >= 0 && r < SR && i >= mm && i < n) {
       const double2 xv = xs_buf[r * DPW + u];
-      st2(p + ((size_t)(i - mm) * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
+      PST(p + ((size_t)(i - mm) * A.ldp + i) * 2, make_double2(xv.x, -xv.y));
     }
   }
+#undef PST
 }
 
 
@@ -488,7 +524,12 @@ __device__ __forceinline__ void agg_body(const SolveArgs& A, const double* __res
 
   double2 v[SUB];
 #pragma unroll
+#if SOLVE_L2HINT
+  const uint64_t wpol = pol_last();
+  for (int r = 0; r < SUB; ++r) v[r] = ld2_pol(wp + r * wstride, wpol);
+#else
   for (int r = 0; r < SUB; ++r) v[r] = ld2(wp + r * wstride);
+#endif
 
   const size_t sub = (size_t)(ib / SUB) * n + m;
   double qm1 = 1.0, q0 = __ldg(A.d0s + sub);
