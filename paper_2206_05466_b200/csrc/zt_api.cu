@@ -66,7 +66,7 @@ int skew_diff(int n, const double* a, double* c, cudaStream_t st);
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
-                  cudaStream_t st, int gemm1_only = 0);
+                  cudaStream_t st, int gemm1_only = 0, double* bbuf = nullptr);
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
@@ -102,6 +102,7 @@ static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
 static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
 static bool g_planes = true; // fused 3M reads precomputed sum planes (ZT_SUM_PLANES=0 disables)
 static bool g_split = true;  // split-K tail in the fused update (ZT_SPLIT=0 disables)
+static bool g_sep_update = true;  // update as a streaming pass after the GEMMs (ZT_SEP_UPDATE=0: fused epilogue)
 
 // ---- step workspace layout -------------------------------------------------
 struct StepWS {
@@ -115,6 +116,7 @@ struct StepWS {
   unsigned int* sync;  // fused update: tile counter + per-panel completion counts
   double* planes;      // 3M sum planes (P A/B layout, X B layout, a A layout)
   double* split;       // split-K tail partial accumulators
+  double* b;           // n x n complex: b = a P (lower / diagonal tiles) for the update pass
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -138,8 +140,9 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
     w->sync = reinterpret_cast<unsigned int*>(base + off + 2 * mat + sb + rb + 256);
     w->planes = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb);
     w->split = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl);
+    w->b = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl + spl);
   }
-  return 2 * mat + sb + rb + 256 + yb + pl + spl;
+  return 2 * mat + sb + rb + 256 + yb + pl + spl + mat;
 }
 
 // small pinned host mailbox for the per-iteration read-back
@@ -220,7 +223,8 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   if (g_fused) {
     // GEMM-1 and GEMM-2 in one persistent launch (profiled as "gemm1")
     rc = zupdate_fused(n, w.p, x, w.a, base, xprev, wn, out, hh, qq, resid, cons, w.sync,
-                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, g_split ? w.split : nullptr, st);
+                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, g_split ? w.split : nullptr, st, 0,
+                       g_sep_update ? w.b : nullptr);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;
@@ -521,6 +525,7 @@ int zt_op_create(int n, int device, zt_op_t* op) {
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
   if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
   if (const char* e = getenv("ZT_SPLIT")) g_split = std::string(e) != "0";
+  if (const char* e = getenv("ZT_SEP_UPDATE")) g_sep_update = std::string(e) != "0";
   if (const char* e = getenv("ZT_FINAL_SANDWICH")) g_final_comm = std::string(e) == "0";
   return op_create(n, device, op);
 }

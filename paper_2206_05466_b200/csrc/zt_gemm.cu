@@ -509,6 +509,9 @@ struct FusedArgs {
   // (per-tile counter `split_sem`) sums them and runs the update epilogue
   int split_s, split_f;
   unsigned int* split_sem;  // [split_s] (zeroed per launch)
+  // b_out != nullptr: GEMM-2 tiles store b = a P (lower and diagonal tiles)
+  // there and the update runs as a separate streaming pass (k_update_pairs)
+  double* b_out;
   double* split_acc;        // [split_s * split_f][NACC*4*WNB*2][consumer threads]
   int gemm1_only;           // final update: only a = P X (no GEMM-2, no a plane)
 };
@@ -606,7 +609,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
         plb = f.pb2;
         // a's row panels I and J must be complete (stored by other CTAs)
         while (ld_acquire(f.done + I) < (unsigned)T) __nanosleep(64);
-        while (ld_acquire(f.done + J) < (unsigned)T) __nanosleep(64);
+        if (!f.b_out)
+          while (ld_acquire(f.done + J) < (unsigned)T) __nanosleep(64);
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       const int kbt = KT;  // k blocks of 16
@@ -710,6 +714,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
 #pragma unroll
           for (int q = 0; q < NV; ++q) aw[q] += __ldcg(other + (size_t)q * (CONSUMER_WARPS * 32) + tid);
         }
+      }
+      if (f.b_out) {
+        GemmArgs gb = g1;
+        gb.c = f.b_out;
+        epilogue_tile<ALGO, EPI_STORE>(gb, acc, I, J, wm, wn, lane, rmax, cmax);
+        continue;
       }
       if (lane == 0) {
         // order this warp's epilogue reads of a after the producer's acquire
@@ -1116,10 +1126,137 @@ int final_commutator(int n, const double* a, const double* wn, double h, double*
   return ZT_OK;
 }
 
+// The update as a streaming pass over 32 x 32 tile pairs (R, C), R >= C:
+// new = base + hh (a - a^H) + qq b with b read where GEMM-2 computed it (the
+// lower and diagonal 128-tiles of `bm`) and mirrored (b_ji = -conj(b_ij))
+// elsewhere -- the same operands and operation order as the fused epilogue
+// (epilogue_tile<EPI_UPDATE>), so the result is bitwise identical; plus the
+// NaN-propagating residual / consistency maxima.  `out` may alias `xprev`
+// (in-place iteration): every element is read and written by one thread.
+template <bool XP, bool WN>
+__global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __restrict__ a,
+                                                      const double* __restrict__ bm, double* out,
+                                                      const double* __restrict__ base, const double* xprev,
+                                                      const double* __restrict__ wn, double hh, double qq,
+                                                      unsigned long long* resid, unsigned long long* cons) {
+  // tb[c][r]: a_ji of tile element (r, c) for phase 1, then (the same slot,
+  // read once) b_ij for the mirror in phase 2
+  __shared__ double2 tb[32][33];
+  __shared__ double2 dd[32][33];  // (a - a^H)_ij of tile (R, C)
+  __shared__ unsigned long long red[2][8];
+  int I = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= (int)blockIdx.x) ++I;
+  while (I * (I + 1) / 2 > (int)blockIdx.x) --I;
+  const int J = blockIdx.x - I * (I + 1) / 2;
+  const int R = I * 32, C = J * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const bool same128 = (R / BM) == (C / BM);  // b computed on both sides
+  double rmax = 0.0, cmax = 0.0;
+  // all loads of both phases first (the in-place `out` == `xprev` stores
+  // would otherwise pin every load behind the previous row's store)
+  const bool two = I != J;
+  double2 aij[4], bij[4], b0[4], xp[4], w0[4], b0m[4], xpm[4], bm2[4], w0m[4];  // unused ones fold away
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q;
+    {
+      const int i = C + r, j = R + tx;
+      tb[r][tx] = (i < n && j < n) ? ld2(a + ((size_t)i * n + j) * 2) : make_double2(0, 0);
+    }
+    const int i = R + r, j = C + tx;
+    const bool ok = i < n && j < n;
+    const size_t o = ((size_t)i * n + j) * 2;
+    const double2 z = make_double2(0, 0);
+    aij[q] = ok ? ld2(a + o) : z;
+    bij[q] = ok ? ld2(bm + o) : z;
+    b0[q] = ok ? ld2(base + o) : z;
+    xp[q] = (XP && ok) ? ld2_plain(xprev + o) : z;
+    w0[q] = (WN && ok) ? ld2(wn + o) : z;
+    // mirror side: (C + r, R + tx)
+    const int im = C + r, jm = R + tx;
+    const bool okm = two && im < n && jm < n;
+    const size_t om = ((size_t)im * n + jm) * 2;
+    b0m[q] = okm ? ld2(base + om) : z;
+    xpm[q] = (XP && okm) ? ld2_plain(xprev + om) : z;
+    w0m[q] = (WN && okm) ? ld2(wn + om) : z;
+    bm2[q] = (okm && same128) ? ld2(bm + om) : z;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q;
+    const int i = R + r, j = C + tx;
+    const double2 aji = tb[tx][r];
+    const double2 dij = make_double2(__dsub_rn(aij[q].x, aji.x), __dadd_rn(aij[q].y, aji.y));
+    const double2 nw = cadd(cadd(b0[q], rmul(hh, dij)), rmul(qq, bij[q]));
+    dd[r][tx] = dij;
+    if (i < n && j < n) {
+      if (XP) rmax = nanmax(rmax, hypot(nw.x - xp[q].x, nw.y - xp[q].y));
+      if (WN) {
+        const double2 rc = cadd(csub(b0[q], rmul(hh, dij)), rmul(qq, bij[q]));
+        cmax = nanmax(cmax, hypot(rc.x - w0[q].x, rc.y - w0[q].y));
+      }
+      st2(out + ((size_t)i * n + j) * 2, nw);
+    }
+  }
+  if (two) {
+    __syncthreads();  // every a_ji of tb is read; reuse it for b_ij
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tb[tx][ty + 8 * q] = bij[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty + 8 * q;
+      const int i = C + r, j = R + tx;  // (i, j) = mirror of tile element (tx, r)
+      if (i < n && j < n) {
+        const double2 d = dd[tx][r];
+        const double2 dji = make_double2(-d.x, d.y);
+        double2 bji;
+        if (same128) {
+          bji = bm2[q];
+        } else {
+          const double2 t = tb[r][tx];
+          bji = make_double2(-t.x, t.y);
+        }
+        const double2 nw = cadd(cadd(b0m[q], rmul(hh, dji)), rmul(qq, bji));
+        if (XP) rmax = nanmax(rmax, hypot(nw.x - xpm[q].x, nw.y - xpm[q].y));
+        if (WN) {
+          const double2 rc = cadd(csub(b0m[q], rmul(hh, dji)), rmul(qq, bji));
+          cmax = nanmax(cmax, hypot(rc.x - w0m[q].x, rc.y - w0m[q].y));
+        }
+        st2(out + ((size_t)i * n + j) * 2, nw);
+      }
+    }
+  }
+  unsigned long long rb = (unsigned long long)__double_as_longlong(fabs(rmax));
+  unsigned long long cb = (unsigned long long)__double_as_longlong(fabs(cmax));
+  if (rmax != rmax) rb = 0x7ff8000000000000ull;
+  if (cmax != cmax) cb = 0x7ff8000000000000ull;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    rb = max(rb, __shfl_xor_sync(0xffffffff, rb, off));
+    cb = max(cb, __shfl_xor_sync(0xffffffff, cb, off));
+  }
+  if (tx == 0) {
+    red[0][ty] = rb;
+    red[1][ty] = cb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = 0, c = 0;
+    for (int q = 0; q < 8; ++q) {
+      r = max(r, red[0][q]);
+      c = max(c, red[1][q]);
+    }
+    if (resid && xprev) atomicMax(resid, r);
+    if (cons && wn) atomicMax(cons, c);
+  }
+}
+
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
-                  cudaStream_t st, int gemm1_only) {
+                  cudaStream_t st, int gemm1_only, double* bbuf) {
   FusedArgs f;
   memset(&f, 0, sizeof f);
   GemmArgs& g = f.g2;
@@ -1178,6 +1315,10 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
   const int grid = std::min(total, dev < 16 ? g_sms[dev] : 148);
   int S = 0, F = 1;
   f.gemm1_only = gemm1_only;
+  // bbuf: GEMM-2 stores b there and the update runs as k_update_pairs after
+  // the persistent kernel (X is then rewritten only once no tile reads it)
+  const bool sep = bbuf && !gemm1_only;
+  f.b_out = sep ? bbuf : nullptr;
   if (split && !gemm1_only) pick_split(total, grid, T * (T + 1) / 2, n, S, F);
   f.split_s = S;
   f.split_f = F;
@@ -1192,6 +1333,20 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
     k_zupdate<ALGO_3M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
+  if (sep) {
+    const int t32 = (n + 31) / 32;
+    const int nb = t32 * (t32 + 1) / 2;
+    if (xprev && wn)
+      k_update_pairs<true, true><<<nb, 256, 0, st>>>(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons);
+    else if (xprev)
+      k_update_pairs<true, false><<<nb, 256, 0, st>>>(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons);
+    else if (wn)
+      k_update_pairs<false, true><<<nb, 256, 0, st>>>(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons);
+    else
+      k_update_pairs<false, false><<<nb, 256, 0, st>>>(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons);
+    ZT_LAUNCHED();
+    ZT_CUDA_CHECK(cudaGetLastError());
+  }
   return ZT_OK;
 }
 
