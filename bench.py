@@ -439,7 +439,8 @@ def run_ours(args):
     achieved = alg / (g1_ms * 1e-3) / 1e12
     roofline = {
         "bound": "tensor",
-        "kernel": "k_zupdate<3M, sum planes>: GEMM-1 a = P X + GEMM-2 b = a P (lower tiles) + fused update" if fused
+        "kernel": "full update: k_zupdate<3M, sum planes> (GEMM-1 a = P X + GEMM-2 b = a P on lower tiles) "
+                  "with its sum-plane pre-pass and k_update_pairs update pass (events around all three)" if fused
         else "k_zgemm<3M,STORE> (GEMM-1 a = P X)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": TRAFFIC_FUSED if fused else None,
@@ -503,7 +504,9 @@ def run_ours(args):
 
 # dram__bytes_read.sum + dram__bytes_write.sum per fused-update launch at
 # N=2048 from the committed `ncu --set full` capture (profiles/r01_ncu_summary.md)
-TRAFFIC_FUSED = 1289.324e6 + 164.925e6  # ncu --set full, one k_zupdate launch (profiles/r01_ncu_summary.md)
+# ncu --set full dram bytes (profiles/r01_ncu_summary.md): k_zupdate 1076.1 + 134.0 MB,
+# k_update_pairs 236.0 + 41.9 MB, k_sum_planes 167.7 + 58.4 MB per full update
+TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
 def main():
