@@ -1128,7 +1128,7 @@ int final_commutator(int n, const double* a, const double* wn, double h, double*
 
 // The update as a streaming pass over 32 x 32 tile pairs (R, C), R >= C:
 // new = base + hh (a - a^H) + qq b with b read where GEMM-2 computed it (the
-// lower and diagonal 128-tiles of `bm`) and mirrored (b_ji = -conj(b_ij))
+// lower and diagonal BM x BN GEMM tiles of `bm`) and mirrored (b_ji = -conj(b_ij))
 // elsewhere -- the same operands and operation order as the fused epilogue
 // (epilogue_tile<EPI_UPDATE>), so the result is bitwise identical; plus the
 // NaN-propagating residual / consistency maxima.  `out` may alias `xprev`
@@ -1150,7 +1150,7 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
   const int J = blockIdx.x - I * (I + 1) / 2;
   const int R = I * 32, C = J * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const bool same128 = (R / BM) == (C / BM);  // b computed on both sides
+  const bool same_tile = (R / BM) == (C / BM);  // b computed on both sides
   double rmax = 0.0, cmax = 0.0;
   // all loads of both phases first (the in-place `out` == `xprev` stores
   // would otherwise pin every load behind the previous row's store)
@@ -1179,7 +1179,7 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
     b0m[q] = okm ? ld2(base + om) : z;
     xpm[q] = (XP && okm) ? ld2_plain(xprev + om) : z;
     w0m[q] = (WN && okm) ? ld2(wn + om) : z;
-    bm2[q] = (okm && same128) ? ld2(bm + om) : z;
+    bm2[q] = (okm && same_tile) ? ld2(bm + om) : z;
   }
   __syncthreads();
 #pragma unroll
@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
         const double2 d = dd[tx][r];
         const double2 dji = make_double2(-d.x, d.y);
         double2 bji;
-        if (same128) {
+        if (same_tile) {
           bji = bm2[q];
         } else {
           const double2 t = tb[r][tx];
