@@ -131,6 +131,17 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
                      int max_iter, void* workspace, size_t workspace_bytes, int* iterations,
                      double* residual, double* consistency, void* stream);
 
+/* zt_midpoint_step that also delivers W_{n+1} to host memory `host_out`
+ * (n*n complex128, page-locked for overlap), as the reference's
+ * midpoint_step_info returns a fresh numpy array (integrator.py:165-171).
+ * With the step graph, the final update's GEMM writes W_{n+1} tile pair by
+ * tile pair and publishes each 64-row block; a copy stream waits on those
+ * flags (cuStreamWaitValue32) and moves the blocks while the GEMM runs.
+ * Returns after the copy completed; w_next holds W_{n+1} as well. */
+int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* host_out, double h_eff,
+                          double tol, int max_iter, void* workspace, size_t workspace_bytes,
+                          int* iterations, double* residual, void* stream);
+
 /* Config-3 ops (integrator.py:127-129): commutator C = P W - W P = a - a^H
  * with a = P W; sandwich S = W - (h/2)(a - a^H) - (h^2/4) a P
  * = (I - hP/2) W (I + hP/2).  `work` holds n*n complex (a). */

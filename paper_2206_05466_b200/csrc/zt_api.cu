@@ -66,7 +66,8 @@ int skew_diff(int n, const double* a, double* c, cudaStream_t st);
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
-                  cudaStream_t st, int gemm1_only = 0, double* bbuf = nullptr);
+                  cudaStream_t st, int gemm1_only = 0, double* bbuf = nullptr, const ProgParams* prog = nullptr);
+size_t zupdate_prog_words(int n);
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
@@ -116,7 +117,9 @@ struct StepWS {
   unsigned int* sync;  // fused update: tile counter + per-panel completion counts
   double* planes;      // 3M sum planes (P A/B layout, X B layout, a A layout)
   double* split;       // split-K tail partial accumulators
-  double* b;           // n x n complex: b = a P (lower / diagonal tiles) for the update pass
+  double* b;           // n x n complex: b = a P (lower / diagonal tiles) for the update pass;
+                       // W_{n+1} staging of the progressive final update
+  unsigned int* prog;  // zupdate_prog_words(n): progressive final update counters / flags / epoch
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -141,8 +144,9 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
     w->planes = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb);
     w->split = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl);
     w->b = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl + spl);
+    w->prog = reinterpret_cast<unsigned int*>(base + off + 3 * mat + sb + rb + 256 + yb + pl + spl);
   }
-  return 2 * mat + sb + rb + 256 + yb + pl + spl + mat;
+  return 3 * mat + sb + rb + 256 + yb + pl + spl + align_up(sizeof(unsigned int) * zupdate_prog_words(n));
 }
 
 // small pinned host mailbox for the per-iteration read-back
@@ -241,21 +245,30 @@ static int update(zt_operator* op, const double* x, const double* base, const do
 // a = P W~, W_{n+1} = W_n + h (a - a^H), in place over W~.  ZT_FINAL_SANDWICH=1
 // (or a consistency request) keeps the reference's sandwich form.
 static bool g_final_comm = true;
-static int final_update(zt_operator* op, double* x, const double* wn, double h, StepWS& w, cudaStream_t st) {
+// prog: the GEMM-1 kernel itself writes W_{n+1} into w.b pair by pair and
+// publishes each 64-row block (FusedArgs::prog) for an overlapped D2H copy;
+// x receives it by one device copy at the end.
+static int final_update(zt_operator* op, double* x, const double* wn, double h, StepWS& w, cudaStream_t st,
+                        bool prog = false) {
   const int n = op->n;
   prof_mark(0, st, 1);
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
+  prog = prog && g_fused;
   if (g_fused) {
+    ProgParams pp{wn, w.b, h, w.prog};
     rc = zupdate_fused(n, w.p, x, w.a, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, nullptr, w.sync,
-                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, nullptr, st, 1);
+                       g_algo == 0 && g_planes ? 3 : g_algo, w.planes, nullptr, st, 1, nullptr, prog ? &pp : nullptr);
   } else {
     rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
   }
   if (rc) return rc;
   prof_mark(2, st);
-  rc = final_commutator(n, w.a, wn, h, x, st);
+  if (prog)
+    rc = cudaMemcpyAsync(x, w.b, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, st) ? ZT_ECUDA : ZT_OK;
+  else
+    rc = final_commutator(n, w.a, wn, h, x, st);
   prof_mark(3, st);
   return rc;
 }
@@ -330,6 +343,7 @@ struct GraphEntry {
   double h, tol;
   int max_iter;
   bool cons;
+  bool prog = false;  // progressive final update (host-copy variant)
   cudaGraphExec_t exec = nullptr;
   int64_t kp = 0, kb = 0, ke = 0;  // kernels in prologue / per iteration / epilogue
 };
@@ -389,7 +403,7 @@ static int build_step_graph(GraphEntry& e, StepWS& w) {
   if (!rc && e.cons) rc = cudaMemsetAsync(w.flags + 1, 0, sizeof(unsigned long long), cs) ? ZT_ECUDA : ZT_OK;
   if (!rc) {
     if (!e.cons && g_final_comm)
-      rc = final_update(op, x, e.wn, e.h, w, cs);
+      rc = final_update(op, x, e.wn, e.h, w, cs, e.prog);
     else
       rc = update(op, x, x, nullptr, e.cons ? e.wn : nullptr, x, hh, -qq, w, nullptr, e.cons ? w.flags + 1 : nullptr,
                   cs);
@@ -412,18 +426,78 @@ static int build_step_graph(GraphEntry& e, StepWS& w) {
   return ZT_OK;
 }
 
+using wait_value_fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static wait_value_fn wait_value32() {
+  static wait_value_fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<wait_value_fn>(f);
+  }
+  return fn;
+}
+static thread_local cudaStream_t t_copy = nullptr, t_copy2 = nullptr;
+static thread_local cudaEvent_t t_copy_ev = nullptr, t_copy_ev2 = nullptr, t_reset_ev = nullptr;
+
+// Enqueue the row-block device-to-host copies of W_{n+1} behind the progressive
+// final update's flags: clear the flags on `st`, then (after that clear, via an
+// event) wait for each block's flag on the copy stream and copy the block.
+// Call right before the step graph launch on `st`; `join` makes `st` wait for
+// the copies (call after the launch).
+static int host_copy_prologue(int n, StepWS& w, cudaStream_t st) {
+  if (!t_copy) {
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_copy, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_copy2, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_copy_ev, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_copy_ev2, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_reset_ev, cudaEventDisableTiming));
+  }
+  const int T = (n + 63) / 64;
+  unsigned* flags = w.prog + (size_t)T * (T + 1) / 2 + T;
+  ZT_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(unsigned) * T, st));
+  ZT_CUDA_CHECK(cudaEventRecord(t_reset_ev, st));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_copy, t_reset_ev, 0));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_copy2, t_reset_ev, 0));
+  return ZT_OK;
+}
+static int host_copy_enqueue(int n, StepWS& w, double* host_out, cudaStream_t st) {
+  const int T = (n + 63) / 64;
+  const unsigned* flags = w.prog + (size_t)T * (T + 1) / 2 + T;
+  // two copy streams (alternating blocks) so one block's flag wait and copy
+  // setup overlap the other's transfer
+  for (int s = 0; s < T; ++s) {
+    cudaStream_t cs = (s & 1) ? t_copy2 : t_copy;
+    const CUresult r = wait_value32()(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(flags + s),
+                                      1u, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(ZT_ECUDA, "cuStreamWaitValue32 failed");
+    const size_t rows = std::min(64, n - s * 64);
+    ZT_CUDA_CHECK(cudaMemcpyAsync(host_out + (size_t)s * 64 * n * 2, w.b + (size_t)s * 64 * n * 2, rows * n * 16,
+                                  cudaMemcpyDeviceToHost, cs));
+  }
+  ZT_CUDA_CHECK(cudaEventRecord(t_copy_ev, t_copy));
+  ZT_CUDA_CHECK(cudaEventRecord(t_copy_ev2, t_copy2));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, t_copy_ev, 0));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, t_copy_ev2, 0));
+  return ZT_OK;
+}
+
 static int midpoint_step_graph(zt_operator* op, const double* wn, double* w_next, double h, double tol,
                                int max_iter, StepWS& w, void* ws, int* iterations, double* residual,
-                               double* consistency, cudaStream_t st) {
+                               double* consistency, cudaStream_t st, double* host_out = nullptr) {
   if (!(h >= 0.0)) return fail(ZT_EINVAL, "time-step must be nonnegative, got " + std::to_string(h));
   if (!(tol > 0.0)) return fail(ZT_EINVAL, "tolerance must be positive, got " + std::to_string(tol));
   if (max_iter < 1) return fail(ZT_EINVAL, "max_iter must be at least 1, got " + std::to_string(max_iter));
   if (!t_mail.h) return fail(ZT_ENOMEM, "pinned mailbox allocation failed");
   const bool cons = consistency != nullptr;
+  const bool prog = host_out != nullptr && !cons && g_fused && g_final_comm && wait_value32() != nullptr;
   GraphEntry* hit = nullptr;
   for (auto& e : t_graphs)
     if (e.op == op && e.n == op->n && e.wn == wn && e.wnext == w_next && e.ws == ws && e.h == h && e.tol == tol &&
-        e.max_iter == max_iter && e.cons == cons)
+        e.max_iter == max_iter && e.cons == cons && e.prog == prog)
       hit = &e;
   if (!hit) {
     if (t_graphs.size() >= 8) {
@@ -440,12 +514,21 @@ static int midpoint_step_graph(zt_operator* op, const double* wn, double* w_next
     e.tol = tol;
     e.max_iter = max_iter;
     e.cons = cons;
+    e.prog = prog;
     int rc = build_step_graph(e, w);
     if (rc) return rc;
     t_graphs.push_back(e);
     hit = &t_graphs.back();
   }
-  ZT_CUDA_CHECK(cudaGraphLaunch(hit->exec, st));
+  if (prog) {
+    int rc = host_copy_prologue(op->n, w, st);
+    if (rc) return rc;
+    ZT_CUDA_CHECK(cudaGraphLaunch(hit->exec, st));
+    rc = host_copy_enqueue(op->n, w, host_out, st);
+    if (rc) return rc;
+  } else {
+    ZT_CUDA_CHECK(cudaGraphLaunch(hit->exec, st));
+  }
   ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h, w.flags, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   ZT_CUDA_CHECK(cudaMemcpyAsync(t_mail.h + 8, w.val, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   ZT_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -471,6 +554,10 @@ static int midpoint_step_graph(zt_operator* op, const double* wn, double* w_next
     return fail(ZT_ENOCONV, buf);
   }
   if (cons) *consistency = bits_to_double(t_mail.h[1]);
+  if (host_out && !prog) {
+    ZT_CUDA_CHECK(cudaMemcpyAsync(host_out, w_next, (size_t)op->n * op->n * 16, cudaMemcpyDeviceToHost, st));
+    ZT_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
   return ZT_OK;
 }
 
@@ -641,6 +728,28 @@ int zt_midpoint_step(zt_op_t op, const double* wn, double* w_next, double h_eff,
     ZT_CUDA_CHECK(cudaStreamSynchronize(st));
     *consistency = bits_to_double(t_mail.h[4]);
   }
+  return ZT_OK;
+}
+
+int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* host_out, double h_eff, double tol,
+                          int max_iter, void* workspace, size_t workspace_bytes, int* iterations, double* residual,
+                          void* stream) {
+  if (!op || !wn || !w_next || !host_out || !workspace || !iterations || !residual)
+    return fail(ZT_EINVAL, "zt_midpoint_step_host: bad argument");
+  if (wn == w_next) return fail(ZT_EINVAL, "zt_midpoint_step_host: w_next must not alias w_n");
+  if (workspace_bytes < zt_step_workspace_bytes(op->n)) return fail(ZT_ENOMEM, "step workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g_graph && !g_prof) {
+    StepWS w;
+    ws_layout(op->n, reinterpret_cast<char*>(workspace), &w);
+    return midpoint_step_graph(op, wn, w_next, h_eff, tol, max_iter, w, workspace, iterations, residual, nullptr,
+                               st, host_out);
+  }
+  int rc = zt_midpoint_step(op, wn, w_next, h_eff, tol, max_iter, workspace, workspace_bytes, iterations, residual,
+                            nullptr, stream);
+  if (rc) return rc;
+  ZT_CUDA_CHECK(cudaMemcpyAsync(host_out, w_next, (size_t)op->n * op->n * 16, cudaMemcpyDeviceToHost, st));
+  ZT_CUDA_CHECK(cudaStreamSynchronize(st));
   return ZT_OK;
 }
 

@@ -44,6 +44,15 @@ int cuda_fail(cudaError_t e, const char* where);
 
 #define ZT_LAUNCHED() ::zt::g_launches.fetch_add(1, std::memory_order_relaxed)
 
+// progressive final update (zt_gemm.cu, FusedArgs::prog): W_{n+1} rows are
+// published block by block for an overlapped device-to-host copy
+struct ProgParams {
+  const double* wn;
+  double* wout;
+  double h;
+  unsigned int* words;  // zupdate_prog_words(n): pair / row counters, row flags
+};
+
 // complex128 as double2 (re, im) — matches numpy/torch interleaved layout
 struct cplx {
   double re, im;

@@ -151,6 +151,23 @@ __device__ __forceinline__ void tile_of(int t, bool lower, int T, int& I, int& J
   }
 }
 
+// Row-block shell order: shell s = tiles (s, s..T-1) then (s+1..T-1, s);
+// prefix(s) = s (2T - s).  Row block s of W_{n+1} needs shells 0..s only.
+__device__ __forceinline__ void shell_tile(int t, int T, int& I, int& J) {
+  int s = (int)((double)T - sqrt((double)T * T - (double)t));
+  s = max(0, min(s, T - 1));
+  while (s > 0 && s * (2 * T - s) > t) --s;
+  while (s + 1 < T && (s + 1) * (2 * T - s - 1) <= t) ++s;
+  const int r = t - s * (2 * T - s);
+  if (r < T - s) {
+    I = s;
+    J = s + r;
+  } else {
+    I = s + 1 + (r - (T - s));
+    J = s;
+  }
+}
+
 // ---- shared pieces --------------------------------------------------------
 template <int ALGO>
 struct Acc {
@@ -514,6 +531,19 @@ struct FusedArgs {
   double* b_out;
   double* split_acc;        // [split_s * split_f][NACC*4*WNB*2][consumer threads]
   int gemm1_only;           // final update: only a = P X (no GEMM-2, no a plane)
+  // progressive final update (gemm1_only): tiles in row-block shell order;
+  // the second CTA to finish a tile pair {(I,J), (J,I)} writes W_{n+1} on
+  // both tiles (W_n + h (a - a^H), k_final_commutator's arithmetic) into
+  // `wout`, and the last pair of a 64-row block publishes it by storing the
+  // step's epoch into row_flag[block] (a copy stream waits on it and moves
+  // the block to the host while the GEMM continues)
+  int prog;
+  const double* wn;
+  double* wout;
+  double h;
+  unsigned int* pair_cnt;   // [T (T + 1) / 2] (zeroed per launch)
+  unsigned int* rows_done;  // [T] (zeroed per launch)
+  unsigned int* row_flag;   // [T] block-ready flags (cleared by the host per step)
 };
 
 constexpr int SPLIT_MAX_PARTS = 320;
@@ -523,6 +553,68 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Progressive final update, called by every consumer thread right after its
+// CTA published GEMM-1 tile (I, J) of a (stores fenced, consumer barrier
+// passed).  The second tile of the pair to finish writes W_{n+1} on both
+// tiles from its own accumulators and the partner tile of a.
+template <int ALGO>
+__device__ __forceinline__ void progressive_pair(const FusedArgs& f, const Acc<ALGO>& A, int I, int J, int T,
+                                                 int wm, int wn, int lane, int& flag_smem) {
+  const int lo = min(I, J), hi = max(I, J);
+  if (threadIdx.x == 0) {
+    const unsigned old = (I == J) ? 1u : atomicAdd(f.pair_cnt + hi * (hi + 1) / 2 + lo, 1u);
+    flag_smem = (old == 1u);
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+  const bool fin = flag_smem;
+  asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+  if (!fin) return;
+  __threadfence();  // acquire: the partner CTA fenced its a tile before counting
+  const int n = f.g2.n;
+  const double h = f.h;
+  const double* a = f.a_out;
+  const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < WNB; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gi = I * BM + wm * 32 + i * 8 + fr;
+        const int gj = J * BN + wn * 8 * WNB + j * 8 + fk * 2 + e;
+        if (gi >= n || gj >= n) continue;
+        double cr, ci;
+        if (ALGO != ALGO_4M) {
+          cr = A.v[0][i][j][e] - A.v[1][i][j][e];
+          ci = A.v[2][i][j][e] - A.v[0][i][j][e] - A.v[1][i][j][e];
+        } else {
+          cr = A.v[0][i][j][e];
+          ci = A.v[1][i][j][e];
+        }
+        const size_t oij = ((size_t)gi * n + gj) * 2, oji = ((size_t)gj * n + gi) * 2;
+        const double2 aji = __ldcg(reinterpret_cast<const double2*>(a + oji));
+        // k_final_commutator's arithmetic: d = a - a^H, W_n + h d
+        const double2 d = make_double2(__dsub_rn(cr, aji.x), __dadd_rn(ci, aji.y));
+        const double2 w0 = ld2(f.wn + oij);
+        st2(f.wout + oij, make_double2(__dadd_rn(w0.x, __dmul_rn(h, d.x)), __dadd_rn(w0.y, __dmul_rn(h, d.y))));
+        if (I != J) {  // (a - a^H)_ji = -conj(d)
+          const double2 w1 = ld2(f.wn + oji);
+          st2(f.wout + oji, make_double2(__dadd_rn(w1.x, __dmul_rn(h, -d.x)), __dadd_rn(w1.y, __dmul_rn(h, d.y))));
+        }
+      }
+  __threadfence_system();
+  asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < (I == J ? 1 : 2); ++q) {
+      const int rb = q ? J : I;
+      if (atomicAdd(f.rows_done + rb, 1u) + 1u == (unsigned)T) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.row_flag + rb), "r"(1u) : "memory");
+      }
+    }
+  }
 }
 
 template <int ALGO>
@@ -595,7 +687,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
       const CUtensorMap *ma, *mb;
       const double *pla, *plb;
       if (id < T1) {
-        tile_of(id, false, T, I, J);
+        if (f.prog)
+          shell_tile(id, T, I, J);
+        else
+          tile_of(id, false, T, I, J);
         ma = &f.tma_p;
         mb = &f.tma_x;
         pla = f.pa1;
@@ -647,7 +742,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
     int I, J, tl = 0, part = -1, sidx = -1;
     const bool phase1 = id < T1;
     if (phase1) {
-      tile_of(id, false, T, I, J);
+      if (f.prog)
+        shell_tile(id, T, I, J);
+      else
+        tile_of(id, false, T, I, J);
     } else {
       g2_unit(id - T1, tl, part, sidx);
       tile_of(tl, true, T, I, J);
@@ -689,6 +787,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_zupdate(const __grid_consta
       asm volatile("fence.proxy.async.global;" ::: "memory");
       asm volatile("bar.sync 2, %0;" ::"r"(CONSUMER_WARPS * 32));
       if (threadIdx.x == 0) atomicAdd(f.done + I, 1u);
+      if (f.prog) progressive_pair(f, acc, I, J, T, wm, wn, lane, split_last);
     } else {
       if (part >= 0) {
         // K slice of a tail tile: publish the partial accumulators; the last
@@ -1061,6 +1160,12 @@ size_t sum_plane_bytes(int n) {
   return (size_t)((n + 63) / 64) * 64 * ((n + 15) / 16) * 16 * sizeof(double);
 }
 
+// progressive final update words: pair counters, row counters, row flags
+size_t zupdate_prog_words(int n) {
+  const size_t T = (n + BM - 1) / BM;
+  return T * (T + 1) / 2 + 2 * T;
+}
+
 size_t zupdate_split_bytes(int n) {
   const int T = (n + BM - 1) / BM;
   const int parts = std::min(SPLIT_MAX_PARTS, 4 * (T * (T + 1) / 2));
@@ -1256,7 +1361,7 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
-                  cudaStream_t st, int gemm1_only, double* bbuf) {
+                  cudaStream_t st, int gemm1_only, double* bbuf, const ProgParams* prog) {
   FusedArgs f;
   memset(&f, 0, sizeof f);
   GemmArgs& g = f.g2;
@@ -1325,6 +1430,16 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
   f.split_sem = sync + 1 + T;
   f.split_acc = split;
   ZT_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned int) * (T + 1 + S), st));
+  if (prog && gemm1_only) {
+    f.prog = 1;
+    f.wn = prog->wn;
+    f.wout = prog->wout;
+    f.h = prog->h;
+    f.pair_cnt = prog->words;
+    f.rows_done = prog->words + T * (T + 1) / 2;
+    f.row_flag = f.rows_done + T;
+    ZT_CUDA_CHECK(cudaMemsetAsync(prog->words, 0, sizeof(unsigned int) * (T * (T + 1) / 2 + T), st));
+  }
   if (algo == ALGO_4M)
     k_zupdate<ALGO_4M><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(f);
   else if (algo == ALGO_3MS)

@@ -127,12 +127,23 @@ def fixed_point_solve(w_n, h: float, tol: float = 1e-12, max_iter: int = 10,
 
 def midpoint_step_raw(w: torch.Tensor, h_eff: float, tol: float, max_iter: int,
                       op: LaplacianOperator, out: torch.Tensor | None = None,
-                      check_consistency: bool = False):
+                      check_consistency: bool = False, host_out: torch.Tensor | None = None):
     """Device fast path: W_{n+1} into ``out`` (fresh if None); returns
-    (w_next, iterations, last_residual, consistency)."""
+    (w_next, iterations, last_residual, consistency).  ``host_out`` (pinned
+    CPU complex128, N x N) also receives W_{n+1}, copied block by block while
+    the step's last GEMM still runs (zt_midpoint_step_host)."""
     w_next = torch.empty_like(w) if out is None else out
     ws = _step_ws(op, w.device)
     it, res, cons = ctypes.c_int(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    if host_out is not None and not check_consistency:
+        if host_out.shape != w.shape or host_out.dtype != torch.complex128 or host_out.is_cuda:
+            raise ValueError("host_out must be a CPU complex128 tensor shaped like w")
+        rc = lib.zt_midpoint_step_host(op.handle, w.data_ptr(), w_next.data_ptr(), host_out.data_ptr(),
+                                       float(h_eff), float(tol), int(max_iter), ws.data_ptr(), ws.numel(),
+                                       ctypes.byref(it), ctypes.byref(res), _stream_ptr(w.device))
+        if rc:
+            _raise(rc, it.value, res.value)
+        return w_next, it.value, res.value, None
     rc = lib.zt_midpoint_step(op.handle, w.data_ptr(), w_next.data_ptr(), float(h_eff), float(tol),
                               int(max_iter), ws.data_ptr(), ws.numel(), ctypes.byref(it),
                               ctypes.byref(res), ctypes.byref(cons) if check_consistency else None,
@@ -149,11 +160,19 @@ def midpoint_step_info(state: StepperState, op: LaplacianOperator | None = None,
     _params(h, state.tol, state.max_iter)
     wd, as_np = _to_device(state.w)
     op = _resolve(op, wd)
-    w_next, iters, res, cons = midpoint_step_raw(wd, h, state.tol, state.max_iter, op,
-                                                 check_consistency=check_consistency)
+    if as_np and not check_consistency:
+        # numpy in, numpy out: W_{n+1} lands in a pinned block (torch's caching
+        # host allocator) through the overlapped block copies
+        host = torch.empty(wd.shape, dtype=torch.complex128, pin_memory=True)
+        _, iters, res, cons = midpoint_step_raw(wd, h, state.tol, state.max_iter, op, host_out=host)
+        w_out = host.numpy()
+    else:
+        w_next, iters, res, cons = midpoint_step_raw(wd, h, state.tol, state.max_iter, op,
+                                                     check_consistency=check_consistency)
+        w_out = _out(w_next, as_np)
     new_state = replace(
         state,
-        w=_out(w_next, as_np),
+        w=w_out,
         time=state.time + state.h,
         step_index=state.step_index + 1,
     )

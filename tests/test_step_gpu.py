@@ -188,3 +188,32 @@ def test_cfg3_commutator_and_sandwich_full_size(zt, n):
     assert np.array_equal(c, -c.conj().T)
     sref = wn - 0.5 * h * cref - 0.25 * h * h * (a @ pn)
     assert relf(S.cpu().numpy(), sref) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [5, 64, 130, 1000])
+def test_host_result_step_bitwise(n):
+    """zt_midpoint_step_host (progressive final update, W_{n+1} copied to the
+    host block by block while the last GEMM runs) == the plain step, on the
+    host and on the device, step after step; errors still raise (no hang)."""
+    from paper_2206_05466_b200 import FixedPointError, build_operator
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+
+    dev = torch.device("cuda:0")
+    w0 = torch.from_numpy(zo.random_admissible(n, np.random.default_rng(n), 1.0 / n)).to(dev)
+    op = build_operator(n, dev)
+    host = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    x1, x2 = w0, w0.clone()
+    for _ in range(3):
+        y1, k1, r1, _ = midpoint_step_raw(x1, 0.01, 1e-12, 10, op)
+        y2, k2, r2, _ = midpoint_step_raw(x2, 0.01, 1e-12, 10, op, host_out=host)
+        assert (k1, r1) == (k2, r2)
+        assert torch.equal(y1, y2)
+        assert torch.equal(y1.cpu(), host)
+        x1, x2 = y1, y2
+    with pytest.raises(FixedPointError):
+        midpoint_step_raw(x2, 0.5, 1e-14, 1, op, host_out=host)
+    # the numpy drop-in goes through it and returns pinned-backed arrays
+    from paper_2206_05466_b200 import StepperState, midpoint_step_info
+
+    st, info = midpoint_step_info(StepperState(w=x1.cpu().numpy(), h=0.01))
+    assert isinstance(st.w, np.ndarray) and np.array_equal(st.w, midpoint_step_raw(x1, 0.01, 1e-12, 10, op)[0].cpu().numpy())
