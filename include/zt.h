@@ -142,6 +142,17 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
                           double tol, int max_iter, void* workspace, size_t workspace_bytes,
                           int* iterations, double* residual, void* stream);
 
+/* INT8 tensor-core building block of an FP64-accurate complex GEMM
+ * (Ozaki scheme II, csrc/zt_oz.cu): for every modulus j < nmod, the
+ * centred residues mod p_j of Re / Im of A * B^T from int8 residue planes
+ * A [nmod][3][mp][kp] (re, im, -im) and B [nmod][2][np][kp] (re, im) into
+ * R [nmod][2][mp][np]; tcgen05 kind::i8 MMAs, int32 accumulation in TMEM.
+ * mp, np, kp multiples of 128; lower != 0: square, only 128-tiles on or
+ * below the diagonal.  zt_oz_moduli writes the moduli, returns their count. */
+int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, const void* b, void* r, int lower,
+                  void* stream);
+int zt_oz_moduli(int* out, int cap);
+
 /* Config-3 ops (integrator.py:127-129): commutator C = P W - W P = a - a^H
  * with a = P W; sandwich S = W - (h/2)(a - a^H) - (h^2/4) a P
  * = (I - hP/2) W (I + hP/2).  `work` holds n*n complex (a). */
