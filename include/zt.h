@@ -152,6 +152,15 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
 int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, const void* b, void* r, int lower,
                   void* stream);
 int zt_oz_moduli(int* out, int cap);
+/* C = A B (complex128, n x n, row-major with leading dimensions) through the
+ * residue GEMM: rows of A and columns of B scaled to integers of up to 53
+ * bits, 18 moduli, CRT reconstruction in 128-bit integers.  bmode 1: B is
+ * skew-Hermitian with B[k][j] == -conj(B[j][k]) exactly off the diagonal
+ * (converted row-wise, no transpose).  lower: only the 128-tiles of C on or
+ * below the diagonal.  workspace: zt_oz_workspace_bytes(n). */
+size_t zt_oz_workspace_bytes(int n);
+int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c,
+                int64_t ldc, int lower, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Config-3 ops (integrator.py:127-129): commutator C = P W - W P = a - a^H
  * with a = P W; sandwich S = W - (h/2)(a - a^H) - (h^2/4) a P

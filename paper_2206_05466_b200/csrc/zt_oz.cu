@@ -13,6 +13,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "zt_common.cuh"
 #include "zt_tma.cuh"
@@ -273,6 +274,269 @@ static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols) {
 
 }  // namespace oz
 
+int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* b, int8_t* r, int lower,
+               cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Operand conversion: scale each row (A operand) / each column (B operand) of
+// a complex128 matrix by a power of two so its largest |re|, |im| lies in
+// [2^(KB-1), 2^KB), round to integers (exact in binary64 for KB <= 53), and
+// write the centred residues mod every p_j as int8 planes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int8_t res8(double x, int p, double invp) {
+  // x integer-valued, |x| < 2^53; any integer quotient keeps x - q p == x
+  // (mod p) exactly; one correction step centres it
+  const double q = rint(x * invp);
+  int r = (int)(x - q * (double)p);
+  const int h = p >> 1;
+  if (r > h) r -= p;
+  if (r < -h) r += p;
+  return (int8_t)r;
+}
+
+// exponent shift that puts amax in [2^(KB-1), 2^KB); 0 for an all-zero line
+__device__ __forceinline__ int oz_shift(double amax, int kb) { return amax > 0.0 ? kb - 1 - ilogb(amax) : 0; }
+
+// A-type rows: planes (re, im, -im) of row i; mode 1 = the B layout of a
+// skew-Hermitian S (B[j][k] = S[k][j] = -conj(S[j][k]) off the diagonal):
+// planes (re, im) of that.  One block per padded row; 4 consecutive k per
+// thread (one 32-bit store per plane).
+__global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __restrict__ src, int64_t ld, int mp,
+                                                      int kp, int nmod, int kb, int mode, int8_t* out,
+                                                      int* __restrict__ shift) {
+  const int i = blockIdx.x;
+  const int nplanes = mode == 0 ? 3 : 2;
+  __shared__ double red[8];
+  double amax = 0.0;
+  if (i < n)
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const double2 v = ld2(src + ((size_t)i * ld + k) * 2);
+      amax = fmax(amax, fmax(fabs(v.x), fabs(v.y)));
+    }
+  for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = red[0];
+  for (int q = 1; q < 8; ++q) amax = fmax(amax, red[q]);
+  const int sh = oz_shift(amax, kb);
+  if (threadIdx.x == 0 && shift) shift[i] = sh;
+  for (int k0 = threadIdx.x * 4; k0 < kp; k0 += blockDim.x * 4) {
+    double xr[4], xi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = k0 + e;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < n && k < n) {
+        v = ld2(src + ((size_t)i * ld + k) * 2);
+        if (mode == 1 && k != i) v = make_double2(-v.x, v.y);
+      }
+      xr[e] = rint(ldexp(v.x, sh));
+      xi[e] = rint(ldexp(v.y, sh));
+    }
+    for (int j = 0; j < nmod; ++j) {
+      const int p = c_oz_p[j];
+      const double invp = 1.0 / (double)p;
+      uint32_t wr = 0, wi = 0, wn = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int8_t rr = res8(xr[e], p, invp), ri = res8(xi[e], p, invp);
+        wr |= (uint32_t)(uint8_t)rr << (8 * e);
+        wi |= (uint32_t)(uint8_t)ri << (8 * e);
+        wn |= (uint32_t)(uint8_t)(int8_t)(-ri) << (8 * e);
+      }
+      int8_t* base = out + ((size_t)(j * nplanes) * mp + i) * kp + k0;
+      *reinterpret_cast<uint32_t*>(base) = wr;
+      *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
+      if (nplanes == 3) *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
+    }
+  }
+}
+
+// B operand of a general matrix X (B[j][k] = X[k][j]): column maxima first
+__global__ void __launch_bounds__(256) k_oz_colmax(int n, const double* __restrict__ x, int64_t ld,
+                                                   unsigned long long* colmax) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r0 = blockIdx.y * 64 + (threadIdx.x >> 5) * 8;
+  if (j >= n) return;
+  double m = 0.0;
+  for (int r = r0; r < min(r0 + 8, n); ++r) {
+    const double2 v = ld2(x + ((size_t)r * ld + j) * 2);
+    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+  }
+  atomicMax(colmax + j, (unsigned long long)__double_as_longlong(m));
+}
+
+// then 32 (k) x 32 (j) tiles through shared memory, residues written as
+// rows j of 32 consecutive k
+__global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __restrict__ x, int64_t ld, int np,
+                                                      int kp, int nmod, int kb,
+                                                      const unsigned long long* __restrict__ colmax, int8_t* out,
+                                                      int* __restrict__ shift) {
+  __shared__ double tr[32][33], ti[32][33];
+  __shared__ int8_t rb[2][32][36];
+  const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int k = k0 + r, j = j0 + tx;
+    double2 v = make_double2(0.0, 0.0);
+    if (k < n && j < n) v = ld2(x + ((size_t)k * ld + j) * 2);
+    tr[r][tx] = v.x;
+    ti[r][tx] = v.y;
+  }
+  __syncthreads();
+  // thread (ty, tx): output row j = j0 + r (r = ty + 8 q), k = k0 + tx
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q, j = j0 + r;
+    const double m = (j < n) ? __longlong_as_double((long long)colmax[j]) : 0.0;
+    const int sh = oz_shift(m, kb);
+    if (blockIdx.y == 0 && tx == 0 && shift && j < np) shift[j] = sh;
+    const double xr = rint(ldexp(tr[tx][r], sh)), xi = rint(ldexp(ti[tx][r], sh));
+    for (int t = 0; t < nmod; ++t) {
+      const int p = c_oz_p[t];
+      const double invp = 1.0 / (double)p;
+      int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + tx;
+      base[0] = res8(xr, p, invp);
+      base[(size_t)np * kp] = res8(xi, p, invp);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reconstruction: the exact integer from its residues (CRT in 128-bit
+// integers), centred, times 2^-(row shift + column shift).
+// ---------------------------------------------------------------------------
+struct CrtConst {
+  unsigned long long mt_lo[OZ_NMOD], mt_hi[OZ_NMOD];  // M / p_t
+  int y[OZ_NMOD];                                     // (M / p_t)^-1 mod p_t
+  unsigned long long m_lo, m_hi;                      // M
+  double m_dbl;
+};
+__constant__ CrtConst c_crt;
+
+__device__ __forceinline__ double crt_value(const int8_t* r, size_t plane_stride, int nmod) {
+  typedef unsigned __int128 u128;
+  u128 s = 0;
+  for (int t = 0; t < nmod; ++t) {
+    const int p = c_oz_p[t];
+    int v = r[(size_t)t * plane_stride];
+    v = (v % p + p) % p;
+    const int u = (v * c_crt.y[t]) % p;
+    const u128 mt = ((u128)c_crt.mt_hi[t] << 64) | c_crt.mt_lo[t];
+    s += (u128)(unsigned)u * mt;
+  }
+  const u128 m = ((u128)c_crt.m_hi << 64) | c_crt.m_lo;
+  // s < nmod * M: reduce with an estimated quotient, then correct
+  const double sd = (double)(unsigned long long)(s >> 64) * 18446744073709551616.0 + (double)(unsigned long long)s;
+  long long q = (long long)(sd / c_crt.m_dbl);
+  u128 qm = (u128)(unsigned long long)q * m;
+  while (qm > s) {
+    qm -= m;
+    --q;
+  }
+  u128 x = s - qm;
+  while (x >= m) x -= m;
+  // centre: x in [0, M) -> (-M/2, M/2]
+  const bool neg = x > (m >> 1);
+  const u128 mag = neg ? m - x : x;
+  const double hi = (double)(unsigned long long)(mag >> 64), lo = (double)(unsigned long long)mag;
+  const double v = fma(hi, 18446744073709551616.0, lo);
+  return neg ? -v : v;
+}
+
+// C (complex128, ldc) = residue product scaled back; lower: only 128-tiles on
+// or below the diagonal.  4 consecutive columns per thread.
+__global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
+                                                  int np, const int* __restrict__ rs, const int* __restrict__ cs,
+                                                  double* c, int64_t ldc, int lower) {
+  const int i = blockIdx.y;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= m || j >= n) return;
+  if (lower && (j >> 7) > (i >> 7)) return;
+  const size_t ps = (size_t)2 * mp * np;  // stride between moduli
+  const int8_t* re = r + (size_t)i * np + j;
+  const double vr = crt_value(re, ps, nmod), vi = crt_value(re + (size_t)mp * np, ps, nmod);
+  const int sh = -(rs[i] + cs[j]);
+  st2(c + ((size_t)i * ldc + j) * 2, make_double2(ldexp(vr, sh), ldexp(vi, sh)));
+}
+
+static bool g_crt_ready = false;
+static int crt_init() {
+  typedef unsigned __int128 u128;
+  CrtConst h;
+  u128 m = 1;
+  for (int t = 0; t < OZ_NMOD; ++t) m *= (u128)h_oz_p[t];
+  for (int t = 0; t < OZ_NMOD; ++t) {
+    const int p = h_oz_p[t];
+    const u128 mt = m / (u128)p;
+    const int r = (int)(mt % (u128)p);
+    int y = 1;
+    while ((r * y) % p != 1) ++y;  // p <= 128: direct search
+    h.mt_lo[t] = (unsigned long long)mt;
+    h.mt_hi[t] = (unsigned long long)(mt >> 64);
+    h.y[t] = y;
+  }
+  h.m_lo = (unsigned long long)m;
+  h.m_hi = (unsigned long long)(m >> 64);
+  h.m_dbl = (double)h.m_hi * 18446744073709551616.0 + (double)h.m_lo;
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
+  g_crt_ready = true;
+  return ZT_OK;
+}
+
+// integer bits per operand entry so that |sum| < M / 2 over K terms (4M form)
+static int oz_bits(int k) {
+  double lg = 0.0;
+  for (int t = 0; t < OZ_NMOD; ++t) lg += std::log2((double)h_oz_p[t]);
+  const int kb = (int)std::floor((lg - 1.0 - std::log2(2.0 * k) - 1e-9) / 2.0);
+  return std::min(53, kb);
+}
+
+size_t oz_workspace_bytes(int n) {
+  const size_t p = ((size_t)n + 127) / 128 * 128;
+  return (size_t)OZ_NMOD * p * p * (3 + 2 + 2) + 2 * p * sizeof(int) + p * 8 + 1024;
+}
+
+// C = A B for complex128 n x n, A general (row scaled), B: bmode 0 general
+// (column scaled, transposed conversion), 1 skew-Hermitian with exact
+// mirror off the diagonal (converted row-wise as -conj).  lower: only the
+// 128-tiles of C on or below the diagonal are computed.
+int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c, int64_t ldc,
+             int lower, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n < 1) return fail(ZT_EINVAL, "oz_zgemm: bad size");
+  if (ws_bytes < oz_workspace_bytes(n)) return fail(ZT_ENOMEM, "oz_zgemm: workspace too small");
+  if (!g_crt_ready) {
+    const int rc = crt_init();
+    if (rc) return rc;
+  }
+  const int p = (n + 127) / 128 * 128;
+  const int kb = oz_bits(n);
+  int8_t* ares = static_cast<int8_t*>(ws);
+  int8_t* bres = ares + (size_t)OZ_NMOD * 3 * p * p;
+  int8_t* rres = bres + (size_t)OZ_NMOD * 2 * p * p;
+  int* rsh = reinterpret_cast<int*>(rres + (size_t)OZ_NMOD * 2 * p * p);
+  int* csh = rsh + p;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(csh + p);
+  k_oz_conv_rows<<<p, 256, 0, st>>>(n, a, lda, p, p, OZ_NMOD, kb, 0, ares, rsh);
+  ZT_LAUNCHED();
+  if (bmode == 1) {
+    k_oz_conv_rows<<<p, 256, 0, st>>>(n, b, ldb, p, p, OZ_NMOD, kb, 1, bres, csh);
+    ZT_LAUNCHED();
+  } else {
+    ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * p, st));
+    if (p != n) ZT_CUDA_CHECK(cudaMemsetAsync(bres, 0, (size_t)OZ_NMOD * 2 * p * p, st));
+    k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, b, ldb, cmax);
+    ZT_LAUNCHED();
+    k_oz_conv_cols<<<dim3(p / 32, p / 32), 256, 0, st>>>(n, b, ldb, p, p, OZ_NMOD, kb, cmax, bres, csh);
+    ZT_LAUNCHED();
+  }
+  int rc = oz_modgemm(OZ_NMOD, p, p, p, ares, bres, rres, lower, st);
+  if (rc) return rc;
+  k_oz_recon<<<dim3((n + 255) / 256, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc, lower);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
 static int g_oz_sms = 0;
 
 // R = A * B^T residues for every modulus (see header); mp, np, kp multiples of 128
@@ -323,3 +587,11 @@ extern "C" int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, co
 }
 
 extern "C" int zt_oz_moduli(int* out, int cap) { return zt::oz_moduli(out, cap); }
+
+extern "C" size_t zt_oz_workspace_bytes(int n) { return zt::oz_workspace_bytes(n); }
+
+extern "C" int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c,
+                           int64_t ldc, int lower, void* ws, size_t ws_bytes, void* stream) {
+  if (!a || !b || !c || !ws) return zt::fail(ZT_EINVAL, "zt_oz_zgemm: bad argument");
+  return zt::oz_zgemm(n, a, lda, b, ldb, bmode, c, ldc, lower, ws, ws_bytes, (cudaStream_t)stream);
+}
