@@ -68,6 +68,10 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,
                   cudaStream_t st, int gemm1_only = 0, double* bbuf = nullptr, const ProgParams* prog = nullptr);
 size_t zupdate_prog_words(int n);
+size_t oz_update_workspace_bytes(int n);
+int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, const double* base,
+              const double* xprev, const double* wn, double* out, double hh, double qq, unsigned long long* resid,
+              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only);
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
@@ -99,7 +103,9 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
                       const double* base, const double* xprev, double* out, int64_t ld, double hh,
                       double qq, unsigned long long* resid, int algo, cudaStream_t st);
 
-static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m)
+static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m), 2 = INT8 Ozaki-II (ZT_GEMM_ALGO=oz)
+// DMMA kernel variant for the products that stay on the FP64 pipe
+static inline int dmma_algo() { return g_algo == 1 ? 1 : 0; }
 static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
 static bool g_planes = true; // fused 3M reads precomputed sum planes (ZT_SUM_PLANES=0 disables)
 static bool g_split = true;  // split-K tail in the fused update (ZT_SPLIT=0 disables)
@@ -120,6 +126,7 @@ struct StepWS {
   double* b;           // n x n complex: b = a P (lower / diagonal tiles) for the update pass;
                        // W_{n+1} staging of the progressive final update
   unsigned int* prog;  // zupdate_prog_words(n): progressive final update counters / flags / epoch
+  void* oz;            // INT8 Ozaki-II residue planes (ZT_GEMM_ALGO=oz only)
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -145,8 +152,10 @@ static size_t ws_layout(int n, char* base, StepWS* w) {
     w->split = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl);
     w->b = reinterpret_cast<double*>(base + off + 2 * mat + sb + rb + 256 + yb + pl + spl);
     w->prog = reinterpret_cast<unsigned int*>(base + off + 3 * mat + sb + rb + 256 + yb + pl + spl);
+    w->oz = base + off + 3 * mat + sb + rb + 256 + yb + pl + spl + align_up(sizeof(unsigned int) * zupdate_prog_words(n));
   }
-  return 3 * mat + sb + rb + 256 + yb + pl + spl + align_up(sizeof(unsigned int) * zupdate_prog_words(n));
+  return 3 * mat + sb + rb + 256 + yb + pl + spl + align_up(sizeof(unsigned int) * zupdate_prog_words(n)) +
+         (g_algo == 2 ? align_up(oz_update_workspace_bytes(n)) : 0);
 }
 
 // small pinned host mailbox for the per-iteration read-back
@@ -224,6 +233,12 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
+  if (g_algo == 2) {
+    rc = oz_update(n, w.p, x, w.a, w.b, base, xprev, wn, out, hh, qq, resid, cons, w.oz, st, 0);
+    prof_mark(2, st);
+    prof_mark(3, st);
+    return rc;
+  }
   if (g_fused) {
     // GEMM-1 and GEMM-2 in one persistent launch (profiled as "gemm1")
     rc = zupdate_fused(n, w.p, x, w.a, base, xprev, wn, out, hh, qq, resid, cons, w.sync,
@@ -233,10 +248,10 @@ static int update(zt_operator* op, const double* x, const double* base, const do
     prof_mark(3, st);
     return rc;
   }
-  rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
+  rc = zgemm(n, w.p, n, x, n, w.a, n, dmma_algo(), st);
   if (rc) return rc;
   prof_mark(2, st);
-  rc = zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, g_algo, st);
+  rc = zgemm_update(n, w.a, w.p, base, xprev, wn, out, n, hh, qq, resid, cons, dmma_algo(), st);
   prof_mark(3, st);
   return rc;
 }
@@ -255,13 +270,19 @@ static int final_update(zt_operator* op, double* x, const double* wn, double h, 
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
+  if (g_algo == 2) {
+    rc = oz_update(n, w.p, x, w.a, nullptr, nullptr, nullptr, wn, x, h, 0.0, nullptr, nullptr, w.oz, st, 1);
+    prof_mark(2, st);
+    prof_mark(3, st);
+    return rc;
+  }
   prog = prog && g_fused;
   if (g_fused) {
     ProgParams pp{wn, w.b, h, w.prog};
     rc = zupdate_fused(n, w.p, x, w.a, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0, nullptr, nullptr, w.sync,
                        g_algo == 0 && g_planes ? 3 : g_algo, w.planes, nullptr, st, 1, nullptr, prog ? &pp : nullptr);
   } else {
-    rc = zgemm(n, w.p, n, x, n, w.a, n, g_algo, st);
+    rc = zgemm(n, w.p, n, x, n, w.a, n, dmma_algo(), st);
   }
   if (rc) return rc;
   prof_mark(2, st);
@@ -493,7 +514,7 @@ static int midpoint_step_graph(zt_operator* op, const double* wn, double* w_next
   if (max_iter < 1) return fail(ZT_EINVAL, "max_iter must be at least 1, got " + std::to_string(max_iter));
   if (!t_mail.h) return fail(ZT_ENOMEM, "pinned mailbox allocation failed");
   const bool cons = consistency != nullptr;
-  const bool prog = host_out != nullptr && !cons && g_fused && g_final_comm && wait_value32() != nullptr;
+  const bool prog = host_out != nullptr && !cons && g_fused && g_algo != 2 && g_final_comm && wait_value32() != nullptr;
   GraphEntry* hit = nullptr;
   for (auto& e : t_graphs)
     if (e.op == op && e.n == op->n && e.wn == wn && e.wnext == w_next && e.ws == ws && e.h == h && e.tol == tol &&
@@ -607,7 +628,7 @@ int zt_profile_read(double* ms, int64_t* counts, int reset) {
 
 int zt_op_create(int n, int device, zt_op_t* op) {
   if (!op) return fail(ZT_EINVAL, "null output");
-  if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : 0;
+  if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : (std::string(e) == "oz" ? 2 : 0);
   if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
   if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
@@ -681,7 +702,7 @@ int zt_zgemm_update_rows(int m, int n, const double* a_rows, const double* p, co
                          double qq, unsigned long long* resid_dev, void* stream) {
   if (m < 1 || n < 1 || !a_rows || !p || !ah_rows || !base || !out)
     return fail(ZT_EINVAL, "zt_zgemm_update_rows: bad argument");
-  return zgemm_update_rows(m, n, a_rows, p, ah_rows, base, xprev, out, ld, hh, qq, resid_dev, g_algo,
+  return zgemm_update_rows(m, n, a_rows, p, ah_rows, base, xprev, out, ld, hh, qq, resid_dev, dmma_algo(),
                            (cudaStream_t)stream);
 }
 
@@ -755,7 +776,7 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
 
 int zt_commutator(int n, const double* p, const double* w, double* c, double* work, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
+  int rc = zgemm(n, p, n, w, n, work, n, dmma_algo(), st);
   if (rc) return rc;
   return skew_diff(n, work, c, st);
 }
@@ -770,7 +791,7 @@ int zt_zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, con
                           double* c, int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc,
                           void* stream) {
   if (!a || !b || !c || !peers) return fail(ZT_EINVAL, "zt_zgemm_rect_scatter: bad argument");
-  return zgemm_rect_scatter(m, n, k, a, lda, b, ldb, c, ldc, peers, npeer, r0, mloc, g_algo, (cudaStream_t)stream);
+  return zgemm_rect_scatter(m, n, k, a, lda, b, ldb, c, ldc, peers, npeer, r0, mloc, dmma_algo(), (cudaStream_t)stream);
 }
 
 int zt_zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* p, const double* acol, int mloc,
@@ -780,13 +801,13 @@ int zt_zgemm_update_rows_peer(int m, int n, const double* a_rows, const double* 
   if (!a_rows || !p || !acol || !base || !out || (npeer && !peers))
     return fail(ZT_EINVAL, "zt_zgemm_update_rows_peer: bad argument");
   return zgemm_update_rows_peer(m, n, a_rows, p, acol, mloc, base, xprev, out, ld, hh, qq, resid, peers, npeer, r0,
-                                g_algo, (cudaStream_t)stream);
+                                dmma_algo(), (cudaStream_t)stream);
 }
 
 int zt_zgemm_rect_mirror(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb,
                          double* c, int64_t ldc, double* mirror, int64_t ld_mirror, void* stream) {
   if (!a || !b || !c) return fail(ZT_EINVAL, "zt_zgemm_rect_mirror: bad argument");
-  return zgemm_rect_mirror(m, n, k, a, lda, b, ldb, c, ldc, mirror, ld_mirror, g_algo, (cudaStream_t)stream);
+  return zgemm_rect_mirror(m, n, k, a, lda, b, ldb, c, ldc, mirror, ld_mirror, dmma_algo(), (cudaStream_t)stream);
 }
 
 int zt_update_rows_ew(int m, int n, const double* a_rows, const double* acol, int mloc, const double* b_rows,
@@ -824,10 +845,10 @@ int zt_basis_project(int n, int m0, int m1, const long long* off, const long lon
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work, void* stream) {
   // S = W - (h/2)(a - a^H) - (h^2/4) a P  with a = P W
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = zgemm(n, p, n, w, n, work, n, g_algo, st);
+  int rc = zgemm(n, p, n, w, n, work, n, dmma_algo(), st);
   if (rc) return rc;
   return zgemm_update(n, work, p, w, nullptr, nullptr, s, n, -0.5 * h, -0.25 * h * h, nullptr, nullptr,
-                      g_algo, st);
+                      dmma_algo(), st);
 }
 
 }  // extern "C"

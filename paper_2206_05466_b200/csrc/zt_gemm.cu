@@ -1358,6 +1358,26 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
   }
 }
 
+// the streaming update pass on its own (b from any GEMM that computed the
+// lower and diagonal BM x BN tiles)
+int update_pairs(int n, const double* a, const double* bm, double* out, const double* base, const double* xprev,
+                 const double* wn, double hh, double qq, unsigned long long* resid, unsigned long long* cons,
+                 cudaStream_t st) {
+  const int t32 = (n + 31) / 32;
+  const int nb = t32 * (t32 + 1) / 2;
+  if (xprev && wn)
+    k_update_pairs<true, true><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
+  else if (xprev)
+    k_update_pairs<true, false><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
+  else if (wn)
+    k_update_pairs<false, true><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
+  else
+    k_update_pairs<false, false><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
 int zupdate_fused(int n, const double* p, const double* x, double* a, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, unsigned long long* resid,
                   unsigned long long* cons, unsigned int* sync, int algo, double* planes, double* split,

@@ -281,17 +281,32 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
 // Operand conversion: scale each row (A operand) / each column (B operand) of
 // a complex128 matrix by a power of two so its largest |re|, |im| lies in
 // [2^(KB-1), 2^KB), round to integers (exact in binary64 for KB <= 53), and
-// write the centred residues mod every p_j as int8 planes.
+// write the centred residues mod every p_j as int8 planes.  Residues come
+// from 18-bit limbs of |x| in 32-bit integer arithmetic (Barrett reduction),
+// not from FP64 divisions.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int8_t res8(double x, int p, double invp) {
-  // x integer-valued, |x| < 2^53; any integer quotient keeps x - q p == x
-  // (mod p) exactly; one correction step centres it
-  const double q = rint(x * invp);
-  int r = (int)(x - q * (double)p);
-  const int h = p >> 1;
-  if (r > h) r -= p;
-  if (r < -h) r += p;
-  return (int8_t)r;
+struct ResConst {
+  unsigned c1[OZ_NMOD], c2[OZ_NMOD];  // 2^18 mod p, 2^36 mod p
+  unsigned m[OZ_NMOD];                // floor(2^32 / p)
+};
+__constant__ ResConst c_res;
+
+__device__ __forceinline__ void limbs(double x, unsigned& l0, unsigned& l1, unsigned& l2, bool& neg) {
+  const long long v = (long long)x;  // integer valued, |x| < 2^53
+  neg = v < 0;
+  const unsigned long long a = neg ? (unsigned long long)(-v) : (unsigned long long)v;
+  l0 = (unsigned)(a & 0x3FFFFu);
+  l1 = (unsigned)((a >> 18) & 0x3FFFFu);
+  l2 = (unsigned)(a >> 36);
+}
+__device__ __forceinline__ int res_limbs(unsigned l0, unsigned l1, unsigned l2, bool neg, int t) {
+  const unsigned p = (unsigned)c_oz_p[t];
+  const unsigned sm = l2 * c_res.c2[t] + l1 * c_res.c1[t] + l0;  // < 2^26
+  unsigned r = sm - __umulhi(sm, c_res.m[t]) * p;                 // [0, 2p)
+  if (r >= p) r -= p;
+  int c = (int)r;
+  if (c > (int)(p >> 1)) c -= (int)p;
+  return neg ? -c : c;
 }
 
 // exponent shift that puts amax in [2^(KB-1), 2^KB); 0 for an all-zero line
@@ -301,11 +316,14 @@ __device__ __forceinline__ int oz_shift(double amax, int kb) { return amax > 0.0
 // skew-Hermitian S (B[j][k] = S[k][j] = -conj(S[j][k]) off the diagonal):
 // planes (re, im) of that.  One block per padded row; 4 consecutive k per
 // thread (one 32-bit store per plane).
+// mode 2: both at once from one read (A planes into out, skew-B planes into
+// out2; the row scale is shared since |-conj(v)| = |v|).
 __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __restrict__ src, int64_t ld, int mp,
                                                       int kp, int nmod, int kb, int mode, int8_t* out,
-                                                      int* __restrict__ shift) {
+                                                      int* __restrict__ shift, int8_t* out2 = nullptr,
+                                                      int* __restrict__ shift2 = nullptr) {
   const int i = blockIdx.x;
-  const int nplanes = mode == 0 ? 3 : 2;
+  const int nplanes = mode == 1 ? 2 : 3;
   __shared__ double red[8];
   double amax = 0.0;
   if (i < n)
@@ -320,8 +338,10 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
   for (int q = 1; q < 8; ++q) amax = fmax(amax, red[q]);
   const int sh = oz_shift(amax, kb);
   if (threadIdx.x == 0 && shift) shift[i] = sh;
+  if (threadIdx.x == 0 && shift2) shift2[i] = sh;
   for (int k0 = threadIdx.x * 4; k0 < kp; k0 += blockDim.x * 4) {
-    double xr[4], xi[4];
+    unsigned a0[8], a1[8], a2[8];
+    bool ng[8];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int k = k0 + e;
@@ -330,24 +350,35 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
         v = ld2(src + ((size_t)i * ld + k) * 2);
         if (mode == 1 && k != i) v = make_double2(-v.x, v.y);
       }
-      xr[e] = rint(ldexp(v.x, sh));
-      xi[e] = rint(ldexp(v.y, sh));
+      limbs(rint(ldexp(v.x, sh)), a0[e], a1[e], a2[e], ng[e]);
+      limbs(rint(ldexp(v.y, sh)), a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e]);
     }
-    for (int j = 0; j < nmod; ++j) {
-      const int p = c_oz_p[j];
-      const double invp = 1.0 / (double)p;
+    for (int t = 0; t < nmod; ++t) {
       uint32_t wr = 0, wi = 0, wn = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int8_t rr = res8(xr[e], p, invp), ri = res8(xi[e], p, invp);
-        wr |= (uint32_t)(uint8_t)rr << (8 * e);
-        wi |= (uint32_t)(uint8_t)ri << (8 * e);
+        const int rr = res_limbs(a0[e], a1[e], a2[e], ng[e], t);
+        const int ri = res_limbs(a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e], t);
+        wr |= (uint32_t)(uint8_t)(int8_t)rr << (8 * e);
+        wi |= (uint32_t)(uint8_t)(int8_t)ri << (8 * e);
         wn |= (uint32_t)(uint8_t)(int8_t)(-ri) << (8 * e);
       }
-      int8_t* base = out + ((size_t)(j * nplanes) * mp + i) * kp + k0;
+      int8_t* base = out + ((size_t)(t * nplanes) * mp + i) * kp + k0;
       *reinterpret_cast<uint32_t*>(base) = wr;
       *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
       if (nplanes == 3) *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
+      if (mode == 2) {
+        // skew-B layout: -re off the diagonal, re on it; im unchanged
+        uint32_t wb = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int rr = (int)(int8_t)(wr >> (8 * e));
+          wb |= (uint32_t)(uint8_t)(int8_t)(k0 + e == i ? rr : -rr) << (8 * e);
+        }
+        int8_t* b2 = out2 + ((size_t)(t * 2) * mp + i) * kp + k0;
+        *reinterpret_cast<uint32_t*>(b2) = wb;
+        *reinterpret_cast<uint32_t*>(b2 + (size_t)mp * kp) = wi;
+      }
     }
   }
 }
@@ -366,119 +397,141 @@ __global__ void __launch_bounds__(256) k_oz_colmax(int n, const double* __restri
   atomicMax(colmax + j, (unsigned long long)__double_as_longlong(m));
 }
 
-// then 32 (k) x 32 (j) tiles through shared memory, residues written as
-// rows j of 32 consecutive k
+// then 32 (k) x 32 (j) tiles through shared memory; thread t produces output
+// row j = j0 + t / 8, k = k0 + 4 (t % 8) .. +3 (one 32-bit store per plane)
 __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __restrict__ x, int64_t ld, int np,
                                                       int kp, int nmod, int kb,
                                                       const unsigned long long* __restrict__ colmax, int8_t* out,
                                                       int* __restrict__ shift) {
-  __shared__ double tr[32][33], ti[32][33];
-  __shared__ int8_t rb[2][32][36];
+  __shared__ double2 tl[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r, j = j0 + tx;
-    double2 v = make_double2(0.0, 0.0);
-    if (k < n && j < n) v = ld2(x + ((size_t)k * ld + j) * 2);
-    tr[r][tx] = v.x;
-    ti[r][tx] = v.y;
+    tl[r][tx] = (k < n && j < n) ? ld2(x + ((size_t)k * ld + j) * 2) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  // thread (ty, tx): output row j = j0 + r (r = ty + 8 q), k = k0 + tx
-  for (int q = 0; q < 4; ++q) {
-    const int r = ty + 8 * q, j = j0 + r;
-    const double m = (j < n) ? __longlong_as_double((long long)colmax[j]) : 0.0;
-    const int sh = oz_shift(m, kb);
-    if (blockIdx.y == 0 && tx == 0 && shift && j < np) shift[j] = sh;
-    const double xr = rint(ldexp(tr[tx][r], sh)), xi = rint(ldexp(ti[tx][r], sh));
-    for (int t = 0; t < nmod; ++t) {
-      const int p = c_oz_p[t];
-      const double invp = 1.0 / (double)p;
-      int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + tx;
-      base[0] = res8(xr, p, invp);
-      base[(size_t)np * kp] = res8(xi, p, invp);
+  const int jj = threadIdx.x >> 3, kk = (threadIdx.x & 7) * 4;
+  const int j = j0 + jj;
+  const double m = (j < n) ? __longlong_as_double((long long)colmax[j]) : 0.0;
+  const int sh = oz_shift(m, kb);
+  if (blockIdx.y == 0 && kk == 0 && shift) shift[j] = sh;
+  unsigned a0[8], a1[8], a2[8];
+  bool ng[8];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double2 v = tl[kk + e][jj];
+    limbs(rint(ldexp(v.x, sh)), a0[e], a1[e], a2[e], ng[e]);
+    limbs(rint(ldexp(v.y, sh)), a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e]);
+  }
+  for (int t = 0; t < nmod; ++t) {
+    uint32_t wr = 0, wi = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      wr |= (uint32_t)(uint8_t)(int8_t)res_limbs(a0[e], a1[e], a2[e], ng[e], t) << (8 * e);
+      wi |= (uint32_t)(uint8_t)(int8_t)res_limbs(a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e], t) << (8 * e);
     }
+    int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + kk;
+    *reinterpret_cast<uint32_t*>(base) = wr;
+    *reinterpret_cast<uint32_t*>(base + (size_t)np * kp) = wi;
   }
 }
 
 // ---------------------------------------------------------------------------
-// Reconstruction: the exact integer from its residues (CRT in 128-bit
-// integers), centred, times 2^-(row shift + column shift).
+// Reconstruction (CRT): x = sum_t u_t M_t mod M with u_t = r_t y_t mod p_t,
+// M_t = M / p_t, y_t = M_t^-1 mod p_t.  Every M_t (and M) is split into three
+// pieces on the grids 2^0, 2^40, 2^80 (<= 41 bits each), so each partial sum
+// S_k = sum_t u_t M_t,k is exact in binary64 (7 + 41 + log2(18) < 53 bits);
+// q = round(S / M) and D_k = S_k - q M_k are exact too, and x = D_2 + D_1 + D_0
+// is the centred representative (|x| << M / 2 by the choice of KB).
 // ---------------------------------------------------------------------------
 struct CrtConst {
-  unsigned long long mt_lo[OZ_NMOD], mt_hi[OZ_NMOD];  // M / p_t
-  int y[OZ_NMOD];                                     // (M / p_t)^-1 mod p_t
-  unsigned long long m_lo, m_hi;                      // M
-  double m_dbl;
+  double mt[OZ_NMOD][3];  // pieces of M_t
+  double mp[3];           // pieces of M
+  double m_inv;           // 1 / M
+  unsigned char u[OZ_NMOD][129];  // (r y_t) mod p_t for centred r in [-64, 64]
 };
 __constant__ CrtConst c_crt;
 
-__device__ __forceinline__ double crt_value(const int8_t* r, size_t plane_stride, int nmod) {
-  typedef unsigned __int128 u128;
-  u128 s = 0;
-  for (int t = 0; t < nmod; ++t) {
-    const int p = c_oz_p[t];
-    int v = r[(size_t)t * plane_stride];
-    v = (v % p + p) % p;
-    const int u = (v * c_crt.y[t]) % p;
-    const u128 mt = ((u128)c_crt.mt_hi[t] << 64) | c_crt.mt_lo[t];
-    s += (u128)(unsigned)u * mt;
-  }
-  const u128 m = ((u128)c_crt.m_hi << 64) | c_crt.m_lo;
-  // s < nmod * M: reduce with an estimated quotient, then correct
-  const double sd = (double)(unsigned long long)(s >> 64) * 18446744073709551616.0 + (double)(unsigned long long)s;
-  long long q = (long long)(sd / c_crt.m_dbl);
-  u128 qm = (u128)(unsigned long long)q * m;
-  while (qm > s) {
-    qm -= m;
-    --q;
-  }
-  u128 x = s - qm;
-  while (x >= m) x -= m;
-  // centre: x in [0, M) -> (-M/2, M/2]
-  const bool neg = x > (m >> 1);
-  const u128 mag = neg ? m - x : x;
-  const double hi = (double)(unsigned long long)(mag >> 64), lo = (double)(unsigned long long)mag;
-  const double v = fma(hi, 18446744073709551616.0, lo);
-  return neg ? -v : v;
-}
-
-// C (complex128, ldc) = residue product scaled back; lower: only 128-tiles on
-// or below the diagonal.  4 consecutive columns per thread.
 __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
                                                   int np, const int* __restrict__ rs, const int* __restrict__ cs,
                                                   double* c, int64_t ldc, int lower) {
+  __shared__ unsigned char ut[OZ_NMOD][129];
+  for (int q = threadIdx.x; q < OZ_NMOD * 129; q += blockDim.x) (&ut[0][0])[q] = (&c_crt.u[0][0])[q];
+  __syncthreads();
   const int i = blockIdx.y;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x);
-  if (i >= m || j >= n) return;
-  if (lower && (j >> 7) > (i >> 7)) return;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= m || j0 >= n) return;
+  if (lower && (j0 >> 7) > (i >> 7)) return;
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
-  const int8_t* re = r + (size_t)i * np + j;
-  const double vr = crt_value(re, ps, nmod), vi = crt_value(re + (size_t)mp * np, ps, nmod);
-  const int sh = -(rs[i] + cs[j]);
-  st2(c + ((size_t)i * ldc + j) * 2, make_double2(ldexp(vr, sh), ldexp(vi, sh)));
+  const int8_t* rre = r + (size_t)i * np + j0;
+  const int8_t* rim = rre + (size_t)mp * np;
+  double s[8][3];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s[e][0] = s[e][1] = s[e][2] = 0.0;
+  for (int t = 0; t < nmod; ++t) {
+    const uint32_t wr = __ldg(reinterpret_cast<const uint32_t*>(rre + (size_t)t * ps));
+    const uint32_t wi = __ldg(reinterpret_cast<const uint32_t*>(rim + (size_t)t * ps));
+    const double m0 = c_crt.mt[t][0], m1 = c_crt.mt[t][1], m2 = c_crt.mt[t][2];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int rv = (int)(int8_t)((e < 4 ? wr : wi) >> (8 * (e & 3)));
+      const double u = (double)ut[t][rv + 64];
+      s[e][0] = fma(u, m0, s[e][0]);
+      s[e][1] = fma(u, m1, s[e][1]);
+      s[e][2] = fma(u, m2, s[e][2]);
+    }
+  }
+  double vr[4], vi[4];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const double q = rint((s[e][2] + s[e][1] + s[e][0]) * c_crt.m_inv);
+    const double d2 = fma(-q, c_crt.mp[2], s[e][2]);
+    const double d1 = fma(-q, c_crt.mp[1], s[e][1]);
+    const double d0 = fma(-q, c_crt.mp[0], s[e][0]);
+    const double v = (d2 + d1) + d0;
+    if (e < 4)
+      vr[e] = v;
+    else
+      vi[e - 4] = v;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int j = j0 + e;
+    if (j < n && !(lower && (j >> 7) > (i >> 7))) {
+      const int sh = -(rs[i] + cs[j]);
+      st2(c + ((size_t)i * ldc + j) * 2, make_double2(ldexp(vr[e], sh), ldexp(vi[e], sh)));
+    }
+  }
 }
 
 static bool g_crt_ready = false;
 static int crt_init() {
   typedef unsigned __int128 u128;
   CrtConst h;
+  ResConst rc;
   u128 m = 1;
   for (int t = 0; t < OZ_NMOD; ++t) m *= (u128)h_oz_p[t];
+  auto piece = [](u128 v, int k) {
+    const u128 part = k < 2 ? (v >> (40 * k)) & (((u128)1 << 40) - 1) : (v >> 80);
+    return std::ldexp((double)(unsigned long long)part, 40 * k);  // <= 41 bits: exact
+  };
   for (int t = 0; t < OZ_NMOD; ++t) {
     const int p = h_oz_p[t];
     const u128 mt = m / (u128)p;
     const int r = (int)(mt % (u128)p);
     int y = 1;
     while ((r * y) % p != 1) ++y;  // p <= 128: direct search
-    h.mt_lo[t] = (unsigned long long)mt;
-    h.mt_hi[t] = (unsigned long long)(mt >> 64);
-    h.y[t] = y;
+    for (int k = 0; k < 3; ++k) h.mt[t][k] = piece(mt, k);
+    for (int v = -64; v <= 64; ++v) h.u[t][v + 64] = (unsigned char)((((v % p) + p) % p) * y % p);
+    rc.c1[t] = (unsigned)((1ull << 18) % (unsigned long long)p);
+    rc.c2[t] = (unsigned)((1ull << 36) % (unsigned long long)p);
+    rc.m[t] = (unsigned)((1ull << 32) / (unsigned long long)p);
   }
-  h.m_lo = (unsigned long long)m;
-  h.m_hi = (unsigned long long)(m >> 64);
-  h.m_dbl = (double)h.m_hi * 18446744073709551616.0 + (double)h.m_lo;
+  for (int k = 0; k < 3; ++k) h.mp[k] = piece(m, k);
+  h.m_inv = 1.0 / (h.mp[2] + h.mp[1] + h.mp[0]);
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_res, &rc, sizeof rc));
   g_crt_ready = true;
   return ZT_OK;
 }
@@ -531,10 +584,68 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   }
   int rc = oz_modgemm(OZ_NMOD, p, p, p, ares, bres, rres, lower, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 255) / 256, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc, lower);
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc, lower);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
+}
+
+int update_pairs(int n, const double* a, const double* bm, double* out, const double* base, const double* xprev,
+                 const double* wn, double hh, double qq, unsigned long long* resid, unsigned long long* cons,
+                 cudaStream_t st);
+int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
+
+size_t oz_update_workspace_bytes(int n) {
+  const size_t p = ((size_t)n + 127) / 128 * 128;
+  return (size_t)OZ_NMOD * p * p * (3 + 2 + 2 + 2) + 4 * p * sizeof(int) + p * 8 + 1024;
+}
+
+// One fixed-point update with both products on the INT8 tensor cores:
+// a = P X (P rows scaled; X columns scaled, transposed conversion), then
+// b = a P on the lower 128-tiles (a rows scaled; P as a skew-Hermitian B
+// operand from the same conversion pass as its A layout), then the update
+// pass.  gemm1_only: the step's final update W_{n+1} = W_n + h (a - a^H)
+// (out = x, h = hh; k_final_commutator).
+int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, const double* base,
+              const double* xprev, const double* wn, double* out, double hh, double qq, unsigned long long* resid,
+              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only) {
+  if (!g_crt_ready) {
+    const int rc = crt_init();
+    if (rc) return rc;
+  }
+  const int pd = (n + 127) / 128 * 128;
+  const int kb = oz_bits(n);
+  const size_t pl = (size_t)OZ_NMOD * pd * pd;
+  int8_t* ares = static_cast<int8_t*>(ws);
+  int8_t* bx = ares + 3 * pl;   // X as B operand
+  int8_t* bp = bx + 2 * pl;     // P as B operand
+  int8_t* rres = bp + 2 * pl;
+  int* sp = reinterpret_cast<int*>(rres + 2 * pl);  // P rows (= P-as-B columns)
+  int* sx = sp + pd;                                // X columns
+  int* sa = sx + pd;                                // a rows
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(sa + 2 * pd);
+  // P: A layout and skew-B layout in one pass
+  k_oz_conv_rows<<<pd, 256, 0, st>>>(n, p, n, pd, pd, OZ_NMOD, kb, gemm1_only ? 0 : 2, ares, sp,
+                                     gemm1_only ? nullptr : bp, nullptr);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pd, st));
+  k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, x, n, cmax);
+  ZT_LAUNCHED();
+  k_oz_conv_cols<<<dim3(pd / 32, pd / 32), 256, 0, st>>>(n, x, n, pd, pd, OZ_NMOD, kb, cmax, bx, sx);
+  ZT_LAUNCHED();
+  int rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bx, rres, 0, st);
+  if (rc) return rc;
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0);
+  ZT_LAUNCHED();
+  if (gemm1_only) return final_commutator(n, a, wn, hh, out, st);
+  k_oz_conv_rows<<<pd, 256, 0, st>>>(n, a, n, pd, pd, OZ_NMOD, kb, 0, ares, sa);
+  ZT_LAUNCHED();
+  rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bp, rres, 1, st);
+  if (rc) return rc;
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, pd, pd, sa, sp, bbuf, n, 1);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return update_pairs(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons, st);
 }
 
 static int g_oz_sms = 0;
