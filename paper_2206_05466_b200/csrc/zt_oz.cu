@@ -26,6 +26,7 @@ __constant__ int c_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
                                     103, 101, 97,  89,  83,  79,  73,  71,  67};
 static const int h_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
                                     103, 101, 97,  89,  83,  79,  73,  71,  67};
+__constant__ double c_oz_inv[OZ_NMOD];  // 1 / p (rounded)
 
 namespace oz {
 
@@ -285,28 +286,14 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
 // from 18-bit limbs of |x| in 32-bit integer arithmetic (Barrett reduction),
 // not from FP64 divisions.
 // ---------------------------------------------------------------------------
-struct ResConst {
-  unsigned c1[OZ_NMOD], c2[OZ_NMOD];  // 2^18 mod p, 2^36 mod p
-  unsigned m[OZ_NMOD];                // floor(2^32 / p)
-};
-__constant__ ResConst c_res;
-
-__device__ __forceinline__ void limbs(double x, unsigned& l0, unsigned& l1, unsigned& l2, bool& neg) {
-  const long long v = (long long)x;  // integer valued, |x| < 2^53
-  neg = v < 0;
-  const unsigned long long a = neg ? (unsigned long long)(-v) : (unsigned long long)v;
-  l0 = (unsigned)(a & 0x3FFFFu);
-  l1 = (unsigned)((a >> 18) & 0x3FFFFu);
-  l2 = (unsigned)(a >> 36);
-}
-__device__ __forceinline__ int res_limbs(unsigned l0, unsigned l1, unsigned l2, bool neg, int t) {
-  const unsigned p = (unsigned)c_oz_p[t];
-  const unsigned sm = l2 * c_res.c2[t] + l1 * c_res.c1[t] + l0;  // < 2^26
-  unsigned r = sm - __umulhi(sm, c_res.m[t]) * p;                 // [0, 2p)
-  if (r >= p) r -= p;
-  int c = (int)r;
-  if (c > (int)(p >> 1)) c -= (int)p;
-  return neg ? -c : c;
+// x integer valued, |x| < 2^53: q = rint(x / p) from the rounded reciprocal
+// (always floor or ceil of x / p), r = x - q p exactly (FMA), and the low
+// word of r + 1.5 * 2^52 is r in two's complement: |r| < 0.54 p <= 69
+constexpr double OZ_MAGIC = 6755399441055744.0;
+__device__ __forceinline__ uint32_t res_byte(double x, double p, double invp) {
+  const double q = fma(x, invp, OZ_MAGIC) - OZ_MAGIC;
+  const double r = fma(-q, p, x);
+  return (uint32_t)__double2loint(r + OZ_MAGIC) & 0xffu;
 }
 
 // exponent shift that puts amax in [2^(KB-1), 2^KB); 0 for an all-zero line
@@ -323,7 +310,6 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
                                                       int* __restrict__ shift, int8_t* out2 = nullptr,
                                                       int* __restrict__ shift2 = nullptr) {
   const int i = blockIdx.x;
-  const int nplanes = mode == 1 ? 2 : 3;
   __shared__ double red[8];
   double amax = 0.0;
   if (i < n)
@@ -340,42 +326,36 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
   if (threadIdx.x == 0 && shift) shift[i] = sh;
   if (threadIdx.x == 0 && shift2) shift2[i] = sh;
   for (int k0 = threadIdx.x * 4; k0 < kp; k0 += blockDim.x * 4) {
-    unsigned a0[8], a1[8], a2[8];
-    bool ng[8];
+    double xv[8];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int k = k0 + e;
       double2 v = make_double2(0.0, 0.0);
-      if (i < n && k < n) {
-        v = ld2(src + ((size_t)i * ld + k) * 2);
-        if (mode == 1 && k != i) v = make_double2(-v.x, v.y);
-      }
-      limbs(rint(ldexp(v.x, sh)), a0[e], a1[e], a2[e], ng[e]);
-      limbs(rint(ldexp(v.y, sh)), a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e]);
+      if (i < n && k < n) v = ld2(src + ((size_t)i * ld + k) * 2);
+      xv[e] = rint(ldexp(v.x, sh));
+      xv[4 + e] = rint(ldexp(v.y, sh));
     }
-    for (int t = 0; t < nmod; ++t) {
-      uint32_t wr = 0, wi = 0, wn = 0;
+#pragma unroll 2
+    for (int t = 0; t < OZ_NMOD; ++t) {
+      const double p = (double)c_oz_p[t], invp = c_oz_inv[t];
+      uint32_t wr = 0, wi = 0, wn = 0, wb = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int rr = res_limbs(a0[e], a1[e], a2[e], ng[e], t);
-        const int ri = res_limbs(a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e], t);
-        wr |= (uint32_t)(uint8_t)(int8_t)rr << (8 * e);
-        wi |= (uint32_t)(uint8_t)(int8_t)ri << (8 * e);
-        wn |= (uint32_t)(uint8_t)(int8_t)(-ri) << (8 * e);
+        const uint32_t rr = res_byte(xv[e], p, invp), ri = res_byte(xv[4 + e], p, invp);
+        wr |= rr << (8 * e);
+        wi |= ri << (8 * e);
+        wn |= ((0x100u - ri) & 0xffu) << (8 * e);
+        // skew-B layout (modes 1, 2): -re off the diagonal, re on it
+        wb |= ((k0 + e == i) ? rr : ((0x100u - rr) & 0xffu)) << (8 * e);
       }
-      int8_t* base = out + ((size_t)(t * nplanes) * mp + i) * kp + k0;
-      *reinterpret_cast<uint32_t*>(base) = wr;
-      *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
-      if (nplanes == 3) *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
-      if (mode == 2) {
-        // skew-B layout: -re off the diagonal, re on it; im unchanged
-        uint32_t wb = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int rr = (int)(int8_t)(wr >> (8 * e));
-          wb |= (uint32_t)(uint8_t)(int8_t)(k0 + e == i ? rr : -rr) << (8 * e);
-        }
-        int8_t* b2 = out2 + ((size_t)(t * 2) * mp + i) * kp + k0;
+      if (mode != 1) {
+        int8_t* base = out + ((size_t)(t * 3) * mp + i) * kp + k0;
+        *reinterpret_cast<uint32_t*>(base) = wr;
+        *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
+        *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
+      }
+      if (mode != 0) {
+        int8_t* b2 = (mode == 1 ? out : out2) + ((size_t)(t * 2) * mp + i) * kp + k0;
         *reinterpret_cast<uint32_t*>(b2) = wb;
         *reinterpret_cast<uint32_t*>(b2 + (size_t)mp * kp) = wi;
       }
@@ -416,20 +396,21 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
   const double m = (j < n) ? __longlong_as_double((long long)colmax[j]) : 0.0;
   const int sh = oz_shift(m, kb);
   if (blockIdx.y == 0 && kk == 0 && shift) shift[j] = sh;
-  unsigned a0[8], a1[8], a2[8];
-  bool ng[8];
+  double xv[8];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const double2 v = tl[kk + e][jj];
-    limbs(rint(ldexp(v.x, sh)), a0[e], a1[e], a2[e], ng[e]);
-    limbs(rint(ldexp(v.y, sh)), a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e]);
+    xv[e] = rint(ldexp(v.x, sh));
+    xv[4 + e] = rint(ldexp(v.y, sh));
   }
-  for (int t = 0; t < nmod; ++t) {
+#pragma unroll 2
+  for (int t = 0; t < OZ_NMOD; ++t) {
+    const double p = (double)c_oz_p[t], invp = c_oz_inv[t];
     uint32_t wr = 0, wi = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      wr |= (uint32_t)(uint8_t)(int8_t)res_limbs(a0[e], a1[e], a2[e], ng[e], t) << (8 * e);
-      wi |= (uint32_t)(uint8_t)(int8_t)res_limbs(a0[4 + e], a1[4 + e], a2[4 + e], ng[4 + e], t) << (8 * e);
+      wr |= res_byte(xv[e], p, invp) << (8 * e);
+      wi |= res_byte(xv[4 + e], p, invp) << (8 * e);
     }
     int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + kk;
     *reinterpret_cast<uint32_t*>(base) = wr;
@@ -438,27 +419,32 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
 }
 
 // ---------------------------------------------------------------------------
-// Reconstruction (CRT): x = sum_t u_t M_t mod M with u_t = r_t y_t mod p_t,
-// M_t = M / p_t, y_t = M_t^-1 mod p_t.  Every M_t (and M) is split into three
-// pieces on the grids 2^0, 2^40, 2^80 (<= 41 bits each), so each partial sum
-// S_k = sum_t u_t M_t,k is exact in binary64 (7 + 41 + log2(18) < 53 bits);
-// q = round(S / M) and D_k = S_k - q M_k are exact too, and x = D_2 + D_1 + D_0
-// is the centred representative (|x| << M / 2 by the choice of KB).
+// Reconstruction (CRT): x = sum_t r_t W_t mod M with W_t = y_t M_t,
+// M_t = M / p_t, y_t = M_t^-1 mod p_t (r_t need not be reduced: a multiple
+// of p_t times M_t is a multiple of M).  W_t (< M < 2^121) and M are split
+// into three pieces on the grids 2^0, 2^40, 2^80 (<= 41 bits), so each
+// partial sum S_k = sum_t r_t W_t,k is exact in binary64 (|r_t| <= 69:
+// 7 + 41 + log2(18) < 53 bits); q = rint(S / M) (|q| < 2^11) and
+// D_k = S_k - q M_k are exact, and x = D_2 + D_1 + D_0 is the centred
+// representative (|x| << M / 2 by the choice of KB).
 // ---------------------------------------------------------------------------
 struct CrtConst {
-  double mt[OZ_NMOD][3];  // pieces of M_t
-  double mp[3];           // pieces of M
-  double m_inv;           // 1 / M
-  unsigned char u[OZ_NMOD][129];  // (r y_t) mod p_t for centred r in [-64, 64]
+  double w[OZ_NMOD][3];  // pieces of W_t
+  double mp[3];          // pieces of M
+  double m_inv;          // 1 / M
 };
 __constant__ CrtConst c_crt;
+
+// int8 (two's complement byte) -> double without an int -> fp64 conversion:
+// 2^52 + 2^31 + v as the bit pattern, minus the bias
+__device__ __forceinline__ double byte_to_double(uint32_t word, int e) {
+  const int v = (int)(int8_t)(word >> (8 * e));
+  return __hiloint2double(0x43300000, (int)((unsigned)v ^ 0x80000000u)) - 4503601774854144.0;
+}
 
 __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
                                                   int np, const int* __restrict__ rs, const int* __restrict__ cs,
                                                   double* c, int64_t ldc, int lower) {
-  __shared__ unsigned char ut[OZ_NMOD][129];
-  for (int q = threadIdx.x; q < OZ_NMOD * 129; q += blockDim.x) (&ut[0][0])[q] = (&c_crt.u[0][0])[q];
-  __syncthreads();
   const int i = blockIdx.y;
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= m || j0 >= n) return;
@@ -466,20 +452,24 @@ __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const 
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
   const int8_t* rre = r + (size_t)i * np + j0;
   const int8_t* rim = rre + (size_t)mp * np;
+  uint32_t wr[OZ_NMOD], wi[OZ_NMOD];
+#pragma unroll
+  for (int t = 0; t < OZ_NMOD; ++t) {
+    wr[t] = __ldg(reinterpret_cast<const uint32_t*>(rre + (size_t)t * ps));
+    wi[t] = __ldg(reinterpret_cast<const uint32_t*>(rim + (size_t)t * ps));
+  }
   double s[8][3];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s[e][0] = s[e][1] = s[e][2] = 0.0;
-  for (int t = 0; t < nmod; ++t) {
-    const uint32_t wr = __ldg(reinterpret_cast<const uint32_t*>(rre + (size_t)t * ps));
-    const uint32_t wi = __ldg(reinterpret_cast<const uint32_t*>(rim + (size_t)t * ps));
-    const double m0 = c_crt.mt[t][0], m1 = c_crt.mt[t][1], m2 = c_crt.mt[t][2];
+#pragma unroll
+  for (int t = 0; t < OZ_NMOD; ++t) {
+    const double w0 = c_crt.w[t][0], w1 = c_crt.w[t][1], w2 = c_crt.w[t][2];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int rv = (int)(int8_t)((e < 4 ? wr : wi) >> (8 * (e & 3)));
-      const double u = (double)ut[t][rv + 64];
-      s[e][0] = fma(u, m0, s[e][0]);
-      s[e][1] = fma(u, m1, s[e][1]);
-      s[e][2] = fma(u, m2, s[e][2]);
+      const double u = byte_to_double(e < 4 ? wr[t] : wi[t], e & 3);
+      s[e][0] = fma(u, w0, s[e][0]);
+      s[e][1] = fma(u, w1, s[e][1]);
+      s[e][2] = fma(u, w2, s[e][2]);
     }
   }
   double vr[4], vi[4];
@@ -505,11 +495,11 @@ __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const 
   }
 }
 
+constexpr int OZ_RECON_SMEM = 0;
 static bool g_crt_ready = false;
 static int crt_init() {
   typedef unsigned __int128 u128;
   CrtConst h;
-  ResConst rc;
   u128 m = 1;
   for (int t = 0; t < OZ_NMOD; ++t) m *= (u128)h_oz_p[t];
   auto piece = [](u128 v, int k) {
@@ -522,16 +512,15 @@ static int crt_init() {
     const int r = (int)(mt % (u128)p);
     int y = 1;
     while ((r * y) % p != 1) ++y;  // p <= 128: direct search
-    for (int k = 0; k < 3; ++k) h.mt[t][k] = piece(mt, k);
-    for (int v = -64; v <= 64; ++v) h.u[t][v + 64] = (unsigned char)((((v % p) + p) % p) * y % p);
-    rc.c1[t] = (unsigned)((1ull << 18) % (unsigned long long)p);
-    rc.c2[t] = (unsigned)((1ull << 36) % (unsigned long long)p);
-    rc.m[t] = (unsigned)((1ull << 32) / (unsigned long long)p);
+    const u128 w = mt * (u128)y;  // < M
+    for (int k = 0; k < 3; ++k) h.w[t][k] = piece(w, k);
   }
   for (int k = 0; k < 3; ++k) h.mp[k] = piece(m, k);
   h.m_inv = 1.0 / (h.mp[2] + h.mp[1] + h.mp[0]);
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
-  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_res, &rc, sizeof rc));
+  double inv[OZ_NMOD];
+  for (int t = 0; t < OZ_NMOD; ++t) inv[t] = 1.0 / (double)h_oz_p[t];
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_inv, inv, sizeof inv));
   g_crt_ready = true;
   return ZT_OK;
 }
@@ -584,7 +573,8 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   }
   int rc = oz_modgemm(OZ_NMOD, p, p, p, ares, bres, rres, lower, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc, lower);
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc,
+                                                                       lower);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -635,14 +625,15 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   ZT_LAUNCHED();
   int rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bx, rres, 0, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0);
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0);
   ZT_LAUNCHED();
   if (gemm1_only) return final_commutator(n, a, wn, hh, out, st);
   k_oz_conv_rows<<<pd, 256, 0, st>>>(n, a, n, pd, pd, OZ_NMOD, kb, 0, ares, sa);
   ZT_LAUNCHED();
   rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bp, rres, 1, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, 0, st>>>(n, n, OZ_NMOD, rres, pd, pd, sa, sp, bbuf, n, 1);
+  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, pd, pd, sa, sp, bbuf, n,
+                                                                       1);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return update_pairs(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons, st);
