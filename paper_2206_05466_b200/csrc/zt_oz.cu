@@ -30,9 +30,17 @@ __constant__ double c_oz_inv[OZ_NMOD];  // 1 / p (rounded)
 
 namespace oz {
 
-constexpr int TM = 128, TN = 128, TK = 128;  // TK in bytes
-constexpr int TILE_BYTES = 128 * TK;         // one 128 x 128 int8 tile
-constexpr int STAGE_BYTES = 5 * TILE_BYTES;  // A re, im, -im; B re, im
+#ifndef OZ_TN
+#define OZ_TN 256
+#endif
+// 128 x TN output tiles: TN = 256 halves the B-operand L2 traffic per MMA
+// (the kernel is L2-bandwidth bound at TN = 128) at the price of a single
+// TMEM accumulator buffer (Re + Im = 2 TN columns of 512)
+constexpr int TM = 128, TN = OZ_TN, TK = 128;  // TK in bytes
+constexpr int NBUF = 512 / (2 * TN);          // TMEM accumulator buffers
+constexpr int TILE_BYTES = 128 * TK;          // one 128-row int8 tile (A)
+constexpr int B_TILE_BYTES = TN * TK;
+constexpr int STAGE_BYTES = 3 * TILE_BYTES + 2 * B_TILE_BYTES;  // A re, im, -im; B re, im
 constexpr int STAGES = 2;
 constexpr int THREADS = 6 * 32;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
@@ -81,22 +89,29 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
       : "r"(addr))
 
 struct GemmArgs {
-  int nmod, mt, nt, kt;  // tiles per dimension (128) and K blocks (128 B)
-  int lower;             // square: only tiles tm >= tn
+  int nmod, mt, nt, kt;  // tiles per dimension (128 rows, TN columns) and K blocks (128 B)
+  int lower;             // square: only tiles meeting the lower 128-block triangle
   int mp, np;            // padded M, N (output leading dimension np)
   int8_t* r;             // [nmod][2][mp][np]
 };
 
-__device__ __forceinline__ void work_of(const GemmArgs& g, int w, int& j, int& tm, int& tn) {
-  const int per = g.lower ? g.mt * (g.mt + 1) / 2 : g.mt * g.nt;
+// lower mode: tile (tm, tn) is needed iff its columns reach 128-block tm,
+// i.e. tn * TN / 128 <= tm
+__host__ __device__ __forceinline__ int lower_count(int mt) {
+  int c = 0;
+  for (int tm = 0; tm < mt; ++tm) c += tm * TM / TN + 1;
+  return c;
+}
+__device__ __forceinline__ void work_of(const GemmArgs& g, int w, int per, int& j, int& tm, int& tn) {
   j = w / per;
   int t = w - j * per;
   if (g.lower) {
-    int c = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((c + 1) * (c + 2) / 2 <= t) ++c;
-    while (c * (c + 1) / 2 > t) --c;
-    tm = c;
-    tn = t - c * (c + 1) / 2;
+    tm = 0;
+    while (t >= tm * TM / TN + 1) {
+      t -= tm * TM / TN + 1;
+      ++tm;
+    }
+    tn = t;
   } else {
     tm = t % g.mt;
     tn = t / g.mt;
@@ -117,10 +132,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = g.lower ? g.mt * (g.mt + 1) / 2 : g.mt * g.nt;
+  const int per = g.lower ? lower_count(g.mt) : g.mt * g.nt;
   const int total = g.nmod * per;
 
   if (threadIdx.x == 0) {
@@ -128,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NBUF; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);
     }
@@ -151,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned it = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         int j, tm, tn;
-        work_of(g, w, j, tm, tn);
+        work_of(g, w, per, j, tm, tn);
         const int ra = (j * 3) * g.mp + tm * TM, rb = (j * 2) * g.np + tn * TN;
         for (int kb = 0; kb < g.kt; ++kb, ++it) {
           const int s = it % STAGES;
@@ -162,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma2d(st + TILE_BYTES, &ma, kb * TK, ra + g.mp, &full[s]);
           tma2d(st + 2 * TILE_BYTES, &ma, kb * TK, ra + 2 * g.mp, &full[s]);
           tma2d(st + 3 * TILE_BYTES, &mb, kb * TK, rb, &full[s]);
-          tma2d(st + 4 * TILE_BYTES, &mb, kb * TK, rb + g.np, &full[s]);
+          tma2d(st + 3 * TILE_BYTES + B_TILE_BYTES, &mb, kb * TK, rb + g.np, &full[s]);
         }
       }
     }
@@ -170,17 +185,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       unsigned it = 0, lt = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x, ++lt) {
-        const int ab = lt & 1;
-        mbar_wait(&tempty[ab], ((lt >> 1) & 1) ^ 1);
+        const int ab = lt % NBUF;
+        mbar_wait(&tempty[ab], ((lt / NBUF) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t dre = tmem + ab * 256, dim = dre + 128;
+        const uint32_t dre = tmem + ab * 2 * TN, dim = dre + TN;
         for (int kb = 0; kb < g.kt; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t are = base, aim = base + TILE_BYTES, anim = base + 2 * TILE_BYTES;
-          const uint32_t bre = base + 3 * TILE_BYTES, bim = base + 4 * TILE_BYTES;
+          const uint32_t bre = base + 3 * TILE_BYTES, bim = bre + B_TILE_BYTES;
 #pragma unroll
           for (int k = 0; k < TK / 32; ++k) {
             const uint32_t first = (kb | k) ? 1u : 0u;
@@ -200,9 +215,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned lt = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++lt) {
       int j, tm, tn;
-      work_of(g, w, j, tm, tn);
-      const int ab = lt & 1;
-      mbar_wait(&tfull[ab], (lt >> 1) & 1);
+      work_of(g, w, per, j, tm, tn);
+      const int ab = lt % NBUF;
+      mbar_wait(&tfull[ab], (lt / NBUF) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int p = c_oz_p[j];
       const double invp = 1.0 / (double)p;
@@ -212,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < TN; c0 += 32) {
         uint32_t v[32];
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + c0;
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ab * 2 * TN + c0;
         OZ_LD32(v, ta);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         uint32_t pk[8];
@@ -226,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint4* d = reinterpret_cast<uint4*>(rre + c0);
         d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        OZ_LD32(v, ta + 128);
+        OZ_LD32(v, ta + TN);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -253,7 +268,7 @@ using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, vo
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols) {
+static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols, int box_rows) {
   static encode_fn fn = nullptr;
   if (!fn) {
     void* f = nullptr;
@@ -264,7 +279,7 @@ static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols};
-  cuuint32_t box[2] = {TK, 128};
+  cuuint32_t box[2] = {TK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -534,7 +549,7 @@ static int oz_bits(int k) {
 }
 
 size_t oz_workspace_bytes(int n) {
-  const size_t p = ((size_t)n + 127) / 128 * 128;
+  const size_t p = ((size_t)n + 255) / 256 * 256;
   return (size_t)OZ_NMOD * p * p * (3 + 2 + 2) + 2 * p * sizeof(int) + p * 8 + 1024;
 }
 
@@ -550,7 +565,7 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
     const int rc = crt_init();
     if (rc) return rc;
   }
-  const int p = (n + 127) / 128 * 128;
+  const int p = (n + 255) / 256 * 256;
   const int kb = oz_bits(n);
   int8_t* ares = static_cast<int8_t*>(ws);
   int8_t* bres = ares + (size_t)OZ_NMOD * 3 * p * p;
@@ -586,7 +601,7 @@ int update_pairs(int n, const double* a, const double* bm, double* out, const do
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 
 size_t oz_update_workspace_bytes(int n) {
-  const size_t p = ((size_t)n + 127) / 128 * 128;
+  const size_t p = ((size_t)n + 255) / 256 * 256;
   return (size_t)OZ_NMOD * p * p * (3 + 2 + 2 + 2) + 4 * p * sizeof(int) + p * 8 + 1024;
 }
 
@@ -603,7 +618,7 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
     const int rc = crt_init();
     if (rc) return rc;
   }
-  const int pd = (n + 127) / 128 * 128;
+  const int pd = (n + 255) / 256 * 256;
   const int kb = oz_bits(n);
   const size_t pl = (size_t)OZ_NMOD * pd * pd;
   int8_t* ares = static_cast<int8_t*>(ws);
@@ -645,11 +660,11 @@ static int g_oz_sms = 0;
 int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* b, int8_t* r, int lower,
                cudaStream_t st) {
   using namespace oz;
-  if (nmod < 1 || nmod > OZ_NMOD || mp % 128 || np % 128 || kp % 128 || (lower && mp != np))
+  if (nmod < 1 || nmod > OZ_NMOD || mp % TM || np % TN || kp % TK || (lower && mp != np))
     return fail(ZT_EINVAL, "oz_modgemm: bad shape");
   CUtensorMap ma, mb;
-  int rc = map_i8(&ma, a, (long long)nmod * 3 * mp, kp);
-  if (!rc) rc = map_i8(&mb, b, (long long)nmod * 2 * np, kp);
+  int rc = map_i8(&ma, a, (long long)nmod * 3 * mp, kp, TM);
+  if (!rc) rc = map_i8(&mb, b, (long long)nmod * 2 * np, kp, TN);
   if (rc) return rc;
   if (!g_oz_sms) {
     int dev;
@@ -666,7 +681,7 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   g.mp = mp;
   g.np = np;
   g.r = r;
-  const int per = lower ? g.mt * (g.mt + 1) / 2 : g.mt * g.nt;
+  const int per = lower ? lower_count(g.mt) : g.mt * g.nt;
   const int grid = std::min(nmod * per, g_oz_sms);
   k_oz_gemm<<<grid, THREADS, SMEM, st>>>(ma, mb, g);
   ZT_LAUNCHED();
