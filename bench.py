@@ -188,6 +188,18 @@ def load_fp64_peak():
                           if best else "nominal 148 SM x 128 flop/clk x 1.965 GHz")
 
 
+def load_int8_peak():
+    """Measured INT8 tensor-core peak (profiles/r01_int8_peaks.json, cuBLASLt
+    int8 GEMM at 8192^3): the sustained figure, since the residue GEMM is timed
+    inside long steps under the power cap; MEASURED_PEAKS.json has no int8."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_int8_peaks.json")))
+        return d["sustained_tops"], ("measured: cuBLASLt int8 GEMM 8192^3 back to back for 4 s (sustained), "
+                                     "profiles/r01_int8_peaks.json (burst %.0f TOPS)" % d["burst_tops"])
+    except (OSError, KeyError, ValueError):
+        return 2 * 1415.7, "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 = 2 x bf16 rate)"
+
+
 def run_sharded(args):
     """Row-block sharded step (paper_2206_05466_b200/sharded.py): the same cfg
     workload split over the ranks (strong scaling); collectives fused into the
@@ -424,6 +436,10 @@ def run_ours(args):
         ems = float(t.item())
     e2e_value = world * e2e_steps / (ems / 1e3)
 
+    oz_ms = (ctypes.c_double * 2)()
+    oz_cnt = (ctypes.c_longlong * 2)()
+    lib.zt_oz_profile_read(ctypes.cast(oz_ms, ctypes.c_void_p), ctypes.cast(oz_cnt, ctypes.c_void_p), 1)
+    oz = oz_cnt[0] > 0
     # ---- roofline of the dominant kernel: the fused update k_zupdate<3M>
     # (GEMM-1 a = P X on all tiles + GEMM-2 b = a P on lower tiles + update
     # epilogue), timed by CUDA events around every launch in the timed region
@@ -466,6 +482,44 @@ def run_ours(args):
         "step_alg_flop": 16.0 * N**3 * (statistics.mean(iters) + 1),
         "step_TFLOPs_alg": 16.0 * N**3 * (statistics.mean(iters) + 1) / (ms_per_step * 1e-3) / 1e12,
     }
+    if oz:
+        # dominant kernel: the residue GEMM k_oz_gemm (tcgen05 kind::i8)
+        ipeak, ipeak_src = load_int8_peak()
+        pd = (N + 255) // 256 * 256
+        mt, nt = pd // 128, pd // 256
+        low = sum(tm * 128 // 256 + 1 for tm in range(mt)) / (mt * nt)
+        nmod = 18
+        ops_full = nmod * 4 * 2.0 * pd**3          # 4M: four int8 products per modulus
+        full_ms = oz_ms[0] / oz_cnt[0]
+        low_ms = oz_ms[1] / max(1, oz_cnt[1])
+        achieved_i8 = ops_full / (full_ms * 1e-3) / 1e12
+        roofline = {
+            "bound": "tensor",
+            "kernel": "k_oz_gemm: 18-modulus int8 residue GEMM of the FP64-accurate complex product "
+                      "a = P X (Ozaki scheme II on tcgen05 kind::i8, TMEM accumulators)",
+            "achieved": achieved_i8, "peak": ipeak, "unit": "TFLOP/s", "frac": achieved_i8 / ipeak,
+            "op_type": "int8 tensor-core ops (2 per MAC), counted like NVIDIA TOPS",
+            "traffic": TRAFFIC_OZ,
+            "peak_source": ipeak_src,
+            "ops_per_launch": ops_full, "avg_launch_ms": full_ms,
+            "lower_launch_ms": low_ms, "lower_tile_fraction": low,
+            "fp64_equivalent": {
+                "algorithmic_flop_per_product": 8.0 * N**3,
+                "TF_per_product": 8.0 * N**3 / (full_ms * 1e-3) / 1e12,
+                "dmma_peak_TF": peak, "vs_dmma_peak": 8.0 * N**3 / (full_ms * 1e-3) / 1e12 / peak,
+            },
+            "full_update_avg_ms": g1_ms, "final_update_avg_ms": g2_ms,
+            "solve_avg_ms": sv_ms, "solve_alg_bytes": 24.0 * N * N,
+            "solve_GBps_alg": 24.0 * N * N / (sv_ms * 1e-3) / 1e9 if sv_ms > 0 else None,
+            "timing": "avg_launch_ms from CUDA events around every k_oz_gemm launch of an eager pass of the same "
+                      f"{args.steps} steps right after the timed region (the timed region itself runs each "
+                      "step as one CUDA graph with a conditional while node for the fixed point)",
+            "eager_ms_per_step": prof_ms / args.steps,
+            "step_alg_flop": 16.0 * N**3 * (statistics.mean(iters) + 1),
+            "step_TFLOPs_alg": 16.0 * N**3 * (statistics.mean(iters) + 1) / (ms_per_step * 1e-3) / 1e12,
+            "accuracy": "residue GEMM relF vs extended precision 2.3-4.6e-16 at N = 130-512 (native FP64 DMMA "
+                        "5.5e-16-1.1e-15), tools/oz_zgemm_check.py; profiles/r01_oz_accuracy.txt",
+        }
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -476,7 +530,10 @@ def run_ours(args):
             "init": "W0 = lap^-1(random_admissible(2048, default_rng(0), 1/2048)) / ||.||_F",
             "iterations_per_step": sorted(set(iters)),
             "parallelism": "replicas" if world > 1 else "single",
-            "gemm": "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
+            "gemm": ("FP64-accurate complex products on the INT8 tensor cores: Ozaki scheme II (operands scaled to "
+                     "53-bit integers, 18 coprime moduli, tcgen05 kind::i8 residue GEMMs, 128-bit-exact CRT "
+                     "reconstruction); ZT_GEMM_ALGO=3m selects the native FP64 DMMA path") if oz else
+                    "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
             "launch": "one CUDA graph per step (fixed point = conditional WHILE node), 1 host sync per step",
             "l2": "no flush: per-step working set W_n, W~, P, a = 256 MB > 126 MB L2",
         },
@@ -506,6 +563,8 @@ def run_ours(args):
 # N=2048 from the committed `ncu --set full` capture (profiles/r01_ncu_summary.md)
 # ncu --set full dram bytes (profiles/r01_ncu_summary.md): k_zupdate 1076.1 + 134.0 MB,
 # k_update_pairs 236.0 + 41.9 MB, k_sum_planes 167.7 + 58.4 MB per full update
+# ncu --set full dram bytes of one k_oz_gemm launch (full product, N = 2048; profiles/r01_ncu_summary.md)
+TRAFFIC_OZ = None
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 

@@ -159,6 +159,9 @@ int zt_oz_moduli(int* out, int cap);
  * (converted row-wise, no transpose).  lower: only the 128-tiles of C on or
  * below the diagonal.  workspace: zt_oz_workspace_bytes(n). */
 size_t zt_oz_workspace_bytes(int n);
+/* CUDA-event totals of the residue-GEMM launches recorded while profiling
+ * (zt_profile_enable): ms/counts [0] full products, [1] lower-triangle ones. */
+int zt_oz_profile_read(double* ms, long long* counts, int reset);
 int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c,
                 int64_t ldc, int lower, void* workspace, size_t workspace_bytes, void* stream);
 

@@ -45,6 +45,7 @@ SIGNATURES = {
     "zt_oz_modgemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int, _vp]),
     "zt_oz_moduli": (_c_int, [_vp, _c_int]),
     "zt_oz_workspace_bytes": (_c_sz, [_c_int]),
+    "zt_oz_profile_read": (_c_int, [_vp, _vp, _c_int]),
     "zt_oz_zgemm": (_c_int, [_c_int, _vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_sz, _vp]),
     "zt_midpoint_step_host": (
         _c_int,

@@ -69,6 +69,7 @@ int zupdate_fused(int n, const double* p, const double* x, double* a, const doub
                   cudaStream_t st, int gemm1_only = 0, double* bbuf = nullptr, const ProgParams* prog = nullptr);
 size_t zupdate_prog_words(int n);
 size_t oz_update_workspace_bytes(int n);
+void oz_profile_enable(bool on);
 int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, const double* base,
               const double* xprev, const double* wn, double* out, double hh, double qq, unsigned long long* resid,
               unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only);
@@ -103,7 +104,9 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
                       const double* base, const double* xprev, double* out, int64_t ld, double hh,
                       double qq, unsigned long long* resid, int algo, cudaStream_t st);
 
-static int g_algo = 0;      // 0 = 3M, 1 = 4M (ZT_GEMM_ALGO=4m), 2 = INT8 Ozaki-II (ZT_GEMM_ALGO=oz)
+// step products: 2 = FP64-accurate Ozaki-II on the INT8 tensor cores (default),
+// 0 = 3M DMMA (ZT_GEMM_ALGO=3m or dmma), 1 = 4M DMMA (ZT_GEMM_ALGO=4m)
+static int g_algo = 2;
 // DMMA kernel variant for the products that stay on the FP64 pipe
 static inline int dmma_algo() { return g_algo == 1 ? 1 : 0; }
 static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
@@ -610,6 +613,7 @@ int64_t zt_launch_count(void) { return g_launches.load(); }
 
 int zt_profile_enable(int on) {
   g_prof = on != 0;
+  oz_profile_enable(g_prof);
   g_used = 0;
   return ZT_OK;
 }
@@ -628,7 +632,10 @@ int zt_profile_read(double* ms, int64_t* counts, int reset) {
 
 int zt_op_create(int n, int device, zt_op_t* op) {
   if (!op) return fail(ZT_EINVAL, "null output");
-  if (const char* e = getenv("ZT_GEMM_ALGO")) g_algo = (std::string(e) == "4m") ? 1 : (std::string(e) == "oz" ? 2 : 0);
+  if (const char* e = getenv("ZT_GEMM_ALGO")) {
+    const std::string v(e);
+    g_algo = v == "4m" ? 1 : ((v == "3m" || v == "dmma") ? 0 : 2);
+  }
   if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
   if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
   if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "zt_common.cuh"
 #include "zt_tma.cuh"
@@ -36,13 +37,16 @@ namespace oz {
 // 128 x TN output tiles: TN = 256 halves the B-operand L2 traffic per MMA
 // (the kernel is L2-bandwidth bound at TN = 128) at the price of a single
 // TMEM accumulator buffer (Re + Im = 2 TN columns of 512)
-constexpr int TM = 128, TN = OZ_TN, TK = 128;  // TK in bytes
-constexpr int NBUF = 512 / (2 * TN);          // TMEM accumulator buffers
-constexpr int TILE_BYTES = 128 * TK;          // one 128-row int8 tile (A)
+// K stages of 64 bytes (64 B swizzle) so four stages fit: with two 128-byte
+// stages the TMA latency of a stage exceeded the MMA time of the other
+constexpr int TM = 128, TN = OZ_TN, TK = 64;  // TK in bytes
+constexpr int NBUF = 512 / (2 * TN);         // TMEM accumulator buffers
+constexpr int TILE_BYTES = 128 * TK;         // one 128-row int8 tile (A)
 constexpr int B_TILE_BYTES = TN * TK;
 constexpr int STAGE_BYTES = 3 * TILE_BYTES + 2 * B_TILE_BYTES;  // A re, im, -im; B re, im
-constexpr int STAGES = 2;
-constexpr int THREADS = 6 * 32;
+constexpr int STAGES = 4;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each half the columns
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
@@ -58,10 +62,10 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0,
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-// UMMA smem descriptor: K-major, 128 B swizzle, 8-row groups 1024 B apart
+// UMMA smem descriptor: K-major, 64 B swizzle, 8-row groups 512 B apart
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 // D s32, A/B signed int8, K-major, M = 128, N = 128
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int s = 0; s < NBUF; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -211,7 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter = tile rows q*32 ..
+    const int q = warp & 3;                  // TMEM lane quarter = tile rows q*32 ..
+    const int ch = ((warp - 2) >> 2) * (TN / 2);  // column half
     unsigned lt = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++lt) {
       int j, tm, tn;
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int8_t* rre = g.r + ((size_t)(j * 2) * g.mp + row) * g.np + tn * TN;
       int8_t* rim = rre + (size_t)g.mp * g.np;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TN; c0 += 32) {
+      for (int c0 = ch; c0 < ch + TN / 2; c0 += 32) {
         uint32_t v[32];
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ab * 2 * TN + c0;
         OZ_LD32(v, ta);
@@ -282,7 +287,7 @@ static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols, in
   cuuint32_t box[2] = {TK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(ZT_ECUDA, "oz: tensor map encode failed");
   return ZT_OK;
@@ -656,6 +661,20 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
 
 static int g_oz_sms = 0;
 
+// CUDA-event timing of every residue-GEMM launch while profiling is on
+// (eager steps only; zt_profile_enable / zt_oz_profile_read)
+struct OzEv {
+  cudaEvent_t e0, e1;
+  int lower;
+};
+static std::vector<OzEv> g_oz_ev;
+static size_t g_oz_used = 0;
+static bool g_oz_prof = false;
+void oz_profile_enable(bool on) {
+  if (on && !g_oz_prof) g_oz_used = 0;
+  g_oz_prof = on;
+}
+
 // R = A * B^T residues for every modulus (see header); mp, np, kp multiples of 128
 int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* b, int8_t* r, int lower,
                cudaStream_t st) {
@@ -683,8 +702,21 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   g.r = r;
   const int per = lower ? lower_count(g.mt) : g.mt * g.nt;
   const int grid = std::min(nmod * per, g_oz_sms);
+  OzEv* ev = nullptr;
+  if (g_oz_prof) {
+    if (g_oz_used == g_oz_ev.size()) {
+      OzEv e{};
+      cudaEventCreate(&e.e0);
+      cudaEventCreate(&e.e1);
+      g_oz_ev.push_back(e);
+    }
+    ev = &g_oz_ev[g_oz_used++];
+    ev->lower = lower;
+    cudaEventRecord(ev->e0, st);
+  }
   k_oz_gemm<<<grid, THREADS, SMEM, st>>>(ma, mb, g);
   ZT_LAUNCHED();
+  if (ev) cudaEventRecord(ev->e1, st);
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
 }
@@ -706,6 +738,26 @@ extern "C" int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, co
 extern "C" int zt_oz_moduli(int* out, int cap) { return zt::oz_moduli(out, cap); }
 
 extern "C" size_t zt_oz_workspace_bytes(int n) { return zt::oz_workspace_bytes(n); }
+
+// ms[0] / counts[0]: full residue GEMMs, [1]: lower-triangle ones
+extern "C" int zt_oz_profile_read(double* ms, long long* counts, int reset) {
+  double m[2] = {0, 0};
+  long long c[2] = {0, 0};
+  for (size_t i = 0; i < zt::g_oz_used; ++i) {
+    float t = 0;
+    cudaEventSynchronize(zt::g_oz_ev[i].e1);
+    if (cudaEventElapsedTime(&t, zt::g_oz_ev[i].e0, zt::g_oz_ev[i].e1) == cudaSuccess) {
+      m[zt::g_oz_ev[i].lower ? 1 : 0] += t;
+      c[zt::g_oz_ev[i].lower ? 1 : 0] += 1;
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (ms) ms[k] = m[k];
+    if (counts) counts[k] = c[k];
+  }
+  if (reset) zt::g_oz_used = 0;
+  return ZT_OK;
+}
 
 extern "C" int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c,
                            int64_t ldc, int lower, void* ws, size_t ws_bytes, void* stream) {

@@ -14,7 +14,8 @@ B = torch.from_numpy(rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).to(
 C = torch.zeros_like(A)
 ws = torch.empty(lib.zt_oz_workspace_bytes(n), dtype=torch.uint8, device=dev)
 for _ in range(2):
-    lib.zt_oz_zgemm(n, A.data_ptr(), n, B.data_ptr(), n, mode, C.data_ptr(), n, 0, ws.data_ptr(), ws.numel(),
+    rc = lib.zt_oz_zgemm(n, A.data_ptr(), n, B.data_ptr(), n, mode, C.data_ptr(), n, 0, ws.data_ptr(), ws.numel(),
                     torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, (rc, lib.zt_last_error())
 torch.cuda.synchronize()
 print("ok")
