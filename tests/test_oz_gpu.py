@@ -1,0 +1,131 @@
+"""FP64-accurate complex GEMM on the INT8 tensor cores (Ozaki scheme II,
+csrc/zt_oz.cu), the step's default product: the tcgen05 kind::i8 residue
+GEMM against exact int64 arithmetic, the reconstructed complex128 product
+against an extended-precision reference (no less accurate than the native
+FP64 DMMA product), the skew-Hermitian B layout and the lower-tile mode; and
+the native DMMA step (ZT_GEMM_ALGO=3m) still matching the reference's cfg 1
+run (the step parity tests run on the default path)."""
+
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+from conftest import ROOT, relf
+
+from oracle import zeitlin_oracle as zo
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2206_05466_b200 import _lib
+
+    return _lib.lib
+
+
+def _moduli(lib):
+    buf = (ctypes.c_int * 32)()
+    k = lib.zt_oz_moduli(ctypes.cast(buf, ctypes.c_void_p), 32)
+    return [buf[i] for i in range(k)]
+
+
+@pytest.mark.parametrize("nmod,mp,np_,kp,lower", [(1, 128, 256, 64, 0), (3, 256, 512, 320, 0), (18, 256, 256, 256, 0),
+                                                  (2, 512, 512, 192, 1), (4, 768, 768, 128, 1)])
+def test_residue_gemm_exact(lib, nmod, mp, np_, kp, lower):
+    """R_j = (A_re B_re^T + A_-im B_im^T, A_re B_im^T + A_im B_re^T) mod p_j, exactly."""
+    P = _moduli(lib)
+    rng = np.random.default_rng(nmod * 7 + mp)
+    a = np.stack([rng.integers(-(P[j] // 2), P[j] // 2 + 1, (3, mp, kp)) for j in range(nmod)]).astype(np.int8)
+    b = np.stack([rng.integers(-(P[j] // 2), P[j] // 2 + 1, (2, np_, kp)) for j in range(nmod)]).astype(np.int8)
+    dev = torch.device("cuda:0")
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    r = torch.zeros(nmod, 2, mp, np_, dtype=torch.int8, device=dev)
+    rc = lib.zt_oz_modgemm(nmod, mp, np_, kp, ad.data_ptr(), bd.data_ptr(), r.data_ptr(), lower,
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    rh = r.cpu().numpy().astype(np.int64)
+    a64, b64 = a.astype(np.int64), b.astype(np.int64)
+    mask = ((np.arange(mp)[:, None] // 128) >= (np.arange(np_)[None, :] // 128)) if lower else np.ones((mp, np_), bool)
+    for j in range(nmod):
+        re = a64[j, 0] @ b64[j, 0].T + a64[j, 2] @ b64[j, 1].T
+        im = a64[j, 0] @ b64[j, 1].T + a64[j, 1] @ b64[j, 0].T
+        for ref, got in ((re, rh[j, 0]), (im, rh[j, 1])):
+            assert np.all((np.mod(ref - got, P[j]) == 0)[mask])
+            assert np.all(np.abs(got[mask]) <= 69)
+
+
+def _oz(lib, a, b, bmode=0, lower=0):
+    n = a.shape[0]
+    ws = torch.empty(lib.zt_oz_workspace_bytes(n), dtype=torch.uint8, device=a.device)
+    c = torch.zeros_like(a)
+    rc = lib.zt_oz_zgemm(n, a.data_ptr(), n, b.data_ptr(), n, bmode, c.data_ptr(), n, lower, ws.data_ptr(),
+                         ws.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rc == 0
+    return c.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [5, 130, 256])
+def test_complex_product_accuracy(lib, n):
+    """relF vs an extended-precision product <= 4e-16 and no worse than the
+    native FP64 DMMA product; the skew-B layout gives the same product."""
+    from paper_2206_05466_b200.integrator import zgemm
+
+    rng = np.random.default_rng(n)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    b = zo.random_admissible(n, rng, 1.0 / n)
+    b[np.diag_indices(n)] += 1e-3 * rng.normal(size=n)  # the solve's P has a real diagonal part
+    ref = (a.astype(np.clongdouble) @ b.astype(np.clongdouble)).astype(np.complex128)
+    dev = torch.device("cuda:0")
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    c0, c1 = _oz(lib, ad, bd, 0), _oz(lib, ad, bd, 1)
+    native = zgemm(ad, bd).cpu().numpy()
+    assert relf(c0, ref) <= 4e-16
+    assert relf(c0, ref) <= relf(native, ref) * 1.05
+    np.testing.assert_array_equal(c0, c1)
+    cl = _oz(lib, ad, bd, 1, lower=1)
+    blk = (np.arange(n)[:, None] // 128) >= (np.arange(n)[None, :] // 128)
+    np.testing.assert_array_equal(cl[blk], c1[blk])
+
+
+def test_zero_and_scaled_inputs(lib):
+    """Zero rows/columns (shift 0) stay exact zeros; the power-of-two scaling
+    makes the product equivariant to 2^k rescaling of either operand."""
+    n = 200
+    rng = np.random.default_rng(3)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    b = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    a[7] = 0
+    b[:, 11] = 0
+    dev = torch.device("cuda:0")
+    c = _oz(lib, torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
+    assert np.all(c[7] == 0) and np.all(c[:, 11] == 0)
+    c2 = _oz(lib, torch.from_numpy(a * 2.0**-300).to(dev), torch.from_numpy(b * 2.0**40).to(dev))
+    np.testing.assert_array_equal(c2, c * 2.0**-260)
+
+
+def test_native_dmma_step_still_matches_reference():
+    """ZT_GEMM_ALGO=3m (native FP64 DMMA products) in a fresh process: cfg 1
+    W10 and iteration counts against the reference's golden run."""
+    code = (
+        "import numpy as np, torch\n"
+        "from conftest import load_golden, relf\n"
+        "import paper_2206_05466_b200 as zt\n"
+        "g = load_golden('cfg1.npz')\n"
+        "st = zt.StepperState(w=torch.from_numpy(g['W0']).cuda(), h=0.01)\n"
+        "its = []\n"
+        "for _ in range(10):\n"
+        "    st, info = zt.midpoint_step_info(st)\n"
+        "    its.append(info.iterations)\n"
+        "assert its == list(g['iters']), its\n"
+        "print(relf(st.w.cpu().numpy(), g['W10']))\n"
+    )
+    env = dict(os.environ, ZT_GEMM_ALGO="3m", PYTHONPATH=os.pathsep.join([ROOT, os.path.join(ROOT, "tests")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-10
