@@ -564,7 +564,7 @@ def run_ours(args):
 # ncu --set full dram bytes (profiles/r01_ncu_summary.md): k_zupdate 1076.1 + 134.0 MB,
 # k_update_pairs 236.0 + 41.9 MB, k_sum_planes 167.7 + 58.4 MB per full update
 # ncu --set full dram bytes of one k_oz_gemm launch (full product, N = 2048; profiles/r01_ncu_summary.md)
-TRAFFIC_OZ = None
+TRAFFIC_OZ = (377.892 + 128.074) * 1e6
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
