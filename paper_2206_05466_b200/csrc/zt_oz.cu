@@ -9,7 +9,7 @@
 // Layouts (int8, zero padded to 128 in every dimension):
 //   A residues [NMOD][3][Mp][Kp]  planes re, im, -im   (K-major rows)
 //   B residues [NMOD][2][Np][Kp]  planes re, im        (K-major: B^T rows)
-//   R residues [NMOD][2][Mp][Np]  Re, Im of the product mod p_j (centred)
+//   R residues [NMOD][2][Mp][Np]  Re, Im of the product mod p_j (in [0, p))
 #include <cuda.h>
 
 #include <algorithm>
@@ -25,9 +25,11 @@ constexpr int OZ_NMOD = 18;
 // pairwise coprime, product ~ 2^120.5
 __constant__ int c_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
                                     103, 101, 97,  89,  83,  79,  73,  71,  67};
+// floor(2^32 / p)
+__constant__ int c_oz_m[OZ_NMOD] = {33554432, 33818640, 34359738, 35495597, 36092162, 36709122, 38008560, 39403369, 40139881,
+                                    41698711, 42524428, 44278013, 48258059, 51746593, 54366674, 58835168, 60492497, 64103989};
 static const int h_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
                                     103, 101, 97,  89,  83,  79,  73,  71,  67};
-__constant__ double c_oz_inv[OZ_NMOD];  // 1 / p (rounded)
 
 namespace oz {
 
@@ -122,11 +124,14 @@ __device__ __forceinline__ void work_of(const GemmArgs& g, int w, int per, int& 
   }
 }
 
-__device__ __forceinline__ int modc(int v, int p, double invp) {
-  // centred residue of an int32 |v| < 2^31 (exact: the quotient is rounded
-  // from a double and the product is formed in integers)
-  const int q = __double2int_rn((double)v * invp);
-  return v - q * p;
+// residue of an int32 accumulator (|v| < 2^26) in [0, p): Barrett quotient
+// from the high word of v * floor(2^32 / p) (floor(v / p) or one less), one
+// correction; integer pipe only.  The CRT accepts any representative, and
+// [0, p) fits int8 for p <= 128.
+__device__ __forceinline__ int modc(int v, int p, int m) {
+  const unsigned u = (unsigned)(v + (p << 20));  // >= 0: |v| < 2^26 <= p 2^20
+  const unsigned r = u - __umulhi(u, (unsigned)m) * (unsigned)p;
+  return (int)(r >= (unsigned)p ? r - p : r);
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -224,11 +229,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int ab = lt % NBUF;
       mbar_wait(&tfull[ab], (lt / NBUF) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int p = c_oz_p[j];
-      const double invp = 1.0 / (double)p;
+      const int p = c_oz_p[j], pm = c_oz_m[j];
       const int row = tm * TM + q * 32 + lane;
       int8_t* rre = g.r + ((size_t)(j * 2) * g.mp + row) * g.np + tn * TN;
       int8_t* rim = rre + (size_t)g.mp * g.np;
+#ifdef OZ_EXP_NOEPI
+      if (p == 12345)
+#endif
 #pragma unroll 1
       for (int c0 = ch; c0 < ch + TN / 2; c0 += 32) {
         uint32_t v[32];
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int e = 0; e < 8; ++e) {
           uint32_t x = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)v[4 * e + b], p, invp) & 0xff)) << (8 * b);
+          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)v[4 * e + b], p, pm) & 0xff)) << (8 * b);
           pk[e] = x;
         }
         uint4* d = reinterpret_cast<uint4*>(rre + c0);
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int e = 0; e < 8; ++e) {
           uint32_t x = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)v[4 * e + b], p, invp) & 0xff)) << (8 * b);
+          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)v[4 * e + b], p, pm) & 0xff)) << (8 * b);
           pk[e] = x;
         }
         d = reinterpret_cast<uint4*>(rim + c0);
@@ -306,14 +313,29 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
 // from 18-bit limbs of |x| in 32-bit integer arithmetic (Barrett reduction),
 // not from FP64 divisions.
 // ---------------------------------------------------------------------------
-// x integer valued, |x| < 2^53: q = rint(x / p) from the rounded reciprocal
-// (always floor or ceil of x / p), r = x - q p exactly (FMA), and the low
-// word of r + 1.5 * 2^52 is r in two's complement: |r| < 0.54 p <= 69
+// Residues of an integer-valued x (|x| < 2^53) for all 18 moduli in two
+// levels: y = x mod Q_g for the six triples Q_g = p_3g p_3g+1 p_3g+2 < 2^21
+// in FP64 (q = rint(x / Q) from the rounded reciprocal is floor or ceil, and
+// y = x - q Q is exact by FMA), then y mod p in FP32 (|y| <= 2^20: exact
+// integer arithmetic in a float); the low byte of r + 1.5 * 2^23 is r in
+// two's complement.  |r| <= 69 for every modulus.
 constexpr double OZ_MAGIC = 6755399441055744.0;
-__device__ __forceinline__ uint32_t res_byte(double x, double p, double invp) {
-  const double q = fma(x, invp, OZ_MAGIC) - OZ_MAGIC;
-  const double r = fma(-q, p, x);
-  return (uint32_t)__double2loint(r + OZ_MAGIC) & 0xffu;
+constexpr float OZ_MAGIC_F = 12582912.0f;
+__constant__ double c_oz_q[6], c_oz_qinv[6];
+__constant__ float c_oz_pf[OZ_NMOD], c_oz_pinvf[OZ_NMOD];
+__device__ __forceinline__ float reduce_triple(double x, int g) {
+  const double q = fma(x, c_oz_qinv[g], OZ_MAGIC) - OZ_MAGIC;
+  return (float)fma(-q, c_oz_q[g], x);
+}
+// residue of y as the low byte of the returned word (yM = y + 1.5 * 2^23,
+// exact for |y| < 2^22): r + 1.5 * 2^23 = fma(-q, p, yM)
+__device__ __forceinline__ uint32_t res_word_f(float y, float yM, int t) {
+  const float q = fmaf(y, c_oz_pinvf[t], OZ_MAGIC_F) - OZ_MAGIC_F;
+  return __float_as_uint(fmaf(-q, c_oz_pf[t], yM));
+}
+// low bytes of four words into one (byte e from word e)
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
 // exponent shift that puts amax in [2^(KB-1), 2^KB); 0 for an all-zero line
@@ -355,30 +377,48 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
       xv[e] = rint(ldexp(v.x, sh));
       xv[4 + e] = rint(ldexp(v.y, sh));
     }
-#pragma unroll 2
-    for (int t = 0; t < OZ_NMOD; ++t) {
-      const double p = (double)c_oz_p[t], invp = c_oz_inv[t];
-      uint32_t wr = 0, wi = 0, wn = 0, wb = 0;
+#pragma unroll 1
+    for (int g = 0; g < 6; ++g) {
+    float yv[8], ym[8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t rr = res_byte(xv[e], p, invp), ri = res_byte(xv[4 + e], p, invp);
-        wr |= rr << (8 * e);
-        wi |= ri << (8 * e);
-        wn |= ((0x100u - ri) & 0xffu) << (8 * e);
-        // skew-B layout (modes 1, 2): -re off the diagonal, re on it
-        wb |= ((k0 + e == i) ? rr : ((0x100u - rr) & 0xffu)) << (8 * e);
+    for (int e = 0; e < 8; ++e) {
+      yv[e] = reduce_triple(xv[e], g);
+      ym[e] = yv[e] + OZ_MAGIC_F;
+    }
+#pragma unroll
+    for (int t = 3 * g; t < 3 * g + 3; ++t) {
+      uint32_t rw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rw[e] = res_word_f(yv[e], ym[e], t);
+      const uint32_t wr = pack4(rw[0], rw[1], rw[2], rw[3]);
+      const uint32_t wi = pack4(rw[4], rw[5], rw[6], rw[7]);
+      const uint32_t wn = __vneg4(wi);
+      // skew-B layout (modes 1, 2): -re off the diagonal, re on it
+      uint32_t wb = __vneg4(wr);
+      if ((unsigned)(i - k0) < 4u) {
+        const int sh8 = 8 * (i - k0);
+        wb = (wb & ~(0xffu << sh8)) | (wr & (0xffu << sh8));
       }
+#ifdef OZ_EXP_NOSTORE
+      if (wr == 0x12345678u && wb == 1u && wn == 7u) {
+#else
       if (mode != 1) {
+#endif
         int8_t* base = out + ((size_t)(t * 3) * mp + i) * kp + k0;
         *reinterpret_cast<uint32_t*>(base) = wr;
         *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
         *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
       }
+#ifdef OZ_EXP_NOSTORE
+      if (wi == 0x12345678u && wb == 3u) {
+#else
       if (mode != 0) {
+#endif
         int8_t* b2 = (mode == 1 ? out : out2) + ((size_t)(t * 2) * mp + i) * kp + k0;
         *reinterpret_cast<uint32_t*>(b2) = wb;
         *reinterpret_cast<uint32_t*>(b2 + (size_t)mp * kp) = wi;
       }
+    }
     }
   }
 }
@@ -423,18 +463,25 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
     xv[e] = rint(ldexp(v.x, sh));
     xv[4 + e] = rint(ldexp(v.y, sh));
   }
-#pragma unroll 2
-  for (int t = 0; t < OZ_NMOD; ++t) {
-    const double p = (double)c_oz_p[t], invp = c_oz_inv[t];
-    uint32_t wr = 0, wi = 0;
+#pragma unroll 1
+  for (int g = 0; g < 6; ++g) {
+    float yv[8], ym[8];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      wr |= res_byte(xv[e], p, invp) << (8 * e);
-      wi |= res_byte(xv[4 + e], p, invp) << (8 * e);
+    for (int e = 0; e < 8; ++e) {
+      yv[e] = reduce_triple(xv[e], g);
+      ym[e] = yv[e] + OZ_MAGIC_F;
     }
-    int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + kk;
-    *reinterpret_cast<uint32_t*>(base) = wr;
-    *reinterpret_cast<uint32_t*>(base + (size_t)np * kp) = wi;
+#pragma unroll
+    for (int t = 3 * g; t < 3 * g + 3; ++t) {
+      uint32_t rw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rw[e] = res_word_f(yv[e], ym[e], t);
+      const uint32_t wr = pack4(rw[0], rw[1], rw[2], rw[3]);
+      const uint32_t wi = pack4(rw[4], rw[5], rw[6], rw[7]);
+      int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + kk;
+      *reinterpret_cast<uint32_t*>(base) = wr;
+      *reinterpret_cast<uint32_t*>(base + (size_t)np * kp) = wi;
+    }
   }
 }
 
@@ -443,8 +490,8 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
 // M_t = M / p_t, y_t = M_t^-1 mod p_t (r_t need not be reduced: a multiple
 // of p_t times M_t is a multiple of M).  W_t (< M < 2^121) and M are split
 // into three pieces on the grids 2^0, 2^40, 2^80 (<= 41 bits), so each
-// partial sum S_k = sum_t r_t W_t,k is exact in binary64 (|r_t| <= 69:
-// 7 + 41 + log2(18) < 53 bits); q = rint(S / M) (|q| < 2^11) and
+// partial sum S_k = sum_t r_t W_t,k is exact in binary64 (|r_t| <= 127:
+// 7 + 41 + log2(18) < 53 bits); q = rint(S / M) (|q| < 2^12) and
 // D_k = S_k - q M_k are exact, and x = D_2 + D_1 + D_0 is the centred
 // representative (|x| << M / 2 by the choice of KB).
 // ---------------------------------------------------------------------------
@@ -538,9 +585,20 @@ static int crt_init() {
   for (int k = 0; k < 3; ++k) h.mp[k] = piece(m, k);
   h.m_inv = 1.0 / (h.mp[2] + h.mp[1] + h.mp[0]);
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
-  double inv[OZ_NMOD];
-  for (int t = 0; t < OZ_NMOD; ++t) inv[t] = 1.0 / (double)h_oz_p[t];
-  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_inv, inv, sizeof inv));
+  double qd[6], qi[6];
+  float pf[OZ_NMOD], pif[OZ_NMOD];
+  for (int g = 0; g < 6; ++g) {
+    qd[g] = (double)h_oz_p[3 * g] * h_oz_p[3 * g + 1] * h_oz_p[3 * g + 2];  // < 2^21
+    qi[g] = 1.0 / qd[g];
+  }
+  for (int t = 0; t < OZ_NMOD; ++t) {
+    pf[t] = (float)h_oz_p[t];
+    pif[t] = 1.0f / (float)h_oz_p[t];
+  }
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_q, qd, sizeof qd));
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_qinv, qi, sizeof qi));
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_pf, pf, sizeof pf));
+  ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_oz_pinvf, pif, sizeof pif));
   g_crt_ready = true;
   return ZT_OK;
 }
