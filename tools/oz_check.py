@@ -47,8 +47,8 @@ def run(nmod, mp, np_, kp, lower=0, check_rows=None, seed=0):
             cc = np.arange(np_)[None, :] // 128
             mask = rr >= cc
         # residues are centred; a tie (p even) may come out as +p/2 or -p/2
-        ok_re = (np.mod(re - gre, P[j]) == 0) & (np.abs(gre) <= P[j] // 2)
-        ok_im = (np.mod(im - gim, P[j]) == 0) & (np.abs(gim) <= P[j] // 2)
+        ok_re = (np.mod(re - gre, P[j]) == 0) & (gre >= 0) & (gre < P[j])  # epilogue residues in [0, p)
+        ok_im = (np.mod(im - gim, P[j]) == 0) & (gim >= 0) & (gim < P[j])
         bad += int(((~ok_re) & mask).sum() + ((~ok_im) & mask).sum())
     return bad, ad, bd, r
 
