@@ -354,11 +354,22 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
   const int i = blockIdx.x;
   __shared__ double red[8];
   double amax = 0.0;
-  if (i < n)
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+  if (i < n) {
+    // all of this thread's loads in flight at once (the max chain would
+    // otherwise serialise them: the dominant stall)
+    int k = threadIdx.x;
+    for (; k + 7 * 256 < n; k += 8 * 256) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ld2(src + ((size_t)i * ld + k + u * 256) * 2);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) amax = fmax(amax, fmax(fabs(v[u].x), fabs(v[u].y)));
+    }
+    for (; k < n; k += 256) {
       const double2 v = ld2(src + ((size_t)i * ld + k) * 2);
       amax = fmax(amax, fmax(fabs(v.x), fabs(v.y)));
     }
+  }
   for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
   __syncthreads();
