@@ -72,7 +72,8 @@ size_t oz_update_workspace_bytes(int n);
 void oz_profile_enable(bool on);
 int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, const double* base,
               const double* xprev, const double* wn, double* out, double hh, double qq, unsigned long long* resid,
-              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only);
+              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only, cudaEvent_t x_join);
+int oz_convert_x(int n, const double* x, void* ws, cudaStream_t st);
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
@@ -227,17 +228,40 @@ static void prof_collect() {
   g_used = 0;
 }
 
+// INT8 path: X's column conversion is independent of the solve, so it runs
+// on a side stream forked from `st` (event fork / join: captured into the
+// step graph as parallel branches) while the latency-bound solve runs.
+static thread_local cudaStream_t t_side = nullptr;
+static thread_local cudaEvent_t t_fork = nullptr, t_join = nullptr;
+static int oz_fork_x(int n, const double* x, StepWS& w, cudaStream_t st) {
+  if (!t_side) {
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_side, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_fork, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_join, cudaEventDisableTiming));
+  }
+  ZT_CUDA_CHECK(cudaEventRecord(t_fork, st));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_side, t_fork, 0));
+  const int rc = oz_convert_x(n, x, w.oz, t_side);
+  if (rc) return rc;
+  ZT_CUDA_CHECK(cudaEventRecord(t_join, t_side));
+  return ZT_OK;
+}
+
 // One update: P = lap^-1 X; a = P X; out = base + hh (a - a^H) + qq a P.
 static int update(zt_operator* op, const double* x, const double* base, const double* xprev,
                   const double* wn, double* out, double hh, double qq, StepWS& w,
                   unsigned long long* resid, unsigned long long* cons, cudaStream_t st) {
   const int n = op->n;
   prof_mark(0, st);
+  if (g_algo == 2) {
+    const int rc0 = oz_fork_x(n, x, w, st);
+    if (rc0) return rc0;
+  }
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
   if (g_algo == 2) {
-    rc = oz_update(n, w.p, x, w.a, w.b, base, xprev, wn, out, hh, qq, resid, cons, w.oz, st, 0);
+    rc = oz_update(n, w.p, x, w.a, w.b, base, xprev, wn, out, hh, qq, resid, cons, w.oz, st, 0, t_join);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;
@@ -270,11 +294,15 @@ static int final_update(zt_operator* op, double* x, const double* wn, double h, 
                         bool prog = false) {
   const int n = op->n;
   prof_mark(0, st, 1);
+  if (g_algo == 2) {
+    const int rc0 = oz_fork_x(n, x, w, st);
+    if (rc0) return rc0;
+  }
   int rc = stream_solve(op, x, n, 0, w.p, n, 0, 1, w.solve, w.solve_bytes, st);
   if (rc) return rc;
   prof_mark(1, st);
   if (g_algo == 2) {
-    rc = oz_update(n, w.p, x, w.a, nullptr, nullptr, nullptr, wn, x, h, 0.0, nullptr, nullptr, w.oz, st, 1);
+    rc = oz_update(n, w.p, x, w.a, nullptr, nullptr, nullptr, wn, x, h, 0.0, nullptr, nullptr, w.oz, st, 1, t_join);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;

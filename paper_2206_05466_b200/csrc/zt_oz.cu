@@ -685,9 +685,33 @@ size_t oz_update_workspace_bytes(int n) {
 // operand from the same conversion pass as its A layout), then the update
 // pass.  gemm1_only: the step's final update W_{n+1} = W_n + h (a - a^H)
 // (out = x, h = hh; k_final_commutator).
+// X (the B operand of GEMM-1) to column-scaled residues; independent of the
+// stream solve, so the step runs it on a side stream beside the solve
+int oz_convert_x(int n, const double* x, void* ws, cudaStream_t st) {
+  if (!g_crt_ready) {
+    const int rc = crt_init();
+    if (rc) return rc;
+  }
+  const int pd = (n + 255) / 256 * 256;
+  const int kb = oz_bits(n);
+  const size_t pl = (size_t)OZ_NMOD * pd * pd;
+  int8_t* bx = static_cast<int8_t*>(ws) + 3 * pl;
+  int* sx = reinterpret_cast<int*>(bx + 6 * pl) + pd;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(sx + 3 * pd);
+  ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pd, st));
+  k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, x, n, cmax);
+  ZT_LAUNCHED();
+  k_oz_conv_cols<<<dim3(pd / 32, pd / 32), 256, 0, st>>>(n, x, n, pd, pd, OZ_NMOD, kb, cmax, bx, sx);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+// x_join: X was converted by oz_convert_x on another stream; wait for this
+// event before GEMM-1 (nullptr: convert X here)
 int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, const double* base,
               const double* xprev, const double* wn, double* out, double hh, double qq, unsigned long long* resid,
-              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only) {
+              unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only, cudaEvent_t x_join) {
   if (!g_crt_ready) {
     const int rc = crt_init();
     if (rc) return rc;
@@ -707,11 +731,13 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   k_oz_conv_rows<<<pd, 256, 0, st>>>(n, p, n, pd, pd, OZ_NMOD, kb, gemm1_only ? 0 : 2, ares, sp,
                                      gemm1_only ? nullptr : bp, nullptr);
   ZT_LAUNCHED();
-  ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pd, st));
-  k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, x, n, cmax);
-  ZT_LAUNCHED();
-  k_oz_conv_cols<<<dim3(pd / 32, pd / 32), 256, 0, st>>>(n, x, n, pd, pd, OZ_NMOD, kb, cmax, bx, sx);
-  ZT_LAUNCHED();
+  if (x_join) {
+    ZT_CUDA_CHECK(cudaStreamWaitEvent(st, x_join, 0));
+  } else {
+    const int rc0 = oz_convert_x(n, x, ws, st);
+    if (rc0) return rc0;
+  }
+  (void)cmax;
   int rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bx, rres, 0, st);
   if (rc) return rc;
   k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0);
