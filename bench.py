@@ -488,14 +488,14 @@ def run_ours(args):
         pd = (N + 255) // 256 * 256
         mt, nt = pd // 128, pd // 256
         low = sum(tm * 128 // 256 + 1 for tm in range(mt)) / (mt * nt)
-        nmod = 18
+        nmod = int(lib.zt_oz_moduli(None, 0)) if hasattr(lib, "zt_oz_moduli") else 16
         ops_full = nmod * 4 * 2.0 * pd**3          # 4M: four int8 products per modulus
         full_ms = oz_ms[0] / oz_cnt[0]
         low_ms = oz_ms[1] / max(1, oz_cnt[1])
         achieved_i8 = ops_full / (full_ms * 1e-3) / 1e12
         roofline = {
             "bound": "tensor",
-            "kernel": "k_oz_gemm: 18-modulus int8 residue GEMM of the FP64-accurate complex product "
+            "kernel": f"k_oz_gemm: {nmod}-modulus int8 residue GEMM of the FP64-accurate complex product "
                       "a = P X (Ozaki scheme II on tcgen05 kind::i8, TMEM accumulators)",
             "achieved": achieved_i8, "peak": ipeak, "unit": "TFLOP/s", "frac": achieved_i8 / ipeak,
             "op_type": "int8 tensor-core ops (2 per MAC), counted like NVIDIA TOPS",
@@ -531,7 +531,7 @@ def run_ours(args):
             "iterations_per_step": sorted(set(iters)),
             "parallelism": "replicas" if world > 1 else "single",
             "gemm": ("FP64-accurate complex products on the INT8 tensor cores: Ozaki scheme II (operands scaled to "
-                     "53-bit integers, 18 coprime moduli, tcgen05 kind::i8 residue GEMMs, 128-bit-exact CRT "
+                     "53-bit integers, 16 coprime moduli <= 256, tcgen05 kind::i8 residue GEMMs, 128-bit-exact CRT "
                      "reconstruction); ZT_GEMM_ALGO=3m selects the native FP64 DMMA path") if oz else
                     "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
             "launch": "one CUDA graph per step (fixed point = conditional WHILE node), 1 host sync per step",

@@ -144,7 +144,8 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
 
 /* INT8 tensor-core building block of an FP64-accurate complex GEMM
  * (Ozaki scheme II, csrc/zt_oz.cu): for every modulus j < nmod, the
- * centred residues mod p_j of Re / Im of A * B^T from int8 residue planes
+ * residues (Re / Im of A * B^T + floor(p_j / 2)) mod p_j, unsigned bytes
+ * in [0, p_j), from centred int8 residue planes
  * A [nmod][3][mp][kp] (re, im, -im) and B [nmod][2][np][kp] (re, im) into
  * R [nmod][2][mp][np]; tcgen05 kind::i8 MMAs, int32 accumulation in TMEM.
  * mp, np, kp multiples of 128; lower != 0: square, only 128-tiles on or
@@ -152,6 +153,12 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
 int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, const void* b, void* r, int lower,
                   void* stream);
 int zt_oz_moduli(int* out, int cap);
+/* Residue-GEMM kernel choice for zt_oz_modgemm and the step (0 = the
+ * ZT_OZ_CTA environment variable, else 1): 1 = one CTA per 128 x 256 tile
+ * (Re + Im accumulators in TMEM), 2 = CTA pairs (tcgen05 cta_group::2, Re
+ * and Im as separate 256 x 256 real tiles with K doubled, double-buffered
+ * TMEM accumulators; used when mp % 256 == 0).  ZT_EINVAL otherwise. */
+int zt_oz_set_cta(int c);
 /* C = A B (complex128, n x n, row-major with leading dimensions) through the
  * residue GEMM: rows of A and columns of B scaled to integers of up to 53
  * bits, 18 moduli, CRT reconstruction in 128-bit integers.  bmode 1: B is

@@ -5,11 +5,14 @@
 // accumulation (4M complex form: Re = Ar Br + (-Ai) Bi, Im = Ar Bi + Ai Br),
 // reduced again modulo p in the epilogue, and reassembled by the Chinese
 // remainder theorem into the exact integer product, then scaled back.
+// 16 pairwise-coprime moduli <= 256 (M ~ 2^125.4): 53-bit operands up to
+// K = 16384 with the 4M sum bound 2 K 2^106 < M / 2.
 //
 // Layouts (int8, zero padded to 128 in every dimension):
 //   A residues [NMOD][3][Mp][Kp]  planes re, im, -im   (K-major rows)
 //   B residues [NMOD][2][Np][Kp]  planes re, im        (K-major: B^T rows)
-//   R residues [NMOD][2][Mp][Np]  Re, Im of the product mod p_j (in [0, p))
+//   R residues [NMOD][2][Mp][Np]  (Re, Im of the product + floor(p_j / 2)) mod p_j,
+//                                 unsigned bytes in [0, p_j)
 #include <cuda.h>
 
 #include <algorithm>
@@ -21,15 +24,15 @@
 
 namespace zt {
 
-constexpr int OZ_NMOD = 18;
-// pairwise coprime, product ~ 2^120.5
-__constant__ int c_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
-                                    103, 101, 97,  89,  83,  79,  73,  71,  67};
+constexpr int OZ_NMOD = 16;
+// pairwise coprime (256 = 2^8, 255 = 3 5 17, 253 = 11 23, 247 = 13 19,
+// 217 = 7 31, the rest prime), product ~ 2^125.4; centred residues fit int8
+__constant__ int c_oz_p[OZ_NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 // floor(2^32 / p)
-__constant__ int c_oz_m[OZ_NMOD] = {33554432, 33818640, 34359738, 35495597, 36092162, 36709122, 38008560, 39403369, 40139881,
-                                    41698711, 42524428, 44278013, 48258059, 51746593, 54366674, 58835168, 60492497, 64103989};
-static const int h_oz_p[OZ_NMOD] = {128, 127, 125, 121, 119, 117, 113, 109, 107,
-                                    103, 101, 97,  89,  83,  79,  73,  71,  67};
+__constant__ unsigned c_oz_m[OZ_NMOD] = {16777216, 16843009, 16976155, 17111423, 17388531, 17821441,
+                                         17970574, 18433336, 18755315, 18920560, 19259943, 19792476,
+                                         20355295, 21582750, 21801864, 22253716};
+static const int h_oz_p[OZ_NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 
 namespace oz {
 
@@ -47,7 +50,10 @@ constexpr int TILE_BYTES = 128 * TK;         // one 128-row int8 tile (A)
 constexpr int B_TILE_BYTES = TN * TK;
 constexpr int STAGE_BYTES = 3 * TILE_BYTES + 2 * B_TILE_BYTES;  // A re, im, -im; B re, im
 constexpr int STAGES = 4;
-constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each half the columns
+#ifndef OZ_EPI_WARPS
+#define OZ_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = OZ_EPI_WARPS;  // EPI_WARPS / 4 per TMEM lane quarter, each a column group
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 
@@ -124,13 +130,14 @@ __device__ __forceinline__ void work_of(const GemmArgs& g, int w, int per, int& 
   }
 }
 
-// residue of an int32 accumulator (|v| < 2^26) in [0, p): Barrett quotient
-// from the high word of v * floor(2^32 / p) (floor(v / p) or one less), one
-// correction; integer pipe only.  The CRT accepts any representative, and
-// [0, p) fits int8 for p <= 128.
-__device__ __forceinline__ int modc(int v, int p, int m) {
-  const unsigned u = (unsigned)(v + (p << 20));  // >= 0: |v| < 2^26 <= p 2^20
-  const unsigned r = u - __umulhi(u, (unsigned)m) * (unsigned)p;
+// (v + floor(p / 2)) mod p in [0, p) for an int32 accumulator v
+// (|v| <= 2 K 128^2 <= 2^29 for K <= 16384): u = v + p 2^23 + floor(p / 2)
+// lies in (0, 2^32); Barrett quotient from the high word of u floor(2^32 / p)
+// (floor(u / p) or one less), one correction; integer pipe only.  The
+// reconstruction subtracts floor(p / 2) again (centred residues, |c| <= 128).
+__device__ __forceinline__ int modc(int v, int p, unsigned m) {
+  const unsigned u = (unsigned)v + ((unsigned)p << 23) + ((unsigned)p >> 1);
+  const unsigned r = u - __umulhi(u, m) * (unsigned)p;
   return (int)(r >= (unsigned)p ? r - p : r);
 }
 
@@ -221,7 +228,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;                  // TMEM lane quarter = tile rows q*32 ..
-    const int ch = ((warp - 2) >> 2) * (TN / 2);  // column half
+    constexpr int CW = TN / (EPI_WARPS / 4);      // columns per warp
+    const int ch = ((warp - 2) >> 2) * CW;        // column group
     unsigned lt = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++lt) {
       int j, tm, tn;
@@ -229,7 +237,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int ab = lt % NBUF;
       mbar_wait(&tfull[ab], (lt / NBUF) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int p = c_oz_p[j], pm = c_oz_m[j];
+      const int p = c_oz_p[j];
+      const unsigned pm = c_oz_m[j];
       const int row = tm * TM + q * 32 + lane;
       int8_t* rre = g.r + ((size_t)(j * 2) * g.mp + row) * g.np + tn * TN;
       int8_t* rim = rre + (size_t)g.mp * g.np;
@@ -237,10 +246,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (p == 12345)
 #endif
 #pragma unroll 1
-      for (int c0 = ch; c0 < ch + TN / 2; c0 += 32) {
-        uint32_t v[32];
+      for (int c0 = ch; c0 < ch + CW; c0 += 32) {
+        uint32_t v[32], u[32];
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ab * 2 * TN + c0;
         OZ_LD32(v, ta);
+        OZ_LD32(u, ta + TN);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         uint32_t pk[8];
 #pragma unroll
@@ -253,13 +263,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint4* d = reinterpret_cast<uint4*>(rre + c0);
         d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        OZ_LD32(v, ta + TN);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           uint32_t x = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)v[4 * e + b], p, pm) & 0xff)) << (8 * b);
+          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(modc((int)u[4 * e + b], p, pm) & 0xff)) << (8 * b);
           pk[e] = x;
         }
         d = reinterpret_cast<uint4*>(rim + c0);
@@ -276,6 +284,247 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+}  // namespace oz
+
+// ---------------------------------------------------------------------------
+// CTA-pair kernel (cta_group::2, the default): the complex product as two
+// real products with K doubled, Re = [Ar | -Ai] [Br ; Bi] and
+// Im = [Ai | Ar] [Br ; Bi], so a work item is ONE real 256 x 256 tile (Re or
+// Im of a pair tile) with a single 256-column accumulator per CTA: the TMEM
+// accumulators double-buffer and the mod-p epilogue of one item overlaps the
+// MMAs of the next (the single-CTA kernel's Re + Im fill TMEM and its
+// epilogue stalls the tensor pipe).  Each CTA of the pair loads 128 rows of
+// the A plane and 128 of the 256 B columns per stage; the leader's single
+// thread issues M = 256, N = 256 MMAs over both CTAs' shared memory, so every
+// SM runs 128 x 256 x 32 MMAs (the full-rate shape) at 8 operand KB per
+// million MACs.  No re-layout: the K halves read the existing re / im / -im
+// planes.
+// ---------------------------------------------------------------------------
+namespace oz2 {
+constexpr int TM = 256, TN = 256, TK = oz::TK;  // pair tile; TK in bytes
+constexpr int A_BYTES = 128 * TK;               // one CTA's 128 rows of an A plane
+constexpr int B_BYTES = (TN / 2) * TK;          // one CTA's 128 columns of a B plane
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+#ifndef OZ2_STAGES
+#define OZ2_STAGES 12
+#endif
+constexpr int STAGES = OZ2_STAGES;
+constexpr int NBUF = 2;  // TMEM accumulator buffers of TN columns
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+// D s32, A/B signed int8, K-major, M = 256 (pair), N = 256
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
+                           ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory, completion counted on the leader's barrier
+__device__ __forceinline__ void tma2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+// arrive on the barrier at this offset in both CTAs once the issued MMAs finish
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+// work item w -> modulus j, part (0 Re, 1 Im), pair tile (tm, tn); lower
+// mode: the 256 x 256 tiles meeting the lower 128-block triangle (tn <= tm)
+__host__ __device__ __forceinline__ int lower_count(int mt) { return mt * (mt + 1) / 2; }
+__device__ __forceinline__ void pair_work_of(const oz::GemmArgs& g, int w, int per, int& j, int& part, int& tm,
+                                             int& tn) {
+  j = w / (2 * per);
+  int t = w - j * 2 * per;
+  part = t & 1;
+  t >>= 1;
+  if (g.lower) {
+    tm = 0;
+    while (t > tm) {
+      t -= tm + 1;
+      ++tm;
+    }
+    tn = t;
+  } else {
+    tm = t % g.mt;
+    tn = t / g.mt;
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_oz_gemm2(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, oz::GemmArgs g) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int per = g.lower ? lower_count(g.mt) : g.mt * g.nt;
+  const int total = g.nmod * 2 * per;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < NBUF; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * EPI_WARPS);  // leader's: both CTAs' epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
+      const uint32_t fb0 = mapa(smem_u32(&full[0]), 0);
+      unsigned it = 0;
+      for (int w = cl; w < total; w += ncl) {
+        int j, part, tm, tn;
+        pair_work_of(g, w, per, j, part, tm, tn);
+        // K half 0: A plane re (Re) / im (Im) with B re; half 1: -im (Re) / re (Im) with B im
+        const int ra0 = (j * 3 + part) * g.mp + tm * TM + rank * 128;
+        const int ra1 = (j * 3 + (part ? 0 : 2)) * g.mp + tm * TM + rank * 128;
+        const int rb0 = (j * 2) * g.np + tn * TN + rank * (TN / 2), rb1 = rb0 + g.np;
+        for (int kb = 0; kb < 2 * g.kt; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          if (rank == 0) oz::mbar_arrive_tx(&full[s], 2 * STAGE_BYTES);
+          const bool h1 = kb >= g.kt;
+          const int kc = (h1 ? kb - g.kt : kb) * TK;
+          tma2d_pair(st, &ma, kc, h1 ? ra1 : ra0, fb0 + s * 8);
+          tma2d_pair(st + A_BYTES, &mb, kc, h1 ? rb1 : rb0, fb0 + s * 8);
+        }
+      }
+      // drain: every issued stage consumed before this CTA may exit
+      for (int i = 0; i < STAGES; ++i, ++it) mbar_wait(&empty[it % STAGES], ((it / STAGES) & 1) ^ 1);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      unsigned it = 0, lt = 0;
+      for (int w = cl; w < total; w += ncl, ++lt) {
+        const int ab = lt % NBUF;
+        mbar_wait_cluster(&tempty[ab], ((lt / NBUF) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + ab * TN;
+        for (int kb = 0; kb < 2 * g.kt; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a = smem_u32(smem + s * STAGE_BYTES), b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < TK / 32; ++k) mma(d, oz::sdesc(a + k * 32), oz::sdesc(b + k * 32), (kb | k) ? 1u : 0u);
+          commit_both(&empty[s]);
+        }
+        commit_both(&tfull[ab]);
+      }
+    }
+  } else {
+    const int q = warp & 3;                       // TMEM lane quarter = tile rows q*32 ..
+    const int ch = ((warp - 2) >> 2) * (TN / 2);  // column half
+    const uint32_t te_remote = mapa(smem_u32(&tempty[0]), 0);
+    unsigned lt = 0;
+    for (int w = cl; w < total; w += ncl, ++lt) {
+      int j, part, tm, tn;
+      pair_work_of(g, w, per, j, part, tm, tn);
+      const int ab = lt % NBUF;
+      mbar_wait(&tfull[ab], (lt / NBUF) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int p = c_oz_p[j];
+      const unsigned pm = c_oz_m[j];
+      const int row = tm * TM + rank * 128 + q * 32 + lane;
+      int8_t* out = g.r + ((size_t)(j * 2 + part) * g.mp + row) * g.np + tn * TN;
+#pragma unroll 1
+      for (int c0 = ch; c0 < ch + TN / 2; c0 += 64) {
+        uint32_t v[32], u[32];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ab * TN + c0;
+        OZ_LD32(v, ta);
+        OZ_LD32(u, ta + 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(oz::modc((int)v[4 * e + b], p, pm) & 0xff)) << (8 * b);
+          pk[e] = x;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + c0);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x |= ((uint32_t)(oz::modc((int)u[4 * e + b], p, pm) & 0xff)) << (8 * b);
+          pk[e] = x;
+        }
+        dst[2] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[3] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(te_remote + ab * 8)
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+}  // namespace oz2
+
+namespace oz {
 using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -313,17 +562,21 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
 // from 18-bit limbs of |x| in 32-bit integer arithmetic (Barrett reduction),
 // not from FP64 divisions.
 // ---------------------------------------------------------------------------
-// Residues of an integer-valued x (|x| < 2^53) for all 18 moduli in two
-// levels: y = x mod Q_g for the six triples Q_g = p_3g p_3g+1 p_3g+2 < 2^21
-// in FP64 (q = rint(x / Q) from the rounded reciprocal is floor or ceil, and
-// y = x - q Q is exact by FMA), then y mod p in FP32 (|y| <= 2^20: exact
-// integer arithmetic in a float); the low byte of r + 1.5 * 2^23 is r in
-// two's complement.  |r| <= 69 for every modulus.
+// Residues of an integer-valued x (|x| < 2^53) for all 16 moduli in two
+// levels: y = x mod Q_g for the eight pairs Q_g = p_2g p_2g+1 < 2^16 in FP64
+// (q = rint(x / Q) from the rounded reciprocal is floor or ceil, and
+// y = x - q Q is exact by FMA; |y| < 2^17), then the centred y mod p in FP32
+// (exact integer arithmetic in a float; the relative error 2^-23 of y / p
+// is far below the 1 / 2p distance of an odd p's quotient from a rounding
+// tie, so |r| <= (p - 1) / 2, and p = 256 divides exactly: r in [-128, 128],
+// whose byte is right mod 256); the low byte of r + 1.5 * 2^23 is r in two's
+// complement.
+constexpr int OZ_NGRP = OZ_NMOD / 2;
 constexpr double OZ_MAGIC = 6755399441055744.0;
 constexpr float OZ_MAGIC_F = 12582912.0f;
-__constant__ double c_oz_q[6], c_oz_qinv[6];
+__constant__ double c_oz_q[OZ_NGRP], c_oz_qinv[OZ_NGRP];
 __constant__ float c_oz_pf[OZ_NMOD], c_oz_pinvf[OZ_NMOD];
-__device__ __forceinline__ float reduce_triple(double x, int g) {
+__device__ __forceinline__ float reduce_pair(double x, int g) {
   const double q = fma(x, c_oz_qinv[g], OZ_MAGIC) - OZ_MAGIC;
   return (float)fma(-q, c_oz_q[g], x);
 }
@@ -389,15 +642,15 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
       xv[4 + e] = rint(ldexp(v.y, sh));
     }
 #pragma unroll 1
-    for (int g = 0; g < 6; ++g) {
+    for (int g = 0; g < OZ_NGRP; ++g) {
     float yv[8], ym[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      yv[e] = reduce_triple(xv[e], g);
+      yv[e] = reduce_pair(xv[e], g);
       ym[e] = yv[e] + OZ_MAGIC_F;
     }
 #pragma unroll
-    for (int t = 3 * g; t < 3 * g + 3; ++t) {
+    for (int t = 2 * g; t < 2 * g + 2; ++t) {
       uint32_t rw[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) rw[e] = res_word_f(yv[e], ym[e], t);
@@ -475,15 +728,15 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
     xv[4 + e] = rint(ldexp(v.y, sh));
   }
 #pragma unroll 1
-  for (int g = 0; g < 6; ++g) {
+  for (int g = 0; g < OZ_NGRP; ++g) {
     float yv[8], ym[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      yv[e] = reduce_triple(xv[e], g);
+      yv[e] = reduce_pair(xv[e], g);
       ym[e] = yv[e] + OZ_MAGIC_F;
     }
 #pragma unroll
-    for (int t = 3 * g; t < 3 * g + 3; ++t) {
+    for (int t = 2 * g; t < 2 * g + 2; ++t) {
       uint32_t rw[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) rw[e] = res_word_f(yv[e], ym[e], t);
@@ -497,27 +750,29 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
 }
 
 // ---------------------------------------------------------------------------
-// Reconstruction (CRT): x = sum_t r_t W_t mod M with W_t = y_t M_t,
-// M_t = M / p_t, y_t = M_t^-1 mod p_t (r_t need not be reduced: a multiple
-// of p_t times M_t is a multiple of M).  W_t (< M < 2^121) and M are split
-// into three pieces on the grids 2^0, 2^40, 2^80 (<= 41 bits), so each
-// partial sum S_k = sum_t r_t W_t,k is exact in binary64 (|r_t| <= 127:
-// 7 + 41 + log2(18) < 53 bits); q = rint(S / M) (|q| < 2^12) and
-// D_k = S_k - q M_k are exact, and x = D_2 + D_1 + D_0 is the centred
-// representative (|x| << M / 2 by the choice of KB).
+// Reconstruction (CRT): x = sum_t c_t W_t mod M with W_t = y_t M_t,
+// M_t = M / p_t, y_t = M_t^-1 mod p_t, c_t = r_t - floor(p_t / 2) the
+// centred residue (|c_t| <= 128; any representative works: a multiple of
+// p_t times M_t is a multiple of M).  W_t (< M < 2^126) and M are split into
+// four pieces on the grids 2^0, 2^32, 2^64, 2^96 (<= 32 bits), so each
+// partial sum S_k = sum_t c_t W_t,k is exact in binary64 (8 + 32 + 4 bits);
+// q = rint(S / M) (|q| <= 2^11) and D_k = S_k - q M_k are exact, and
+// x = D_3 + D_2 + D_1 + D_0 is the centred representative (|x| < M / 2 by
+// the choice of KB).
 // ---------------------------------------------------------------------------
+constexpr int OZ_NPC = 4;
 struct CrtConst {
-  double w[OZ_NMOD][3];  // pieces of W_t
-  double mp[3];          // pieces of M
-  double m_inv;          // 1 / M
+  double w[OZ_NMOD][OZ_NPC];  // pieces of W_t
+  double mp[OZ_NPC];          // pieces of M
+  double m_inv;               // 1 / M
+  double bias[OZ_NMOD];       // 2^52 + 2^31 + floor(p_t / 2)
 };
 __constant__ CrtConst c_crt;
 
-// int8 (two's complement byte) -> double without an int -> fp64 conversion:
-// 2^52 + 2^31 + v as the bit pattern, minus the bias
-__device__ __forceinline__ double byte_to_double(uint32_t word, int e) {
-  const int v = (int)(int8_t)(word >> (8 * e));
-  return __hiloint2double(0x43300000, (int)((unsigned)v ^ 0x80000000u)) - 4503601774854144.0;
+// unsigned byte r -> centred residue r - floor(p / 2) as a double without an
+// int -> fp64 conversion: 2^52 + 2^31 + r as the bit pattern, minus the bias
+__device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bias) {
+  return __hiloint2double(0x43300000, (int)(((word >> (8 * e)) & 0xffu) | 0x80000000u)) - bias;
 }
 
 __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
@@ -536,28 +791,30 @@ __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const 
     wr[t] = __ldg(reinterpret_cast<const uint32_t*>(rre + (size_t)t * ps));
     wi[t] = __ldg(reinterpret_cast<const uint32_t*>(rim + (size_t)t * ps));
   }
-  double s[8][3];
+  double s[8][OZ_NPC];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) s[e][0] = s[e][1] = s[e][2] = 0.0;
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int k = 0; k < OZ_NPC; ++k) s[e][k] = 0.0;
 #pragma unroll
   for (int t = 0; t < OZ_NMOD; ++t) {
-    const double w0 = c_crt.w[t][0], w1 = c_crt.w[t][1], w2 = c_crt.w[t][2];
+    const double bias = c_crt.bias[t];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const double u = byte_to_double(e < 4 ? wr[t] : wi[t], e & 3);
-      s[e][0] = fma(u, w0, s[e][0]);
-      s[e][1] = fma(u, w1, s[e][1]);
-      s[e][2] = fma(u, w2, s[e][2]);
+      const double u = byte_to_double(e < 4 ? wr[t] : wi[t], e & 3, bias);
+#pragma unroll
+      for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, c_crt.w[t][k], s[e][k]);
     }
   }
   double vr[4], vi[4];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const double q = rint((s[e][2] + s[e][1] + s[e][0]) * c_crt.m_inv);
+    const double q = rint((((s[e][3] + s[e][2]) + s[e][1]) + s[e][0]) * c_crt.m_inv);
+    const double d3 = fma(-q, c_crt.mp[3], s[e][3]);
     const double d2 = fma(-q, c_crt.mp[2], s[e][2]);
     const double d1 = fma(-q, c_crt.mp[1], s[e][1]);
     const double d0 = fma(-q, c_crt.mp[0], s[e][0]);
-    const double v = (d2 + d1) + d0;
+    const double v = ((d3 + d2) + d1) + d0;
     if (e < 4)
       vr[e] = v;
     else
@@ -581,25 +838,26 @@ static int crt_init() {
   u128 m = 1;
   for (int t = 0; t < OZ_NMOD; ++t) m *= (u128)h_oz_p[t];
   auto piece = [](u128 v, int k) {
-    const u128 part = k < 2 ? (v >> (40 * k)) & (((u128)1 << 40) - 1) : (v >> 80);
-    return std::ldexp((double)(unsigned long long)part, 40 * k);  // <= 41 bits: exact
+    const u128 part = k < OZ_NPC - 1 ? (v >> (32 * k)) & (((u128)1 << 32) - 1) : (v >> (32 * k));
+    return std::ldexp((double)(unsigned long long)part, 32 * k);  // <= 32 bits: exact
   };
   for (int t = 0; t < OZ_NMOD; ++t) {
     const int p = h_oz_p[t];
     const u128 mt = m / (u128)p;
     const int r = (int)(mt % (u128)p);
     int y = 1;
-    while ((r * y) % p != 1) ++y;  // p <= 128: direct search
+    while ((r * y) % p != 1) ++y;  // p <= 256: direct search
     const u128 w = mt * (u128)y;  // < M
-    for (int k = 0; k < 3; ++k) h.w[t][k] = piece(w, k);
+    for (int k = 0; k < OZ_NPC; ++k) h.w[t][k] = piece(w, k);
+    h.bias[t] = 4503601774854144.0 + (double)(p / 2);
   }
-  for (int k = 0; k < 3; ++k) h.mp[k] = piece(m, k);
-  h.m_inv = 1.0 / (h.mp[2] + h.mp[1] + h.mp[0]);
+  for (int k = 0; k < OZ_NPC; ++k) h.mp[k] = piece(m, k);
+  h.m_inv = 1.0 / (((h.mp[3] + h.mp[2]) + h.mp[1]) + h.mp[0]);
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
-  double qd[6], qi[6];
+  double qd[OZ_NGRP], qi[OZ_NGRP];
   float pf[OZ_NMOD], pif[OZ_NMOD];
-  for (int g = 0; g < 6; ++g) {
-    qd[g] = (double)h_oz_p[3 * g] * h_oz_p[3 * g + 1] * h_oz_p[3 * g + 2];  // < 2^21
+  for (int g = 0; g < OZ_NGRP; ++g) {
+    qd[g] = (double)h_oz_p[2 * g] * h_oz_p[2 * g + 1];  // < 2^16
     qi[g] = 1.0 / qd[g];
   }
   for (int t = 0; t < OZ_NMOD; ++t) {
@@ -755,6 +1013,24 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
 }
 
 static int g_oz_sms = 0;
+// residue-GEMM kernel: 1 = single-CTA 128 x 256 tiles (default), 2 = the
+// CTA-pair kernel (ZT_OZ_CTA=2 or zt_oz_set_cta(2); needs mp % 256 == 0;
+// measured 5-20% slower)
+static int g_oz_cta = 0;
+int oz_set_cta(int c) {
+  if (c != 0 && c != 1 && c != 2) return fail(ZT_EINVAL, "zt_oz_set_cta: 0 (default), 1 or 2");
+  g_oz_cta = c;
+  return ZT_OK;
+}
+static int oz_cta() {
+  if (g_oz_cta) return g_oz_cta;
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("ZT_OZ_CTA");
+    env = (e && e[0] == '2') ? 2 : 1;
+  }
+  return env;
+}
 
 // CUDA-event timing of every residue-GEMM launch while profiling is on
 // (eager steps only; zt_profile_enable / zt_oz_profile_read)
@@ -776,15 +1052,17 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   using namespace oz;
   if (nmod < 1 || nmod > OZ_NMOD || mp % TM || np % TN || kp % TK || (lower && mp != np))
     return fail(ZT_EINVAL, "oz_modgemm: bad shape");
+  const bool pair = oz_cta() == 2 && mp % oz2::TM == 0;
   CUtensorMap ma, mb;
-  int rc = map_i8(&ma, a, (long long)nmod * 3 * mp, kp, TM);
-  if (!rc) rc = map_i8(&mb, b, (long long)nmod * 2 * np, kp, TN);
+  int rc = map_i8(&ma, a, (long long)nmod * 3 * mp, kp, 128);
+  if (!rc) rc = map_i8(&mb, b, (long long)nmod * 2 * np, kp, pair ? oz2::TN / 2 : TN);
   if (rc) return rc;
   if (!g_oz_sms) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_oz_sms, cudaDevAttrMultiProcessorCount, dev);
     ZT_CUDA_CHECK(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    ZT_CUDA_CHECK(cudaFuncSetAttribute(oz2::k_oz_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, oz2::SMEM));
   }
   GemmArgs g;
   g.nmod = nmod;
@@ -795,8 +1073,12 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   g.mp = mp;
   g.np = np;
   g.r = r;
-  const int per = lower ? lower_count(g.mt) : g.mt * g.nt;
-  const int grid = std::min(nmod * per, g_oz_sms);
+  if (pair) {
+    g.mt = mp / oz2::TM;
+    g.nt = np / oz2::TN;
+  }
+  const int per = pair ? 2 * (lower ? oz2::lower_count(g.mt) : g.mt * g.nt) : (lower ? lower_count(g.mt) : g.mt * g.nt);
+  const int grid = pair ? 2 * std::min(nmod * per, g_oz_sms / 2) : std::min(nmod * per, g_oz_sms);
   OzEv* ev = nullptr;
   if (g_oz_prof) {
     if (g_oz_used == g_oz_ev.size()) {
@@ -809,7 +1091,10 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
     ev->lower = lower;
     cudaEventRecord(ev->e0, st);
   }
-  k_oz_gemm<<<grid, THREADS, SMEM, st>>>(ma, mb, g);
+  if (pair)
+    oz2::k_oz_gemm2<<<grid, oz2::THREADS, oz2::SMEM, st>>>(ma, mb, g);
+  else
+    k_oz_gemm<<<grid, THREADS, SMEM, st>>>(ma, mb, g);
   ZT_LAUNCHED();
   if (ev) cudaEventRecord(ev->e1, st);
   ZT_CUDA_CHECK(cudaGetLastError());
@@ -829,6 +1114,8 @@ extern "C" int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, co
   return zt::oz_modgemm(nmod, mp, np, kp, static_cast<const int8_t*>(a), static_cast<const int8_t*>(b),
                         static_cast<int8_t*>(r), lower, (cudaStream_t)stream);
 }
+
+extern "C" int zt_oz_set_cta(int c) { return zt::oz_set_cta(c); }
 
 extern "C" int zt_oz_moduli(int* out, int cap) { return zt::oz_moduli(out, cap); }
 

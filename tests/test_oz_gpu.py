@@ -34,10 +34,27 @@ def _moduli(lib):
     return [buf[i] for i in range(k)]
 
 
-@pytest.mark.parametrize("nmod,mp,np_,kp,lower", [(1, 128, 256, 64, 0), (3, 256, 512, 320, 0), (18, 256, 256, 256, 0),
-                                                  (2, 512, 512, 192, 1), (4, 768, 768, 128, 1)])
-def test_residue_gemm_exact(lib, nmod, mp, np_, kp, lower):
-    """R_j = (A_re B_re^T + A_-im B_im^T, A_re B_im^T + A_im B_re^T) mod p_j, exactly."""
+@pytest.mark.parametrize("nmod,mp,np_,kp,lower", [(1, 128, 256, 64, 0), (3, 256, 512, 320, 0), (16, 256, 256, 256, 0),
+                                                  (2, 512, 512, 192, 1), (4, 768, 768, 128, 1),
+                                                  (5, 1024, 1024, 256, 1), (3, 768, 512, 448, 0)])
+@pytest.mark.parametrize("cta", [1, 2])
+def test_residue_gemm_exact(lib, nmod, mp, np_, kp, lower, cta):
+    """R_j = (A_re B_re^T + A_-im B_im^T, A_re B_im^T + A_im B_re^T) + p_j // 2 mod p_j, exactly,
+    for the single-CTA 128 x 256 kernel and the CTA-pair (cta_group::2) kernel (Re and Im as
+    separate 256 x 256 real tiles with K doubled)."""
+    assert lib.zt_oz_set_cta(cta) == 0
+    try:
+        _check_residue_gemm(lib, nmod, mp, np_, kp, lower)
+    finally:
+        lib.zt_oz_set_cta(0)
+
+
+def test_set_cta_rejects_bad_values(lib):
+    assert lib.zt_oz_set_cta(3) != 0
+    assert lib.zt_oz_set_cta(-1) != 0
+
+
+def _check_residue_gemm(lib, nmod, mp, np_, kp, lower):
     P = _moduli(lib)
     rng = np.random.default_rng(nmod * 7 + mp)
     a = np.stack([rng.integers(-(P[j] // 2), P[j] // 2 + 1, (3, mp, kp)) for j in range(nmod)]).astype(np.int8)
@@ -48,15 +65,16 @@ def test_residue_gemm_exact(lib, nmod, mp, np_, kp, lower):
     rc = lib.zt_oz_modgemm(nmod, mp, np_, kp, ad.data_ptr(), bd.data_ptr(), r.data_ptr(), lower,
                            torch.cuda.current_stream().cuda_stream)
     assert rc == 0
-    rh = r.cpu().numpy().astype(np.int64)
+    rh = r.cpu().numpy().view(np.uint8).astype(np.int64)
     a64, b64 = a.astype(np.int64), b.astype(np.int64)
     mask = ((np.arange(mp)[:, None] // 128) >= (np.arange(np_)[None, :] // 128)) if lower else np.ones((mp, np_), bool)
     for j in range(nmod):
         re = a64[j, 0] @ b64[j, 0].T + a64[j, 2] @ b64[j, 1].T
         im = a64[j, 0] @ b64[j, 1].T + a64[j, 1] @ b64[j, 0].T
         for ref, got in ((re, rh[j, 0]), (im, rh[j, 1])):
-            assert np.all((np.mod(ref - got, P[j]) == 0)[mask])
-            assert np.all((got[mask] >= 0) & (got[mask] < P[j]))  # epilogue residues in [0, p)
+            # epilogue residues: (product + p // 2) mod p as unsigned bytes in [0, p)
+            assert np.all((np.mod(ref + P[j] // 2 - got, P[j]) == 0)[mask])
+            assert np.all((got[mask] >= 0) & (got[mask] < P[j]))
 
 
 def _oz(lib, a, b, bmode=0, lower=0):
