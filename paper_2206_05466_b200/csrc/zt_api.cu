@@ -16,6 +16,10 @@
 namespace zt {
 
 std::atomic<int64_t> g_launches{0};
+bool g_pdl = [] {
+  const char* e = getenv("ZT_PDL");
+  return !(e && e[0] == '0');
+}();
 static thread_local std::string t_err;
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "../../include/zt.h"
 
@@ -43,6 +44,40 @@ int cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 #define ZT_LAUNCHED() ::zt::g_launches.fetch_add(1, std::memory_order_relaxed)
+
+// Programmatic dependent launch along the step's main chain (conversion ->
+// residue GEMM -> reconstruction -> update): a kernel launched by launch_pdl
+// may start while its stream predecessor drains (its blocks are scheduled,
+// set up TMEM / barriers / tensor-map prefetches) and MUST execute
+// pdl_wait() before touching memory the predecessor writes or reads (the
+// wait returns once every predecessor grid completed and flushed; completion
+// is transitive along the chain).  pdl_trigger() lets the dependent launch
+// early.  ZT_PDL=0 turns the attribute off (plain stream order).
+extern bool g_pdl;
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef ZT_PDL_TRIGGER
+#define ZT_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if ZT_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // progressive final update (zt_gemm.cu, FusedArgs::prog): W_{n+1} rows are
 // published block by block for an overlapped device-to-host copy

@@ -1206,6 +1206,7 @@ __global__ void __launch_bounds__(256) k_final_commutator(int n, const double* _
   __shared__ double2 tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  pdl_wait();
   for (int r = ty; r < 32; r += 8) {
     const int i = bx + r, j = by + tx;  // a[bx.., by..], read transposed below
     tile[r][tx] = (i < n && j < n) ? ld2(a + ((size_t)i * n + j) * 2) : make_double2(0, 0);
@@ -1225,7 +1226,7 @@ __global__ void __launch_bounds__(256) k_final_commutator(int n, const double* _
 
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st) {
   dim3 grid((n + 31) / 32, (n + 31) / 32);
-  k_final_commutator<<<grid, 256, 0, st>>>(n, a, wn, h, out);
+  ZT_CUDA_CHECK(launch_pdl(k_final_commutator, grid, dim3(256), 0, st, n, a, wn, h, out));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -1254,6 +1255,7 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
   while (I * (I + 1) / 2 > (int)blockIdx.x) --I;
   const int J = blockIdx.x - I * (I + 1) / 2;
   const int R = I * 32, C = J * 32;
+  pdl_wait();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const bool same_tile = (R / BM) == (C / BM);  // b computed on both sides
   double rmax = 0.0, cmax = 0.0;
@@ -1365,16 +1367,10 @@ int update_pairs(int n, const double* a, const double* bm, double* out, const do
                  cudaStream_t st) {
   const int t32 = (n + 31) / 32;
   const int nb = t32 * (t32 + 1) / 2;
-  if (xprev && wn)
-    k_update_pairs<true, true><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
-  else if (xprev)
-    k_update_pairs<true, false><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
-  else if (wn)
-    k_update_pairs<false, true><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
-  else
-    k_update_pairs<false, false><<<nb, 256, 0, st>>>(n, a, bm, out, base, xprev, wn, hh, qq, resid, cons);
+  auto k = xprev ? (wn ? k_update_pairs<true, true> : k_update_pairs<true, false>)
+                 : (wn ? k_update_pairs<false, true> : k_update_pairs<false, false>);
+  ZT_CUDA_CHECK(launch_pdl(k, dim3(nb), dim3(256), 0, st, n, a, bm, out, base, xprev, wn, hh, qq, resid, cons));
   ZT_LAUNCHED();
-  ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
 }
 

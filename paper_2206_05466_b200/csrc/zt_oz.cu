@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "zt_common.cuh"
@@ -174,11 +175,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
+  }
+  pdl_trigger();
+  pdl_wait();  // operands from the conversions; R still read by the previous reconstruction
 
   if (warp == 0) {
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
       unsigned it = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         int j, tm, tn;
@@ -593,6 +598,14 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 
 // exponent shift that puts amax in [2^(KB-1), 2^KB); 0 for an all-zero line
 __device__ __forceinline__ int oz_shift(double amax, int kb) { return amax > 0.0 ? kb - 1 - ilogb(amax) : 0; }
+// 2^sh as two normal factors (sh in [-971, 1126]): v * s.x * s.y == ldexp(v, sh)
+// whenever the result is >= 2^-1022 (scaling is exact; a smaller result
+// rounds to 0 either way under rint), at two DMULs instead of ldexp's
+// special-case chain
+__device__ __forceinline__ double2 oz_scale2(int sh) {
+  const int a = sh / 2, b = sh - a;
+  return make_double2(__hiloint2double((a + 1023) << 20, 0), __hiloint2double((b + 1023) << 20, 0));
+}
 
 // A-type rows: planes (re, im, -im) of row i; mode 1 = the B layout of a
 // skew-Hermitian S (B[j][k] = S[k][j] = -conj(S[j][k]) off the diagonal):
@@ -600,13 +613,28 @@ __device__ __forceinline__ int oz_shift(double amax, int kb) { return amax > 0.0
 // thread (one 32-bit store per plane).
 // mode 2: both at once from one read (A planes into out, skew-B planes into
 // out2; the row scale is shared since |-conj(v)| = |v|).
-__global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __restrict__ src, int64_t ld, int mp,
+// conversions: <= 80 registers (3 blocks of 256 per SM) measured 5% faster
+#ifndef OZ_CONV_MINB
+#define OZ_CONV_MINB 3
+#endif
+// reconstruction: 2 output columns per thread at <= 64 registers (4 blocks
+// of 256 per SM) measured 2% faster per step than 4 columns at 106
+// registers (the FP64 chains need the extra warps to hide the loads)
+#ifndef OZ_RECON_MINB
+#define OZ_RECON_MINB 4
+#endif
+#ifndef OZ_RECON_COLS
+#define OZ_RECON_COLS 2  // output columns per thread (4 or 2)
+#endif
+__global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_rows(int n, const double* __restrict__ src, int64_t ld, int mp,
                                                       int kp, int nmod, int kb, int mode, int8_t* out,
                                                       int* __restrict__ shift, int8_t* out2 = nullptr,
                                                       int* __restrict__ shift2 = nullptr) {
   const int i = blockIdx.x;
   __shared__ double red[8];
   double amax = 0.0;
+  pdl_trigger();
+  pdl_wait();
   if (i < n) {
     // all of this thread's loads in flight at once (the max chain would
     // otherwise serialise them: the dominant stall)
@@ -629,6 +657,7 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
   amax = red[0];
   for (int q = 1; q < 8; ++q) amax = fmax(amax, red[q]);
   const int sh = oz_shift(amax, kb);
+  const double2 sc = oz_scale2(sh);
   if (threadIdx.x == 0 && shift) shift[i] = sh;
   if (threadIdx.x == 0 && shift2) shift2[i] = sh;
   for (int k0 = threadIdx.x * 4; k0 < kp; k0 += blockDim.x * 4) {
@@ -638,8 +667,8 @@ __global__ void __launch_bounds__(256) k_oz_conv_rows(int n, const double* __res
       const int k = k0 + e;
       double2 v = make_double2(0.0, 0.0);
       if (i < n && k < n) v = ld2(src + ((size_t)i * ld + k) * 2);
-      xv[e] = rint(ldexp(v.x, sh));
-      xv[4 + e] = rint(ldexp(v.y, sh));
+      xv[e] = rint(v.x * sc.x * sc.y);
+      xv[4 + e] = rint(v.y * sc.x * sc.y);
     }
 #pragma unroll 1
     for (int g = 0; g < OZ_NGRP; ++g) {
@@ -703,7 +732,7 @@ __global__ void __launch_bounds__(256) k_oz_colmax(int n, const double* __restri
 
 // then 32 (k) x 32 (j) tiles through shared memory; thread t produces output
 // row j = j0 + t / 8, k = k0 + 4 (t % 8) .. +3 (one 32-bit store per plane)
-__global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __restrict__ x, int64_t ld, int np,
+__global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_cols(int n, const double* __restrict__ x, int64_t ld, int np,
                                                       int kp, int nmod, int kb,
                                                       const unsigned long long* __restrict__ colmax, int8_t* out,
                                                       int* __restrict__ shift) {
@@ -719,13 +748,14 @@ __global__ void __launch_bounds__(256) k_oz_conv_cols(int n, const double* __res
   const int j = j0 + jj;
   const double m = (j < n) ? __longlong_as_double((long long)colmax[j]) : 0.0;
   const int sh = oz_shift(m, kb);
+  const double2 sc = oz_scale2(sh);
   if (blockIdx.y == 0 && kk == 0 && shift) shift[j] = sh;
   double xv[8];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const double2 v = tl[kk + e][jj];
-    xv[e] = rint(ldexp(v.x, sh));
-    xv[4 + e] = rint(ldexp(v.y, sh));
+    xv[e] = rint(v.x * sc.x * sc.y);
+    xv[4 + e] = rint(v.y * sc.x * sc.y);
   }
 #pragma unroll 1
   for (int g = 0; g < OZ_NGRP; ++g) {
@@ -772,56 +802,62 @@ __constant__ CrtConst c_crt;
 // unsigned byte r -> centred residue r - floor(p / 2) as a double without an
 // int -> fp64 conversion: 2^52 + 2^31 + r as the bit pattern, minus the bias
 __device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bias) {
-  return __hiloint2double(0x43300000, (int)(((word >> (8 * e)) & 0xffu) | 0x80000000u)) - bias;
+  // one byte permute: byte e of word, then 0x00, 0x00, 0x80
+  return __hiloint2double(0x43300000, (int)__byte_perm(word, 0x80000000u, 0x7540u | e)) - bias;
 }
 
-__global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
+__global__ void __launch_bounds__(256, OZ_RECON_MINB) k_oz_recon(int m, int n, int nmod, const int8_t* __restrict__ r, int mp,
                                                   int np, const int* __restrict__ rs, const int* __restrict__ cs,
                                                   double* c, int64_t ldc, int lower) {
   const int i = blockIdx.y;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
+  pdl_trigger();
+  pdl_wait();
   if (i >= m || j0 >= n) return;
   if (lower && (j0 >> 7) > (i >> 7)) return;
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
+  // C columns per thread (C = 4: one 32-bit word per modulus and plane; C = 2: 16-bit)
+  constexpr int C = OZ_RECON_COLS;
+  using word_t = typename std::conditional<C == 4, uint32_t, unsigned short>::type;
   const int8_t* rre = r + (size_t)i * np + j0;
   const int8_t* rim = rre + (size_t)mp * np;
-  uint32_t wr[OZ_NMOD], wi[OZ_NMOD];
+  word_t wr[OZ_NMOD], wi[OZ_NMOD];
 #pragma unroll
   for (int t = 0; t < OZ_NMOD; ++t) {
-    wr[t] = __ldg(reinterpret_cast<const uint32_t*>(rre + (size_t)t * ps));
-    wi[t] = __ldg(reinterpret_cast<const uint32_t*>(rim + (size_t)t * ps));
+    wr[t] = __ldg(reinterpret_cast<const word_t*>(rre + (size_t)t * ps));
+    wi[t] = __ldg(reinterpret_cast<const word_t*>(rim + (size_t)t * ps));
   }
-  double s[8][OZ_NPC];
+  double s[2 * C][OZ_NPC];
 #pragma unroll
-  for (int e = 0; e < 8; ++e)
+  for (int e = 0; e < 2 * C; ++e)
 #pragma unroll
     for (int k = 0; k < OZ_NPC; ++k) s[e][k] = 0.0;
 #pragma unroll
   for (int t = 0; t < OZ_NMOD; ++t) {
     const double bias = c_crt.bias[t];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const double u = byte_to_double(e < 4 ? wr[t] : wi[t], e & 3, bias);
+    for (int e = 0; e < 2 * C; ++e) {
+      const double u = byte_to_double(e < C ? wr[t] : wi[t], e % C, bias);
 #pragma unroll
       for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, c_crt.w[t][k], s[e][k]);
     }
   }
-  double vr[4], vi[4];
+  double vr[C], vi[C];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int e = 0; e < 2 * C; ++e) {
     const double q = rint((((s[e][3] + s[e][2]) + s[e][1]) + s[e][0]) * c_crt.m_inv);
     const double d3 = fma(-q, c_crt.mp[3], s[e][3]);
     const double d2 = fma(-q, c_crt.mp[2], s[e][2]);
     const double d1 = fma(-q, c_crt.mp[1], s[e][1]);
     const double d0 = fma(-q, c_crt.mp[0], s[e][0]);
-    const double v = ((d3 + d2) + d1) + d0;
-    if (e < 4)
-      vr[e] = v;
+    const double x = ((d3 + d2) + d1) + d0;
+    if (e < C)
+      vr[e] = x;
     else
-      vi[e - 4] = v;
+      vi[e - C] = x;
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < C; ++e) {
     const int j = j0 + e;
     if (j < n && !(lower && (j >> 7) > (i >> 7))) {
       const int sh = -(rs[i] + cs[j]);
@@ -830,7 +866,11 @@ __global__ void __launch_bounds__(256) k_oz_recon(int m, int n, int nmod, const 
   }
 }
 
-constexpr int OZ_RECON_SMEM = 0;
+static cudaError_t launch_recon(int m, int n, int nmod, const int8_t* r, int mp, int np, const int* rs, const int* cs,
+                                double* c, int64_t ldc, int lower, cudaStream_t st) {
+  const dim3 grid((n + 256 * OZ_RECON_COLS - 1) / (256 * OZ_RECON_COLS), m);
+  return launch_pdl(k_oz_recon, grid, dim3(256), 0, st, m, n, nmod, r, mp, np, rs, cs, c, ldc, lower);
+}
 static bool g_crt_ready = false;
 static int crt_init() {
   typedef unsigned __int128 u128;
@@ -905,10 +945,12 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   int* rsh = reinterpret_cast<int*>(rres + (size_t)OZ_NMOD * 2 * p * p);
   int* csh = rsh + p;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(csh + p);
-  k_oz_conv_rows<<<p, 256, 0, st>>>(n, a, lda, p, p, OZ_NMOD, kb, 0, ares, rsh);
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, a, lda, p, p, OZ_NMOD, kb, 0, ares, rsh,
+                           nullptr, nullptr));
   ZT_LAUNCHED();
   if (bmode == 1) {
-    k_oz_conv_rows<<<p, 256, 0, st>>>(n, b, ldb, p, p, OZ_NMOD, kb, 1, bres, csh);
+    ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, b, ldb, p, p, OZ_NMOD, kb, 1, bres, csh,
+                             nullptr, nullptr));
     ZT_LAUNCHED();
   } else {
     ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * p, st));
@@ -920,8 +962,7 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   }
   int rc = oz_modgemm(OZ_NMOD, p, p, p, ares, bres, rres, lower, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc,
-                                                                       lower);
+  ZT_CUDA_CHECK(launch_recon(n, n, OZ_NMOD, rres, p, p, rsh, csh, c, ldc, lower, st));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -986,8 +1027,8 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   int* sa = sx + pd;                                // a rows
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(sa + 2 * pd);
   // P: A layout and skew-B layout in one pass
-  k_oz_conv_rows<<<pd, 256, 0, st>>>(n, p, n, pd, pd, OZ_NMOD, kb, gemm1_only ? 0 : 2, ares, sp,
-                                     gemm1_only ? nullptr : bp, nullptr);
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, p, (int64_t)n, pd, pd, OZ_NMOD, kb,
+                           gemm1_only ? 0 : 2, ares, sp, gemm1_only ? nullptr : bp, nullptr));
   ZT_LAUNCHED();
   if (x_join) {
     ZT_CUDA_CHECK(cudaStreamWaitEvent(st, x_join, 0));
@@ -998,15 +1039,15 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   (void)cmax;
   int rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bx, rres, 0, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0);
+  ZT_CUDA_CHECK(launch_recon(n, n, OZ_NMOD, rres, pd, pd, sp, sx, a, n, 0, st));
   ZT_LAUNCHED();
   if (gemm1_only) return final_commutator(n, a, wn, hh, out, st);
-  k_oz_conv_rows<<<pd, 256, 0, st>>>(n, a, n, pd, pd, OZ_NMOD, kb, 0, ares, sa);
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, (const double*)a, (int64_t)n, pd, pd,
+                           OZ_NMOD, kb, 0, ares, sa, nullptr, nullptr));
   ZT_LAUNCHED();
   rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bp, rres, 1, st);
   if (rc) return rc;
-  k_oz_recon<<<dim3((n + 1023) / 1024, n), 256, OZ_RECON_SMEM, st>>>(n, n, OZ_NMOD, rres, pd, pd, sa, sp, bbuf, n,
-                                                                       1);
+  ZT_CUDA_CHECK(launch_recon(n, n, OZ_NMOD, rres, pd, pd, sa, sp, bbuf, n, 1, st));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return update_pairs(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons, st);
@@ -1094,7 +1135,7 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   if (pair)
     oz2::k_oz_gemm2<<<grid, oz2::THREADS, oz2::SMEM, st>>>(ma, mb, g);
   else
-    k_oz_gemm<<<grid, THREADS, SMEM, st>>>(ma, mb, g);
+    ZT_CUDA_CHECK(launch_pdl(k_oz_gemm, dim3(grid), dim3(THREADS), SMEM, st, ma, mb, g));
   ZT_LAUNCHED();
   if (ev) cudaEventRecord(ev->e1, st);
   ZT_CUDA_CHECK(cudaGetLastError());
