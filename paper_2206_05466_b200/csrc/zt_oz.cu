@@ -309,9 +309,13 @@ namespace oz2 {
 constexpr int TM = 256, TN = 256, TK = oz::TK;  // pair tile; TK in bytes
 constexpr int A_BYTES = 128 * TK;               // one CTA's 128 rows of an A plane
 constexpr int B_BYTES = (TN / 2) * TK;          // one CTA's 128 columns of a B plane
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+#ifndef OZ2_KPS
+#define OZ2_KPS 2  // K blocks per pipeline stage (amortises the MMA thread's barrier work)
+#endif
+constexpr int KPS = OZ2_KPS;
+constexpr int STAGE_BYTES = KPS * (A_BYTES + B_BYTES);  // [A kb0 | B kb0 | A kb1 | B kb1 ...]
 #ifndef OZ2_STAGES
-#define OZ2_STAGES 12
+#define OZ2_STAGES (12 / OZ2_KPS)
 #endif
 constexpr int STAGES = OZ2_STAGES;
 constexpr int NBUF = 2;  // TMEM accumulator buffers of TN columns
@@ -439,15 +443,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int ra0 = (j * 3 + part) * g.mp + tm * TM + rank * 128;
         const int ra1 = (j * 3 + (part ? 0 : 2)) * g.mp + tm * TM + rank * 128;
         const int rb0 = (j * 2) * g.np + tn * TN + rank * (TN / 2), rb1 = rb0 + g.np;
-        for (int kb = 0; kb < 2 * g.kt; ++kb, ++it) {
+        for (int kb = 0; kb < 2 * g.kt; kb += KPS, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
           if (rank == 0) oz::mbar_arrive_tx(&full[s], 2 * STAGE_BYTES);
-          const bool h1 = kb >= g.kt;
-          const int kc = (h1 ? kb - g.kt : kb) * TK;
-          tma2d_pair(st, &ma, kc, h1 ? ra1 : ra0, fb0 + s * 8);
-          tma2d_pair(st + A_BYTES, &mb, kc, h1 ? rb1 : rb0, fb0 + s * 8);
+#pragma unroll
+          for (int u = 0; u < KPS; ++u) {
+            const int kbu = kb + u;
+            const bool h1 = kbu >= g.kt;
+            const int kc = (h1 ? kbu - g.kt : kbu) * TK;
+            unsigned char* su = st + u * (A_BYTES + B_BYTES);
+            tma2d_pair(su, &ma, kc, h1 ? ra1 : ra0, fb0 + s * 8);
+            tma2d_pair(su + A_BYTES, &mb, kc, h1 ? rb1 : rb0, fb0 + s * 8);
+          }
         }
       }
       // drain: every issued stage consumed before this CTA may exit
@@ -461,13 +470,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait_cluster(&tempty[ab], ((lt / NBUF) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + ab * TN;
-        for (int kb = 0; kb < 2 * g.kt; ++kb, ++it) {
+        for (int kb = 0; kb < 2 * g.kt; kb += KPS, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a = smem_u32(smem + s * STAGE_BYTES), b = a + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < TK / 32; ++k) mma(d, oz::sdesc(a + k * 32), oz::sdesc(b + k * 32), (kb | k) ? 1u : 0u);
+          for (int u = 0; u < KPS; ++u) {
+            const uint32_t a = smem_u32(smem + s * STAGE_BYTES + u * (A_BYTES + B_BYTES)), b = a + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < TK / 32; ++k)
+              mma(d, oz::sdesc(a + k * 32), oz::sdesc(b + k * 32), (kb | u | k) ? 1u : 0u);
+          }
           commit_both(&empty[s]);
         }
         commit_both(&tfull[ab]);

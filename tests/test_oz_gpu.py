@@ -127,6 +127,41 @@ def test_zero_and_scaled_inputs(lib):
     np.testing.assert_array_equal(c2, c * 2.0**-260)
 
 
+def test_extreme_row_scales(lib):
+    """Rows / columns whose maxima span the whole binary64 range (subnormal to
+    ~1e300): the two-factor power-of-two scaling keeps them exact, so each
+    scaled row of the product equals the unscaled product row times the same
+    power of two (bitwise), and tiny rows far below the rest do not lose
+    accuracy (row scaling is per row)."""
+    n = 256
+    rng = np.random.default_rng(5)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    b = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    dev = torch.device("cuda:0")
+    c = _oz(lib, torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
+    rows = {3: -1060, 17: -1000, 40: -600, 99: 900, 150: 1000}  # 2^-1060: subnormal entries
+    cols = {5: -1000, 77: 980}
+    a2, b2 = a.copy(), b.copy()
+    for i, e in rows.items():
+        a2[i] = a[i] * 2.0**e
+    for j, e in cols.items():
+        b2[:, j] = b[:, j] * 2.0**e
+    c2 = _oz(lib, torch.from_numpy(a2).to(dev), torch.from_numpy(b2).to(dev))
+    for i, e in rows.items():
+        for j in range(n):
+            ej = e + cols.get(j, 0)
+            if -1000 <= ej <= 1000 and e > -1060:  # results stay normal: exactly the scaled product
+                assert c2[i, j] == c[i, j] * 2.0**ej, (i, j)
+    # subnormal inputs: the row is still computed from its own scale (relative accuracy of
+    # the subnormal entries themselves, ~2^-1074 absolute)
+    ref = (a2[3].astype(np.clongdouble) @ b2.astype(np.clongdouble)).astype(np.complex128)
+    sub = np.ones(n, bool)
+    sub[77] = False  # column 77 (x 2^980) lifts row 3 back into the normal range
+    assert np.abs(c2[3, sub] - ref[sub]).max() <= 2.0**-1072
+    assert abs(c2[3, 77] - ref[77]) <= 4e-16 * abs(ref[77])
+    assert np.all(np.isfinite(c2))
+
+
 def test_native_dmma_step_still_matches_reference():
     """ZT_GEMM_ALGO=3m (native FP64 DMMA products) in a fresh process: cfg 1
     W10 and iteration counts against the reference's golden run."""
