@@ -188,6 +188,13 @@ def load_fp64_peak():
                           if best else "nominal 148 SM x 128 flop/clk x 1.965 GHz")
 
 
+def load_int8_burst():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_int8_peaks.json")))["burst_tops"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_int8_peak():
     """Measured INT8 tensor-core peak (profiles/r01_int8_peaks.json, cuBLASLt
     int8 GEMM at 8192^3): the sustained figure, since the residue GEMM is timed
@@ -499,6 +506,7 @@ def run_ours(args):
                       "a = P X (Ozaki scheme II on tcgen05 kind::i8, TMEM accumulators)",
             "achieved": achieved_i8, "peak": ipeak, "unit": "TFLOP/s", "frac": achieved_i8 / ipeak,
             "op_type": "int8 tensor-core ops (2 per MAC), counted like NVIDIA TOPS",
+            "frac_vs_burst": (achieved_i8 / load_int8_burst()) if load_int8_burst() else None,
             "traffic": TRAFFIC_OZ,
             "peak_source": ipeak_src,
             "ops_per_launch": ops_full, "avg_launch_ms": full_ms,
@@ -564,7 +572,7 @@ def run_ours(args):
 # ncu --set full dram bytes (profiles/r01_ncu_summary.md): k_zupdate 1076.1 + 134.0 MB,
 # k_update_pairs 236.0 + 41.9 MB, k_sum_planes 167.7 + 58.4 MB per full update
 # ncu --set full dram bytes of one k_oz_gemm launch (full product, N = 2048; profiles/r01_ncu_summary.md)
-TRAFFIC_OZ = (377.892 + 128.074) * 1e6
+TRAFFIC_OZ = (335.688 + 112.857) * 1e6  # ncu --set full, one 16-modulus k_oz_gemm at N = 2048
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 

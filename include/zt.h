@@ -161,7 +161,7 @@ int zt_oz_moduli(int* out, int cap);
 int zt_oz_set_cta(int c);
 /* C = A B (complex128, n x n, row-major with leading dimensions) through the
  * residue GEMM: rows of A and columns of B scaled to integers of up to 53
- * bits, 18 moduli, CRT reconstruction in 128-bit integers.  bmode 1: B is
+ * bits, 16 moduli <= 256, CRT reconstruction in 128-bit integers.  bmode 1: B is
  * skew-Hermitian with B[k][j] == -conj(B[j][k]) exactly off the diagonal
  * (converted row-wise, no transpose).  lower: only the 128-tiles of C on or
  * below the diagonal.  workspace: zt_oz_workspace_bytes(n). */
