@@ -683,6 +683,11 @@ __global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_rows(int n, const
       xv[e] = rint(v.x * sc.x * sc.y);
       xv[4 + e] = rint(v.y * sc.x * sc.y);
     }
+    // running word pointers into the planes of modulus t (advanced per
+    // modulus: no 64-bit index arithmetic per store)
+    const size_t pw = (size_t)mp * kp / 4;  // plane stride in words
+    uint32_t* pa = reinterpret_cast<uint32_t*>(out + (size_t)i * kp + k0);
+    uint32_t* pb = reinterpret_cast<uint32_t*>((mode == 1 ? out : out2) + (size_t)i * kp + k0);
 #pragma unroll 1
     for (int g = 0; g < OZ_NGRP; ++g) {
     float yv[8], ym[8];
@@ -710,20 +715,20 @@ __global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_rows(int n, const
 #else
       if (mode != 1) {
 #endif
-        int8_t* base = out + ((size_t)(t * 3) * mp + i) * kp + k0;
-        *reinterpret_cast<uint32_t*>(base) = wr;
-        *reinterpret_cast<uint32_t*>(base + (size_t)mp * kp) = wi;
-        *reinterpret_cast<uint32_t*>(base + (size_t)2 * mp * kp) = wn;
+        pa[0] = wr;
+        pa[pw] = wi;
+        pa[2 * pw] = wn;
       }
+      pa += 3 * pw;
 #ifdef OZ_EXP_NOSTORE
       if (wi == 0x12345678u && wb == 3u) {
 #else
       if (mode != 0) {
 #endif
-        int8_t* b2 = (mode == 1 ? out : out2) + ((size_t)(t * 2) * mp + i) * kp + k0;
-        *reinterpret_cast<uint32_t*>(b2) = wb;
-        *reinterpret_cast<uint32_t*>(b2 + (size_t)mp * kp) = wi;
+        pb[0] = wb;
+        pb[pw] = wi;
       }
+      pb += 2 * pw;
     }
     }
   }
@@ -770,6 +775,8 @@ __global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_cols(int n, const
     xv[e] = rint(v.x * sc.x * sc.y);
     xv[4 + e] = rint(v.y * sc.x * sc.y);
   }
+  const size_t pw = (size_t)np * kp / 4;  // plane stride in words
+  uint32_t* pb = reinterpret_cast<uint32_t*>(out + (size_t)j * kp + k0 + kk);
 #pragma unroll 1
   for (int g = 0; g < OZ_NGRP; ++g) {
     float yv[8], ym[8];
@@ -785,9 +792,9 @@ __global__ void __launch_bounds__(256, OZ_CONV_MINB) k_oz_conv_cols(int n, const
       for (int e = 0; e < 8; ++e) rw[e] = res_word_f(yv[e], ym[e], t);
       const uint32_t wr = pack4(rw[0], rw[1], rw[2], rw[3]);
       const uint32_t wi = pack4(rw[4], rw[5], rw[6], rw[7]);
-      int8_t* base = out + ((size_t)(t * 2) * np + j) * kp + k0 + kk;
-      *reinterpret_cast<uint32_t*>(base) = wr;
-      *reinterpret_cast<uint32_t*>(base + (size_t)np * kp) = wi;
+      pb[0] = wr;
+      pb[pw] = wi;
+      pb += 2 * pw;
     }
   }
 }
