@@ -251,6 +251,13 @@ int zt_profile_read(double* ms3, int64_t* counts3, int reset);
  * evidence for the bench's gpu_launches claim). */
 int64_t zt_launch_count(void);
 
+/* Step execution mode for zt_midpoint_step / zt_midpoint_step_host: 1 (the
+ * default, or ZT_GRAPH unset/1) runs each step as one CUDA graph with the
+ * fixed point as a conditional WHILE node; 0 launches the same kernels
+ * eagerly with one 8-byte read-back per iteration (results are bitwise
+ * identical).  Returns the previous mode. */
+int zt_set_graph(int on);
+
 #ifdef __cplusplus
 }
 #endif

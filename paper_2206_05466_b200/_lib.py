@@ -75,6 +75,7 @@ SIGNATURES = {
         [_c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_dbl, _vp, _vp, _c_int, _c_int, _vp],
     ),
     "zt_launch_count": (_c_i64, []),
+    "zt_set_graph": (_c_int, [_c_int]),
     "zt_profile_enable": (_c_int, [_c_int]),
     "zt_profile_read": (_c_int, [_vp, _vp, _c_int]),
 }

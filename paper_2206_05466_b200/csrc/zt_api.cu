@@ -79,6 +79,12 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
               unsigned long long* cons, void* ws, cudaStream_t st, int gemm1_only, cudaEvent_t x_join);
 int oz_convert_x(int n, const double* x, void* ws, cudaStream_t st);
 int final_commutator(int n, const double* a, const double* wn, double h, double* out, cudaStream_t st);
+size_t oz_workspace_bytes(int n);
+int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c, int64_t ldc,
+             int lower, void* ws, size_t ws_bytes, cudaStream_t st);
+int update_pairs(int n, const double* a, const double* bm, double* out, const double* base, const double* xprev,
+                 const double* wn, double hh, double qq, unsigned long long* resid, unsigned long long* cons,
+                 cudaStream_t st);
 size_t zupdate_split_bytes(int n);
 int zgemm_rect_scatter(int m, int n, int k, const double* a, int64_t lda, const double* b, int64_t ldb, double* c,
                        int64_t ldc, const unsigned long long* peers, int npeer, int r0, int mloc, int algo,
@@ -109,15 +115,27 @@ int zgemm_update_rows(int m, int n, const double* a_rows, const double* p, const
                       const double* base, const double* xprev, double* out, int64_t ld, double hh,
                       double qq, unsigned long long* resid, int algo, cudaStream_t st);
 
+// Library configuration, read ONCE from the environment when the library is
+// loaded (so a workspace sized by zt_step_workspace_bytes stays valid for
+// every later call in the process):
 // step products: 2 = FP64-accurate Ozaki-II on the INT8 tensor cores (default),
 // 0 = 3M DMMA (ZT_GEMM_ALGO=3m or dmma), 1 = 4M DMMA (ZT_GEMM_ALGO=4m)
-static int g_algo = 2;
+static bool env_on(const char* name, bool dflt) {
+  const char* e = getenv(name);
+  return e ? std::string(e) != "0" : dflt;
+}
+static const int g_algo = [] {
+  const char* e = getenv("ZT_GEMM_ALGO");
+  if (!e) return 2;
+  const std::string v(e);
+  return v == "4m" ? 1 : ((v == "3m" || v == "dmma") ? 0 : 2);
+}();
 // DMMA kernel variant for the products that stay on the FP64 pipe
 static inline int dmma_algo() { return g_algo == 1 ? 1 : 0; }
-static bool g_fused = true;  // persistent fused GEMM-1 + GEMM-2 per update (ZT_FUSED=0 disables)
-static bool g_planes = true; // fused 3M reads precomputed sum planes (ZT_SUM_PLANES=0 disables)
-static bool g_split = true;  // split-K tail in the fused update (ZT_SPLIT=0 disables)
-static bool g_sep_update = true;  // update as a streaming pass after the GEMMs (ZT_SEP_UPDATE=0: fused epilogue)
+static const bool g_fused = env_on("ZT_FUSED", true);   // persistent fused GEMM-1 + GEMM-2 per update (DMMA path)
+static const bool g_planes = env_on("ZT_SUM_PLANES", true);  // fused 3M reads precomputed sum planes
+static const bool g_split = env_on("ZT_SPLIT", true);   // split-K tail in the fused update
+static const bool g_sep_update = env_on("ZT_SEP_UPDATE", true);  // update as a streaming pass after the GEMMs
 
 // ---- step workspace layout -------------------------------------------------
 struct StepWS {
@@ -290,7 +308,7 @@ static int update(zt_operator* op, const double* x, const double* base, const do
 // The step's last update without GEMM-2 (see k_final_commutator): solve,
 // a = P W~, W_{n+1} = W_n + h (a - a^H), in place over W~.  ZT_FINAL_SANDWICH=1
 // (or a consistency request) keeps the reference's sandwich form.
-static bool g_final_comm = true;
+static const bool g_final_comm = !env_on("ZT_FINAL_SANDWICH", false);
 // prog: the GEMM-1 kernel itself writes W_{n+1} into w.b pair by pair and
 // publishes each 64-row block (FusedArgs::prog) for an overlapped D2H copy;
 // x receives it by one device copy at the end.
@@ -390,6 +408,12 @@ __global__ void k_fp_decide(unsigned long long* flags, double tol, int max_iter,
   cudaGraphSetConditional(h, (!(r <= tol) && (int)k < max_iter) ? 1u : 0u);
 }
 
+// laplacian.py:107-116 on the gate's residuals (NaN passes, as `r > tol`
+// is false in the reference); the WHILE condition starts at 1 otherwise
+__global__ void k_gate(const double* val, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (val[0] > 1e-10 || val[1] > 1e-10) ? 0u : 1u);
+}
+
 struct GraphEntry {
   zt_operator* op;
   int n;
@@ -405,7 +429,8 @@ struct GraphEntry {
 };
 static thread_local std::vector<GraphEntry> t_graphs;
 static thread_local cudaStream_t t_cap[2] = {nullptr, nullptr};
-static bool g_graph = true;  // ZT_GRAPH=0: eager step with per-iteration host sync
+// ZT_GRAPH=0 or zt_set_graph(0): eager step with per-iteration host sync
+static std::atomic<bool> g_graph{env_on("ZT_GRAPH", true)};
 
 static int build_step_graph(GraphEntry& e, StepWS& w) {
   zt_operator* op = e.op;
@@ -420,18 +445,30 @@ static int build_step_graph(GraphEntry& e, StepWS& w) {
   cudaGraph_t graph = nullptr;
   ZT_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   int64_t c0 = g_launches.load();
-  rc = residuals(n, e.wn, n, w.val, w.resid, cs);
+  cudaGraphConditionalHandle hc;
+  {
+    cudaStreamCaptureStatus stt;
+    cudaGraph_t cg;
+    cudaError_t ce = cudaStreamGetCaptureInfo(cs, &stt, nullptr, &cg, nullptr, nullptr);
+    if (!ce) ce = cudaGraphConditionalHandleCreate(&hc, cg, 1, cudaGraphCondAssignDefault);
+    if (ce) rc = cuda_fail(ce, "graph: conditional handle");
+  }
+  if (!rc) rc = residuals(n, e.wn, n, w.val, w.resid, cs);
   if (!rc) rc = cudaMemcpyAsync(x, e.wn, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, cs) ? ZT_ECUDA : ZT_OK;
   if (!rc) rc = cudaMemsetAsync(w.flags + 2, 0, sizeof(unsigned long long), cs) ? ZT_ECUDA : ZT_OK;
+  if (!rc) {
+    // the input gate decides before the first update: a rejected W_n skips
+    // the fixed point entirely (0 iterations; the host raises StructureError)
+    k_gate<<<1, 1, 0, cs>>>(w.val, hc);
+    ZT_LAUNCHED();
+  }
   int64_t c1 = g_launches.load();
-  cudaGraphConditionalHandle hc;
   if (!rc) {
     cudaStreamCaptureStatus stt;
     cudaGraph_t cg;
     const cudaGraphNode_t* deps;
     size_t nd;
     cudaError_t ce = cudaStreamGetCaptureInfo(cs, &stt, nullptr, &cg, &deps, &nd);
-    if (!ce) ce = cudaGraphConditionalHandleCreate(&hc, cg, 1, cudaGraphCondAssignDefault);
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = hc;
@@ -643,6 +680,8 @@ const char* zt_last_error(void) { return t_err.c_str(); }
 
 int64_t zt_launch_count(void) { return g_launches.load(); }
 
+int zt_set_graph(int on) { return g_graph.exchange(on != 0) ? 1 : 0; }
+
 int zt_profile_enable(int on) {
   g_prof = on != 0;
   oz_profile_enable(g_prof);
@@ -664,16 +703,6 @@ int zt_profile_read(double* ms, int64_t* counts, int reset) {
 
 int zt_op_create(int n, int device, zt_op_t* op) {
   if (!op) return fail(ZT_EINVAL, "null output");
-  if (const char* e = getenv("ZT_GEMM_ALGO")) {
-    const std::string v(e);
-    g_algo = v == "4m" ? 1 : ((v == "3m" || v == "dmma") ? 0 : 2);
-  }
-  if (const char* e = getenv("ZT_FUSED")) g_fused = std::string(e) != "0";
-  if (const char* e = getenv("ZT_SUM_PLANES")) g_planes = std::string(e) != "0";
-  if (const char* e = getenv("ZT_GRAPH")) g_graph = std::string(e) != "0";
-  if (const char* e = getenv("ZT_SPLIT")) g_split = std::string(e) != "0";
-  if (const char* e = getenv("ZT_SEP_UPDATE")) g_sep_update = std::string(e) != "0";
-  if (const char* e = getenv("ZT_FINAL_SANDWICH")) g_final_comm = std::string(e) == "0";
   return op_create(n, device, op);
 }
 int zt_op_destroy(zt_op_t op) { return op_destroy(op); }
@@ -813,9 +842,22 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
   return ZT_OK;
 }
 
+// cfg 3 ops on the step's product: the INT8 Ozaki-II GEMM by default (its
+// residue planes in a stream-ordered temporary), the DMMA GEMM under
+// ZT_GEMM_ALGO=3m/4m
+static int product_for_op(int n, const double* a, const double* b, int bmode, int lower, double* c, void* oz_ws,
+                          cudaStream_t st) {
+  if (g_algo == 2) return oz_zgemm(n, a, n, b, n, bmode, c, n, lower, oz_ws, oz_workspace_bytes(n), st);
+  return zgemm(n, a, n, b, n, c, n, dmma_algo(), st);
+}
+
 int zt_commutator(int n, const double* p, const double* w, double* c, double* work, void* stream) {
+  if (n < 1 || !p || !w || !c || !work) return fail(ZT_EINVAL, "zt_commutator: bad argument");
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = zgemm(n, p, n, w, n, work, n, dmma_algo(), st);
+  void* oz = nullptr;
+  if (g_algo == 2) ZT_CUDA_CHECK(cudaMallocAsync(&oz, oz_workspace_bytes(n), st));
+  int rc = product_for_op(n, p, w, 0, 0, work, oz, st);
+  if (oz) cudaFreeAsync(oz, st);
   if (rc) return rc;
   return skew_diff(n, work, c, st);
 }
@@ -882,12 +924,27 @@ int zt_basis_project(int n, int m0, int m1, const long long* off, const long lon
 }
 
 int zt_sandwich(int n, const double* p, const double* w, double h, double* s, double* work, void* stream) {
-  // S = W - (h/2)(a - a^H) - (h^2/4) a P  with a = P W
+  // S = W - (h/2)(a - a^H) - (h^2/4) a P  with a = P W; a P = P W P is
+  // skew-Hermitian for skew P, W, so (as in the step) only its lower tiles
+  // are computed and the update pass mirrors them
+  if (n < 1 || !p || !w || !s || !work) return fail(ZT_EINVAL, "zt_sandwich: bad argument");
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = zgemm(n, p, n, w, n, work, n, dmma_algo(), st);
-  if (rc) return rc;
-  return zgemm_update(n, work, p, w, nullptr, nullptr, s, n, -0.5 * h, -0.25 * h * h, nullptr, nullptr,
-                      dmma_algo(), st);
+  if (g_algo != 2) {
+    int rc = zgemm(n, p, n, w, n, work, n, dmma_algo(), st);
+    if (rc) return rc;
+    return zgemm_update(n, work, p, w, nullptr, nullptr, s, n, -0.5 * h, -0.25 * h * h, nullptr, nullptr,
+                        dmma_algo(), st);
+  }
+  void* oz = nullptr;
+  double* b = nullptr;
+  ZT_CUDA_CHECK(cudaMallocAsync(&oz, oz_workspace_bytes(n), st));
+  ZT_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&b), (size_t)n * n * 16, st));
+  int rc = product_for_op(n, p, w, 0, 0, work, oz, st);
+  if (!rc) rc = product_for_op(n, work, p, 0, 1, b, oz, st);
+  if (!rc) rc = update_pairs(n, work, b, s, w, nullptr, nullptr, -0.5 * h, -0.25 * h * h, nullptr, nullptr, st);
+  cudaFreeAsync(b, st);
+  cudaFreeAsync(oz, st);
+  return rc;
 }
 
 }  // extern "C"

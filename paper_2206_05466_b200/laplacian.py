@@ -72,7 +72,11 @@ def _to_device(w):
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError(f"expected a square matrix, got shape {a.shape}")
     a = np.ascontiguousarray(a, dtype=np.complex128)
-    return torch.from_numpy(a).to(torch.device("cuda", torch.cuda.current_device())), True
+    # stream-ordered copy: asynchronous when the array is pinned (results of
+    # this module are, so a state fed back step after step is DMA'd directly);
+    # every public call synchronises before returning, so the caller may
+    # reuse the array afterwards
+    return torch.from_numpy(a).to(torch.device("cuda", torch.cuda.current_device()), non_blocking=True), True
 
 
 def _out(t: torch.Tensor, as_numpy: bool):
@@ -208,12 +212,25 @@ def build_operator(n: int, device=None) -> LaplacianOperator:
 
 
 def _resolve(op, w) -> LaplacianOperator:
-    """laplacian.py:325-333."""
+    """laplacian.py:325-333.
+
+    ``op`` may be any operator object with an ``n`` attribute: unmodified
+    reference callers pass the reference's own ``zeitlin.laplacian.
+    LaplacianOperator`` (driver.py:290, 396; diagnostics.py:62), which holds
+    host tables only.  Such an operator (or one of ours built for another
+    device) is mapped to the cached device operator for (N, the matrix's
+    device); the size check and its message are the reference's.
+    """
     n = w.shape[0]
     if op is None:
         return build_operator(n, w.device)
-    if op.n != n:
-        raise ValueError(f"operator size {op.n} does not match matrix size {n}")
+    op_n = getattr(op, "n", None)
+    if op_n is None:
+        raise TypeError(f"expected a LaplacianOperator, got {type(op).__name__}")
+    if op_n != n:
+        raise ValueError(f"operator size {op_n} does not match matrix size {n}")
+    if not isinstance(op, LaplacianOperator) or op.device != w.device:
+        return build_operator(n, w.device)
     return op
 
 
@@ -311,10 +328,9 @@ def solve_stream_batched(w: torch.Tensor, op: LaplacianOperator | None = None) -
     if w.dim() != 3 or w.shape[1] != w.shape[2]:
         raise ValueError("expected a (B, N, N) stack")
     w = w.contiguous()
-    b, n = w.shape[0], w.shape[1]
-    op = build_operator(n, w.device) if op is None else op
-    if op.n != n:
-        raise ValueError(f"operator size {op.n} does not match matrix size {n}")
+    b = w.shape[0]
+    op = _resolve(op, w[0])
+    n = op.n
     p = torch.empty_like(w)
     ws = workspace(w.device, "solve_b", lib.zt_solve_workspace_bytes(n, b))
     check(lib.zt_stream_solve_ws(op.handle, w.data_ptr(), n, n * n, p.data_ptr(), n, n * n, b,

@@ -164,12 +164,13 @@ def test_long_run_structure_full_size(zt, n):
     assert abs(zt.casimirs(x, 2)[1] - c2_0) <= 1e-12 * abs(c2_0)
 
 
-@pytest.mark.parametrize("n", (2048, 4096))
+@pytest.mark.parametrize("n", (2048, 4096, 8192))
 def test_cfg3_commutator_and_sandwich_full_size(zt, n):
-    """BASELINE cfg 3 at full size (P then W from random_admissible(N, rng(0),
-    1/N), h = 0.01): C = a - a^H and S = W - (h/2)(a - a^H) - (h^2/4) a P with
-    a = P W (integrator.py:127-129) against numpy/OpenBLAS, relF <= 1e-14;
-    C exactly skew-Hermitian."""
+    """BASELINE cfg 3 at every size it names (P then W from
+    random_admissible(N, rng(0), 1/N), h = 0.01) through the DEFAULT product
+    (the INT8 Ozaki-II GEMM, as in the step): C = a - a^H and
+    S = W - (h/2)(a - a^H) - (h^2/4) a P with a = P W (integrator.py:127-129)
+    against numpy/OpenBLAS, relF <= 1e-14; C exactly skew-Hermitian."""
     from paper_2206_05466_b200 import _lib
 
     h = 0.01
@@ -217,3 +218,126 @@ def test_host_result_step_bitwise(n):
 
     st, info = midpoint_step_info(StepperState(w=x1.cpu().numpy(), h=0.01))
     assert isinstance(st.w, np.ndarray) and np.array_equal(st.w, midpoint_step_raw(x1, 0.01, 1e-12, 10, op)[0].cpu().numpy())
+
+
+@pytest.mark.parametrize("n,recipe", [(130, "random"), (300, "smooth"), (1024, "smooth")])
+def test_fixed_point_solve_h_positive_vs_oracle(zt, n, recipe):
+    """Public fixed_point_solve (integrator.py:96-138) at h > 0: W~ and the
+    iteration count against the oracle's fixed point from the same W_n."""
+    w = zo.random_admissible(n, np.random.default_rng(n), 1.0 / n) if recipe == "random" else zo.smooth_initial(n)
+    h = 0.01 if recipe == "random" else 0.005
+    ref, kref = zo.fixed_point_solve(w, h)
+    got, k = zt.fixed_point_solve(dev(w), h)
+    assert k == kref
+    assert relf(got.cpu().numpy(), ref) <= 1e-12
+    # numpy in -> numpy out, same numbers
+    got_np, k2 = zt.fixed_point_solve(w, h)
+    assert k2 == k and isinstance(got_np, np.ndarray)
+    np.testing.assert_array_equal(got_np, got.cpu().numpy())
+
+
+class _ForeignOperator:
+    """Duck-typed stand-in for the reference's zeitlin.laplacian.LaplacianOperator
+    (host tables only; laplacian.py:179-219): what the unmodified driver passes
+    (driver.py:290, 396; diagnostics.py:62)."""
+
+    def __init__(self, n):
+        self.n = n
+        self._solve_linv = np.zeros((n, n))
+        self._solve_dinv = np.zeros((n, n))
+
+
+def test_foreign_operator_object(zt):
+    """The drop-in accepts the reference's own operator object: the driver's
+    exact calls midpoint_step_info(state, ref_op) and hamiltonian(w, ref_op)
+    with a numpy state give the same numbers as op=None; a size mismatch keeps
+    the reference's ValueError text."""
+    n = 96
+    w = zo.smooth_initial(n)
+    op = _ForeignOperator(n)
+    st = zt.StepperState(w=w.copy(), h=0.005)
+    a, ia = zt.midpoint_step_info(st, op)
+    b, ib = zt.midpoint_step_info(st)
+    assert ia.iterations == ib.iterations
+    np.testing.assert_array_equal(a.w, b.w)
+    assert zt.hamiltonian(w, op) == zt.hamiltonian(w)
+    np.testing.assert_array_equal(zt.solve_stream(w, op), zt.solve_stream(w))
+    np.testing.assert_array_equal(zt.apply_laplacian(w, op=op), zt.apply_laplacian(w))
+    wt, k = zt.fixed_point_solve(w, 0.005, op=op)
+    assert k == ib.iterations
+    with pytest.raises(ValueError, match="does not match"):
+        zt.midpoint_step_info(st, _ForeignOperator(n + 1))
+    try:  # the real reference class when the reference install travelled with the repo
+        import sys
+        from conftest import ROOT
+        import os
+
+        ref_path = os.path.join(ROOT, "baseline", "_ref")
+        if os.path.isdir(os.path.join(ref_path, "zeitlin")) and ref_path not in sys.path:
+            sys.path.append(ref_path)
+        from zeitlin.laplacian import LaplacianOperator as RefOp
+    except Exception:
+        return
+    np.testing.assert_array_equal(zt.midpoint_step_info(st, RefOp(n))[0].w, b.w)
+
+
+@pytest.mark.parametrize("n,steps", [(4096, 2), (8192, 1)])
+def test_cfg5_sizes_on_default_path_vs_oracle(zt, n, steps):
+    """BASELINE cfg 5 sizes (smooth recipe, h = 0.0025) on the default INT8
+    product path against the CPU oracle from the same W0: identical iteration
+    counts, relF(W) <= 1e-10, Casimir C2/C3 and energy drift no larger than
+    the oracle's (floor 1e-13 relative)."""
+    w = zo.smooth_initial(n)
+    c0, h0 = zo.casimirs(w, 3), zo.hamiltonian(w)
+    x = dev(w)
+    op = zt.build_operator(n)
+    oop = zo.build_operator(n)
+    ref = w
+    for _ in range(steps):
+        ref, kr, _ = zo.midpoint_step(ref, 0.0025, op=oop)
+        x, k, _, _ = zt.integrator.midpoint_step_raw(x, 0.0025, 1e-12, 10, op)
+        assert k == kr
+    assert relf(x.cpu().numpy(), ref) <= 1e-10
+    c_ref, c_gpu = zo.casimirs(ref, 3), zt.casimirs(x, 3)
+    floor = 1e-13
+    for j in (1, 2):
+        assert abs(c_gpu[j] - c0[j]) <= max(abs(c_ref[j] - c0[j]), floor * abs(c0[j]))
+    assert abs(zt.hamiltonian(x) - h0) <= max(abs(zo.hamiltonian(ref, op=oop) - h0), floor * abs(h0))
+
+
+def test_eager_and_graph_steps_bitwise(zt):
+    """zt_set_graph(0) (eager launches, one read-back per iteration) and the
+    CUDA-graph step give bitwise identical W_{n+1}, iterations and residual."""
+    from paper_2206_05466_b200 import _lib
+
+    n = 300
+    x = dev(zo.smooth_initial(n))
+    op = zt.build_operator(n)
+    y1, k1, r1, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, op)
+    prev = _lib.lib.zt_set_graph(0)
+    try:
+        y2, k2, r2, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, op)
+    finally:
+        _lib.lib.zt_set_graph(prev)
+    assert (k1, r1) == (k2, r2)
+    assert torch.equal(y1, y2)
+
+
+def test_gate_rejects_before_the_fixed_point(zt):
+    """A W_n that fails the input gate raises StructureError with the
+    reference's text on both the graph and the eager path."""
+    n = 64
+    w = zo.random_admissible(n, np.random.default_rng(9), 1.0 / n)
+    bad = w + 0.01 * np.eye(n)
+    op = zt.build_operator(n)
+    from paper_2206_05466_b200 import _lib
+
+    for mode in (1, 0):
+        prev = _lib.lib.zt_set_graph(mode)
+        try:
+            with pytest.raises(zt.StructureError, match="traceless|skew"):
+                zt.integrator.midpoint_step_raw(dev(bad), 0.005, 1e-12, 10, op)
+            y, k, _, _ = zt.integrator.midpoint_step_raw(dev(w), 0.005, 1e-12, 10, op)
+            assert k >= 1
+        finally:
+            _lib.lib.zt_set_graph(prev)
