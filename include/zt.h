@@ -143,25 +143,27 @@ int zt_midpoint_step_host(zt_op_t op, const double* wn, double* w_next, double* 
                           int* iterations, double* residual, void* stream);
 
 /* INT8 tensor-core building block of an FP64-accurate complex GEMM
- * (Ozaki scheme II, csrc/zt_oz.cu): for every modulus j < nmod, the
- * residues (Re / Im of A * B^T + floor(p_j / 2)) mod p_j, unsigned bytes
- * in [0, p_j), from centred int8 residue planes
- * A [nmod][3][mp][kp] (re, im, -im) and B [nmod][2][np][kp] (re, im) into
- * R [nmod][2][mp][np]; tcgen05 kind::i8 MMAs, int32 accumulation in TMEM.
- * mp, np, kp multiples of 128; lower != 0: square, only 128-tiles on or
- * below the diagonal.  zt_oz_moduli writes the moduli, returns their count. */
+ * (Ozaki scheme II with a Gaussian-integer split, csrc/zt_oz.cu).  Every
+ * modulus p_j (odd, prime factors = 1 mod 4, zt_oz_moduli) has a square root
+ * iota_j of -1 (zt_oz_iotas), so a complex residue product is two real ones:
+ * given centred int8 planes A [nmod][2][mp][kp] = (phi+, phi-) and
+ * B [nmod][2][np][kp] (K-major rows of B^T), with U = A+ B+^T and
+ * V = A- B-^T (exact int32 accumulation in TMEM, tcgen05 kind::i8 MMAs on
+ * CTA pairs), R [nmod][2][mp][np] receives ((U + V) + k_j) mod p_j and
+ * ((U - V) + k_j) mod p_j, k_j = (p_j - 1) / 2, unsigned bytes in [0, p_j).
+ * For phi+- = re +- iota_j im (mod p_j) of complex matrices A, B this is
+ * 2 Re(A B^T) and 2 iota_j Im(A B^T) mod p_j.  mp, np multiples of 256, kp
+ * of 128; lower != 0: square, only the 256-tiles on or below the diagonal.
+ * zt_oz_moduli / zt_oz_iotas write the moduli / roots, return their count. */
 int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, const void* b, void* r, int lower,
                   void* stream);
 int zt_oz_moduli(int* out, int cap);
-/* Residue-GEMM kernel choice for zt_oz_modgemm and the step (0 = the
- * ZT_OZ_CTA environment variable, else 1): 1 = one CTA per 128 x 256 tile
- * (Re + Im accumulators in TMEM), 2 = CTA pairs (tcgen05 cta_group::2, Re
- * and Im as separate 256 x 256 real tiles with K doubled, double-buffered
- * TMEM accumulators; used when mp % 256 == 0).  ZT_EINVAL otherwise. */
-int zt_oz_set_cta(int c);
+int zt_oz_iotas(int* out, int cap);
 /* C = A B (complex128, n x n, row-major with leading dimensions) through the
  * residue GEMM: rows of A and columns of B scaled to integers of up to 53
- * bits, 16 moduli <= 256, CRT reconstruction in 128-bit integers.  bmode 1: B is
+ * bits, 17 moduli <= 241, CRT reconstruction from 42-bit FP64 pieces; a
+ * row of A or column of B holding a NaN or an infinity gives a NaN row /
+ * column of C.  bmode 1: B is
  * skew-Hermitian with B[k][j] == -conj(B[j][k]) exactly off the diagonal
  * (converted row-wise, no transpose).  lower: only the 128-tiles of C on or
  * below the diagonal.  workspace: zt_oz_workspace_bytes(n). */

@@ -44,7 +44,7 @@ SIGNATURES = {
     "zt_fixed_point": (_c_int, [_vp, _vp, _vp, _c_dbl, _c_dbl, _c_int, _vp, _c_sz, _PI, _PD, _vp]),
     "zt_oz_modgemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int, _vp]),
     "zt_oz_moduli": (_c_int, [_vp, _c_int]),
-    "zt_oz_set_cta": (_c_int, [_c_int]),
+    "zt_oz_iotas": (_c_int, [_vp, _c_int]),
     "zt_oz_workspace_bytes": (_c_sz, [_c_int]),
     "zt_oz_profile_read": (_c_int, [_vp, _vp, _c_int]),
     "zt_oz_zgemm": (_c_int, [_c_int, _vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_sz, _vp]),
