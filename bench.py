@@ -10,14 +10,17 @@ default_rng(0), 1/2048)) normalised to unit Frobenius norm, h=0.005.
 
 ours:       device-resident steps through the C ABI (zt_midpoint_step);
             `value` = steps/s with W resident in HBM; `e2e` = the same through
-            the public Python API with the step's W copied from pinned host
-            memory and the result copied back every step; `roofline` for the
-            dominant kernel (3M DMMA ZGEMM, GEMM-1 a = P X) from CUDA events
-            around every launch in the timed region; `cpu_baseline` = the CPU
-            oracle port on this host's cores (rank 0, N=1 only).
-reference:  the CPU oracle port (restating the reference's numpy/OpenBLAS
-            path; the reference itself is Python and is not on the GPU box)
-            timed on all host cores, same config/metric.
+            the public Python API with the step's W copied from host memory
+            and the result copied back every step; `roofline` for the dominant
+            kernel (the INT8 residue GEMM k_oz_gemm) from CUDA events around
+            every launch of an eager pass of the same steps; `n4096` = the
+            device-resident rate at N = 4096; `cpu_baseline` = the reference
+            on this host's cores (rank 0, N=1 only).
+reference:  the unmodified reference package `zeitlin` staged under
+            baseline/_ref (tools/stage_reference.sh) through its public API
+            (build_operator + midpoint_step_info; numba + OpenBLAS on all host
+            cores), or the oracle port when it is not staged; same config and
+            metric, a bounded sample of steps.
 Multi-GPU (torchrun): the row-block sharded step (sharded.py) of the same
 workload, NCCL collectives, strong scaling, time = max over ranks
 (`--replicas` runs independent replicas instead; `--sharded --n 4096` is cfg 5).
@@ -94,11 +97,75 @@ def oracle_steps(steps, warmup, n=N):
     return times, iters, cores, blas
 
 
+def bench_config(iters):
+    """The workload description both arms print (identical keys and values)."""
+    return {
+        "workload": WORKLOAD, "N": N, "h": H, "tol": TOL, "max_iter": MAX_ITER,
+        "init": "W0 = lap^-1(random_admissible(2048, default_rng(0), 1/2048)) / ||.||_F",
+        "iterations_per_step": sorted(set(iters)),
+    }
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_steps(steps, warmup, n=N):
+    """The UNMODIFIED reference package `zeitlin` (staged under baseline/_ref
+    by tools/stage_reference.sh) through its public API: build_operator +
+    midpoint_step_info (integrator.py:141-171; numba sweeps, OpenBLAS zgemm on
+    all host cores).  None when it is not importable here."""
+    if not os.path.isdir(os.path.join(REF_DIR, "zeitlin")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "zt_numba_cache"))
+    sys.path.insert(0, REF_DIR)
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        from zeitlin.integrator import StepperState, midpoint_step_info
+        from zeitlin.laplacian import build_operator, solve_stream
+    except Exception as exc:  # pragma: no cover - broken install
+        print(f"[bench] reference package not importable ({exc!r}); timing the oracle port", file=sys.stderr)
+        return None
+    finally:
+        sys.path.remove(REF_DIR)
+    cores = host_cores()
+    with threadpool_limits(limits=cores):
+        op = build_operator(n)
+        w = solve_stream(cfg4_initial_numpy(n), op)
+        w = w / np.linalg.norm(w)
+        state = StepperState(w=w, h=H, tol=TOL, max_iter=MAX_ITER)
+        times, iters = [], []
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            state, info = midpoint_step_info(state, op)
+            dt = time.perf_counter() - t0
+            if s >= warmup:
+                times.append(dt)
+                iters.append(info.iterations)
+        blas = [f"{d.get('internal_api')} {d.get('version')} x{d.get('num_threads')}" for d in threadpool_info()]
+    return times, iters, cores, blas
+
+
+# a reference step is ~1-2 s at N = 2048: the arm times a bounded sample
+REF_MAX_STEPS = 20
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    times, iters, cores, blas = oracle_steps(args.steps, args.warmup)
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = 1  # numba JIT compile + first-touch; not timed
+    got = reference_steps(steps, warm)
+    if got is not None:
+        times, iters, cores, blas = got
+        kind = "reference"
+        what = ("the unmodified reference package zeitlin 0.1.0 (baseline/_ref): "
+                "zeitlin.integrator.midpoint_step_info with zeitlin.laplacian.build_operator; numba sweeps "
+                "(serial), numpy/OpenBLAS zgemm")
+    else:
+        times, iters, cores, blas = oracle_steps(steps, warm)
+        kind = "port"
+        what = "oracle/zeitlin_oracle.py restating integrator.py:96-171 + laplacian.py:272-316 (numpy row loops)"
     total = sum(times)
     value = len(times) / total
     line = {
@@ -107,12 +174,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "N": N, "h": H, "iterations_per_step": iters},
+        "config": bench_config(iters),
         "cpu_baseline": {
-            "value": value, "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"{len(times)} full cfg-4 steps at N=2048 (after {args.warmup} warm-up); "
-                      f"oracle/zeitlin_oracle.py restating integrator.py:96-171 + laplacian.py:272-316; "
-                      f"BLAS: {'; '.join(blas)}; sweeps are numpy row loops",
+            "value": value, "unit": "steps/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} full cfg-4 steps at N=2048 (after {warm} untimed warm-up step; "
+                      f"--steps {args.steps} capped at {REF_MAX_STEPS}); {what}; BLAS: {'; '.join(blas)}",
         },
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -188,23 +254,23 @@ def load_fp64_peak():
                           if best else "nominal 148 SM x 128 flop/clk x 1.965 GHz")
 
 
-def load_int8_burst():
+def load_int8_peaks():
+    """Measured INT8 tensor-core peaks from the tcgen05.mma kind::i8 issue-rate
+    microbenchmark (tools/i8_peaks.cu, pseudo-random operands; the residue
+    GEMM's cta_group::2 256 x 256 x 32 shape): burst (20 ms) and sustained
+    (4 s, under the 1 kW power cap).  MEASURED_PEAKS.json has no int8 figure."""
+    burst = sustained = None
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_int8_peaks.json")))["burst_tops"]
-    except (OSError, KeyError, ValueError):
-        return None
-
-
-def load_int8_peak():
-    """Measured INT8 tensor-core peak (profiles/r01_int8_peaks.json, cuBLASLt
-    int8 GEMM at 8192^3): the sustained figure, since the residue GEMM is timed
-    inside long steps under the power cap; MEASURED_PEAKS.json has no int8."""
-    try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_int8_peaks.json")))
-        return d["sustained_tops"], ("measured: cuBLASLt int8 GEMM 8192^3 back to back for 4 s (sustained), "
-                                     "profiles/r01_int8_peaks.json (burst %.0f TOPS)" % d["burst_tops"])
-    except (OSError, KeyError, ValueError):
-        return 2 * 1415.7, "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 = 2 x bf16 rate)"
+        for line in open(os.path.join(ROOT, "profiles", "r02_int8_peaks.jsonl")):
+            d = json.loads(line)
+            if "cta_group::2" in d.get("bench", ""):
+                if "burst" in d["bench"]:
+                    burst = d
+                elif "sustained" in d["bench"]:
+                    sustained = d
+    except (OSError, ValueError):
+        pass
+    return burst, sustained
 
 
 def run_sharded(args):
@@ -333,7 +399,34 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def _steps_per_s_device(zt, midpoint_step_raw, torch, dev, n, h, steps):
+    """Device-resident graph steps at size n (cfg 4 recipe); (steps/s, ms, iterations)."""
+    op = zt.build_operator(n, dev)
+    r = torch.from_numpy(cfg4_initial_numpy(n)).to(dev)
+    w = zt.solve_stream(r, op)
+    x = w / torch.linalg.norm(w)
+    out = torch.empty_like(x)
+    for _ in range(3):
+        y, k, _, _ = midpoint_step_raw(x, h, TOL, MAX_ITER, op, out=out)
+        x, out = y, x
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = []
+    e0.record(stream)
+    for _ in range(steps):
+        y, k, _, _ = midpoint_step_raw(x, h, TOL, MAX_ITER, op, out=out)
+        x, out = y, x
+        its.append(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return steps / (ms / 1e3), ms / steps, sorted(set(its))
+
+
 def run_ours(args):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -381,26 +474,29 @@ def run_ours(args):
             iters.append(k)
         e1.record(stream)
         torch.cuda.synchronize()
-    barrier()
-    launches = lib.zt_launch_count() - launches0
-    # per-kernel CUDA-event timing of the same steps (eager launches, events
-    # around every solve / fused-update launch) right after the timed region
-    import ctypes
-
-    lib.zt_profile_read(None, None, 1)
-    lib.zt_profile_enable(1)
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        y, k, _, _ = midpoint_step_raw(x, H, TOL, MAX_ITER, op, out=out)
-        x, out = y, x
-    p1.record(stream)
-    torch.cuda.synchronize()
-    lib.zt_profile_enable(0)
+        barrier()
+        launches = lib.zt_launch_count() - launches0
+        # per-kernel CUDA-event timing of the same steps (eager launches, events
+        # around every solve / update / residue-GEMM launch on the launching
+        # stream) right after the timed region, under the same clock sampler
+        lib.zt_profile_read(None, None, 1)
+        lib.zt_oz_profile_read(None, None, 1)
+        lib.zt_profile_enable(1)
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            y, k, _, _ = midpoint_step_raw(x, H, TOL, MAX_ITER, op, out=out)
+            x, out = y, x
+        p1.record(stream)
+        torch.cuda.synchronize()
+        lib.zt_profile_enable(0)
     pms = (ctypes.c_double * 3)()
     pcnt = (ctypes.c_int64 * 3)()
     lib.zt_profile_read(ctypes.cast(pms, ctypes.c_void_p), ctypes.cast(pcnt, ctypes.c_void_p), 1)
+    oz_ms = (ctypes.c_double * 2)()
+    oz_cnt = (ctypes.c_longlong * 2)()
+    lib.zt_oz_profile_read(ctypes.cast(oz_ms, ctypes.c_void_p), ctypes.cast(oz_cnt, ctypes.c_void_p), 1)
     prof_ms = p0.elapsed_time(p1)
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -443,108 +539,115 @@ def run_ours(args):
         ems = float(t.item())
     e2e_value = world * e2e_steps / (ems / 1e3)
 
-    oz_ms = (ctypes.c_double * 2)()
-    oz_cnt = (ctypes.c_longlong * 2)()
-    lib.zt_oz_profile_read(ctypes.cast(oz_ms, ctypes.c_void_p), ctypes.cast(oz_cnt, ctypes.c_void_p), 1)
-    oz = oz_cnt[0] > 0
-    # ---- roofline of the dominant kernel: the fused update k_zupdate<3M>
-    # (GEMM-1 a = P X on all tiles + GEMM-2 b = a P on lower tiles + update
-    # epilogue), timed by CUDA events around every launch in the timed region
-    peak, peak_src = load_fp64_peak()
-    fused = os.environ.get("ZT_FUSED", "1") != "0"  # zt_api.cu: fused update unless ZT_FUSED=0
+    kbar = statistics.mean(iters)
+    sv_ms = pms[0] / max(1, pcnt[0])
     g1_ms = pms[1] / max(1, pcnt[1])
     g2_ms = pms[2] / max(1, pcnt[2])
-    sv_ms = pms[0] / max(1, pcnt[0])
-    T = (N + 63) // 64
-    tiles_frac = (T * T + T * (T + 1) / 2) / (T * T)
-    alg = 16.0 * N**3 if fused else 8.0 * N**3  # the reference's two ZGEMMs per update
-    executed = 6.0 * N**3 * (tiles_frac if fused else 1.0)
-    achieved = alg / (g1_ms * 1e-3) / 1e12
-    roofline = {
-        "bound": "tensor",
-        "kernel": "full update: k_zupdate<3M, sum planes> (GEMM-1 a = P X + GEMM-2 b = a P on lower tiles) "
-                  "with its sum-plane pre-pass and k_update_pairs update pass (events around all three)" if fused
-        else "k_zgemm<3M,STORE> (GEMM-1 a = P X)",
-        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-        "traffic": TRAFFIC_FUSED if fused else None,
-        "peak_source": peak_src,
-        "algorithmic_flop_per_launch": alg,
-        "executed_dmma_flop_per_launch": executed,
-        "executed_frac": executed / (g1_ms * 1e-3) / 1e12 / peak,
-        "avg_launch_ms": g1_ms,
-        "note": "algorithmic = the reference update's two full complex products (16 N^3); executed = 3M "
-                "(6 N^3 per product) on all GEMM-1 tiles and the lower-triangle GEMM-2 tiles "
-                "(b = P X P is skew-Hermitian), so achieved/peak exceeds 1; the step's final update "
-                "computes W_n + h (a - a^H) (equal to the reference's sandwich form at the fixed point), "
-                "one product instead of two (final_update_avg_ms); step_alg_flop counts the reference's "
-                "16 N^3 (k+1)",
-        "final_update_avg_ms": g2_ms,
+    oz = oz_cnt[0] > 0
+    common = {
         "solve_avg_ms": sv_ms, "solve_alg_bytes": 24.0 * N * N,
         "solve_GBps_alg": 24.0 * N * N / (sv_ms * 1e-3) / 1e9 if sv_ms > 0 else None,
-        "timing": "avg_launch_ms from CUDA events around every launch of an eager pass of the same "
-                  f"{args.steps} steps right after the timed region (the timed region itself runs each "
-                  "step as one CUDA graph with a conditional while node for the fixed point)",
+        "full_update_avg_ms": g1_ms, "final_update_avg_ms": g2_ms,
         "eager_ms_per_step": prof_ms / args.steps,
-        "step_share": {"update_gemms": (pms[1] + pms[2]) / prof_ms, "solve": pms[0] / prof_ms},
-        "step_alg_flop": 16.0 * N**3 * (statistics.mean(iters) + 1),
-        "step_TFLOPs_alg": 16.0 * N**3 * (statistics.mean(iters) + 1) / (ms_per_step * 1e-3) / 1e12,
+        "products_per_step": {
+            "reference_algorithmic": f"2 (k+1) = {2 * (kbar + 1):g} full complex products (integrator.py:127-128, 155-156)",
+            "executed": {"full": kbar + 1, "lower_tiles": kbar,
+                         "why": "the fixed point's b = a P is skew-Hermitian (lower tiles + mirror); the final "
+                                "update W_n + h (a - a^H) needs a = P W~ only (the (h^2/4) a P terms cancel at "
+                                "the fixed point)"},
+        },
+        "step_alg_flop": 16.0 * N**3 * (kbar + 1),
+        "step_TFLOPs_alg": 16.0 * N**3 * (kbar + 1) / (ms_per_step * 1e-3) / 1e12,
+        "timing": "avg launch times from CUDA events around every launch of an eager pass of the same "
+                  f"{args.steps} steps right after the timed region (the timed region itself runs each step "
+                  "as one CUDA graph with a conditional WHILE node for the fixed point); clocks sampled over both",
     }
     if oz:
-        # dominant kernel: the residue GEMM k_oz_gemm (tcgen05 kind::i8)
-        ipeak, ipeak_src = load_int8_peak()
+        # dominant kernel: the residue GEMM k_oz_gemm (tcgen05 kind::i8, CTA pairs)
+        burst, sustained = load_int8_peaks()
         pd = (N + 255) // 256 * 256
-        mt, nt = pd // 128, pd // 256
-        low = sum(tm * 128 // 256 + 1 for tm in range(mt)) / (mt * nt)
-        nmod = int(lib.zt_oz_moduli(None, 0)) if hasattr(lib, "zt_oz_moduli") else 16
-        ops_full = nmod * 4 * 2.0 * pd**3          # 4M: four int8 products per modulus
+        mt = pd // 256
+        nmod = int(lib.zt_oz_moduli(None, 0))
+        ops_full = nmod * 2 * 2.0 * pd**3  # two real int8 products (U, V) per modulus, 2 ops per MAC
         full_ms = oz_ms[0] / oz_cnt[0]
         low_ms = oz_ms[1] / max(1, oz_cnt[1])
-        achieved_i8 = ops_full / (full_ms * 1e-3) / 1e12
+        achieved = ops_full / (full_ms * 1e-3) / 1e12
+        # peak at the clock this run saw: the microbenchmark's measured MACs
+        # per clock per SM (8192 for kind::i8) x SMs x the median SM clock
+        # sampled over the timed region and the eager pass
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        clocks = clk.summary()
+        mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+        per_clk = burst["macs_per_clk_sm"] if burst else 8192.0
+        peak = 2.0 * per_clk * sms * mhz * 1e6 / 1e12
         roofline = {
             "bound": "tensor",
-            "kernel": f"k_oz_gemm: {nmod}-modulus int8 residue GEMM of the FP64-accurate complex product "
-                      "a = P X (Ozaki scheme II on tcgen05 kind::i8, TMEM accumulators)",
-            "achieved": achieved_i8, "peak": ipeak, "unit": "TFLOP/s", "frac": achieved_i8 / ipeak,
-            "op_type": "int8 tensor-core ops (2 per MAC), counted like NVIDIA TOPS",
-            "frac_vs_burst": (achieved_i8 / load_int8_burst()) if load_int8_burst() else None,
-            "traffic": TRAFFIC_OZ,
-            "peak_source": ipeak_src,
+            "kernel": f"k_oz_gemm: {nmod}-modulus int8 residue GEMM of the FP64-accurate complex product a = P X "
+                      "(Ozaki scheme II, Gaussian-integer split: 2 real int8 products per modulus; tcgen05 "
+                      "kind::i8 on CTA pairs, TMEM accumulators)",
+            "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
+            "op_type": "int8 tensor-core ops (2 per MAC)",
+            "peak_source": ("measured rate %.0f int8 MACs/clk/SM (tcgen05.mma.cta_group::2.kind::i8 256x256x32 "
+                            "issue-rate microbenchmark tools/i8_peaks.cu, profiles/r02_int8_peaks.jsonl) x %d SMs x "
+                            "%.0f MHz (median SM clock sampled during this run)" % (per_clk, sms, mhz)),
+            "peak_burst_measured": burst["tops"] if burst else None,
+            "peak_sustained": sustained["tops"] if sustained else None,
+            "frac_vs_sustained": achieved / sustained["tops"] if sustained else None,
+            "traffic": TRAFFIC_OZ, "traffic_source": TRAFFIC_OZ_SRC,
             "ops_per_launch": ops_full, "avg_launch_ms": full_ms,
-            "lower_launch_ms": low_ms, "lower_tile_fraction": low,
+            "lower_launch_ms": low_ms, "lower_tile_fraction": (mt * (mt + 1) / 2) / (mt * mt),
             "fp64_equivalent": {
                 "algorithmic_flop_per_product": 8.0 * N**3,
                 "TF_per_product": 8.0 * N**3 / (full_ms * 1e-3) / 1e12,
-                "dmma_peak_TF": peak, "vs_dmma_peak": 8.0 * N**3 / (full_ms * 1e-3) / 1e12 / peak,
+                "dmma_peak_TF": load_fp64_peak()[0],
             },
-            "full_update_avg_ms": g1_ms, "final_update_avg_ms": g2_ms,
-            "solve_avg_ms": sv_ms, "solve_alg_bytes": 24.0 * N * N,
-            "solve_GBps_alg": 24.0 * N * N / (sv_ms * 1e-3) / 1e9 if sv_ms > 0 else None,
-            "timing": "avg_launch_ms from CUDA events around every k_oz_gemm launch of an eager pass of the same "
-                      f"{args.steps} steps right after the timed region (the timed region itself runs each "
-                      "step as one CUDA graph with a conditional while node for the fixed point)",
-            "eager_ms_per_step": prof_ms / args.steps,
-            "step_alg_flop": 16.0 * N**3 * (statistics.mean(iters) + 1),
-            "step_TFLOPs_alg": 16.0 * N**3 * (statistics.mean(iters) + 1) / (ms_per_step * 1e-3) / 1e12,
-            "accuracy": "residue GEMM relF vs extended precision 2.3-4.6e-16 at N = 130-512 (native FP64 DMMA "
-                        "5.5e-16-1.1e-15), tools/oz_zgemm_check.py; profiles/r01_oz_accuracy.txt",
+            "accuracy": "relF vs extended precision <= 4e-16 at N = 5-256 (native FP64 DMMA 5.5e-16-1.1e-15); "
+                        "per-row/column bound tests/test_oz_gpu.py",
         }
+        roofline.update(common)
+    else:
+        peak, peak_src = load_fp64_peak()
+        T = (N + 63) // 64
+        tiles_frac = (T * T + T * (T + 1) / 2) / (T * T)
+        alg = 16.0 * N**3
+        executed = 6.0 * N**3 * tiles_frac
+        achieved = alg / (g1_ms * 1e-3) / 1e12
+        roofline = {
+            "bound": "tensor",
+            "kernel": "full update: k_zupdate<3M> (GEMM-1 a = P X + GEMM-2 b = a P on lower tiles) with its "
+                      "sum-plane pre-pass and k_update_pairs (events around all three)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": TRAFFIC_FUSED, "traffic_source": "ncu --set full, profiles/r01_ncu_summary.md",
+            "peak_source": peak_src,
+            "algorithmic_flop_per_launch": alg, "executed_dmma_flop_per_launch": executed,
+            "executed_frac": executed / (g1_ms * 1e-3) / 1e12 / peak, "avg_launch_ms": g1_ms,
+        }
+        roofline.update(common)
+
+    # BASELINE's metric names N = 2048 and 4096: the device-resident rate at
+    # N = 4096 (cfg 4 recipe, same h), 10 steps
+    n4 = {}
+    if world == 1 and not args.no_n4096:
+        v4, ms4, it4 = _steps_per_s_device(zt, midpoint_step_raw, torch, dev, 4096, H, 10)
+        n4 = {"value": v4, "unit": "steps/s", "ms_per_step": ms4, "steps": 10, "iterations_per_step": it4,
+              "config": "cfg 4 recipe at N=4096, h=0.005, device-resident graph steps"}
+    cfg = bench_config(iters)
+    cfg.update({
+        "parallelism": "replicas" if world > 1 else "single",
+        "gemm": ("FP64-accurate complex products on the INT8 tensor cores: Ozaki scheme II with a Gaussian-integer "
+                 "split (operands scaled to 53-bit integers, 17 odd coprime moduli <= 241 with sqrt(-1), two real "
+                 "tcgen05 kind::i8 residue GEMMs per modulus, exact CRT reconstruction); ZT_GEMM_ALGO=3m selects "
+                 "the native FP64 DMMA path") if oz else
+                "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
+        "launch": "one CUDA graph per step (fixed point = conditional WHILE node), 1 host sync per step",
+        "l2": "no flush: per-step working set W_n, W~, P, a = 256 MB > 126 MB L2",
+    })
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": WORKLOAD, "N": N, "h": H, "tol": TOL, "max_iter": MAX_ITER,
-            "init": "W0 = lap^-1(random_admissible(2048, default_rng(0), 1/2048)) / ||.||_F",
-            "iterations_per_step": sorted(set(iters)),
-            "parallelism": "replicas" if world > 1 else "single",
-            "gemm": ("FP64-accurate complex products on the INT8 tensor cores: Ozaki scheme II (operands scaled to "
-                     "53-bit integers, 16 coprime moduli <= 256, tcgen05 kind::i8 residue GEMMs, 128-bit-exact CRT "
-                     "reconstruction); ZT_GEMM_ALGO=3m selects the native FP64 DMMA path") if oz else
-                    "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
-            "launch": "one CUDA graph per step (fixed point = conditional WHILE node), 1 host sync per step",
-            "l2": "no flush: per-step working set W_n, W~, P, a = 256 MB > 126 MB L2",
-        },
+        "config": cfg,
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 16 * N * N,
                 "d2h_bytes_per_step": 16 * N * N, "steps": e2e_steps,
@@ -553,13 +656,20 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if n4:
+        line["n4096"] = n4
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, citers, cores, blas = oracle_steps(args.cpu_steps, 1)
+        got = reference_steps(args.cpu_steps, 1)
+        kind = "reference"
+        if got is None:
+            got, kind = oracle_steps(args.cpu_steps, 1), "port"
+        times, citers, cores, blas = got
         line["cpu_baseline"] = {
-            "value": len(times) / sum(times), "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"{len(times)} full cfg-4 steps at N=2048 after 1 warm-up "
-                      f"(iterations {citers}); oracle/zeitlin_oracle.py numpy/OpenBLAS; "
-                      f"BLAS: {'; '.join(blas)}",
+            "value": len(times) / sum(times), "unit": "steps/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} full cfg-4 steps at N=2048 after 1 warm-up (iterations {citers}); "
+                      + ("the unmodified zeitlin package (baseline/_ref), numba sweeps + OpenBLAS"
+                         if kind == "reference" else "oracle/zeitlin_oracle.py numpy/OpenBLAS")
+                      + f"; BLAS: {'; '.join(blas)}",
         }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -567,12 +677,10 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# dram__bytes_read.sum + dram__bytes_write.sum per fused-update launch at
-# N=2048 from the committed `ncu --set full` capture (profiles/r01_ncu_summary.md)
-# ncu --set full dram bytes (profiles/r01_ncu_summary.md): k_zupdate 1076.1 + 134.0 MB,
-# k_update_pairs 236.0 + 41.9 MB, k_sum_planes 167.7 + 58.4 MB per full update
-# ncu --set full dram bytes of one k_oz_gemm launch (full product, N = 2048; profiles/r01_ncu_summary.md)
-TRAFFIC_OZ = (335.688 + 112.857) * 1e6  # ncu --set full, one 16-modulus k_oz_gemm at N = 2048
+# ncu --set full dram bytes per launch (profiles/): the residue GEMM and the
+# DMMA path's fused update
+TRAFFIC_OZ = (285.3 + 115.4) * 1e6
+TRAFFIC_OZ_SRC = "ncu --set full, one 17-modulus k_oz_gemm at N = 2048, profiles/r02_ncu_summary.md (not measured in this run)"
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
@@ -584,6 +692,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-n4096", action="store_true", help="skip the extra N=4096 device-resident rate")
     ap.add_argument("--sharded", action="store_true",
                     help="row-block sharded step over the ranks (default when WORLD_SIZE > 1)")
     ap.add_argument("--transport", choices=("p2p", "nccl"), default="p2p",
