@@ -371,6 +371,7 @@ def run_sharded(args):
     kbar = statistics.mean(iters)
     alg = 16.0 * n**3 * (kbar + 1)
     achieved = alg / (ms_per_step * 1e-3) / 1e12
+    oz = be.oz
     line = {
         "metric": METRIC if n == N else f"isospectral time-steps/sec at N={n} complex128",
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -385,9 +386,13 @@ def run_sharded(args):
                                   "NCCL all_gather(X) + all_to_all(a tiles) + all_reduce(max residual) per update",
                    "l2": "no flush: per-step working set > 126 MB L2"},
         "roofline": {"bound": "tensor", "kernel": "whole sharded step (all ranks)", "achieved": achieved,
-                     "peak": peak * world, "unit": "TFLOP/s", "frac": achieved / (peak * world),
-                     "traffic": None, "peak_source": peak_src,
-                     "note": "algorithmic 16 N^3 (k+1) flop per step; GEMM-2 runs full per rank (no lower-tile saving)"},
+                     "peak": peak * world, "unit": "TFLOP/s (FP64-equivalent, algorithmic)",
+                     "frac": achieved / (peak * world), "traffic": None, "peak_source": peak_src,
+                     "products": ("INT8 Ozaki-II (Gaussian split) residue GEMMs, tcgen05 kind::i8" if oz else
+                                  "native FP64 DMMA"),
+                     "note": "algorithmic 16 N^3 (k+1) flop per step against the FP64 DMMA peak x ranks; "
+                             "GEMM-2 skew-balanced: (G+1)/2 m x m x N blocks per rank, the diagonal block on its "
+                             "lower tiles"},
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 16 * n * n,
                 "d2h_bytes_per_step": 16 * n * n, "steps": e2e_steps,
                 "api": "ShardedStepper.midpoint_step with pinned-host row blocks in/out every step"},

@@ -174,6 +174,38 @@ int zt_oz_profile_read(double* ms, long long* counts, int reset);
 int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, int bmode, double* c,
                 int64_t ldc, int lower, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Building blocks of the row-block sharded step on the INT8 product
+ * (paper_2206_05466_b200/sharded.py): no reference
+ * counterpart (the reference is single-process; the paper's
+ * distributed products are ScaLAPACK pzgemm).
+ *   zt_oz_bits(K): integer bits per operand entry for inner dimension K.
+ *   zt_oz_plane_bytes(rows, cols): bytes of one residue-plane set
+ *     [17][2][pad(rows)][pad(cols)], pad = multiple of 256.
+ *   zt_oz_convert_rows: rows x kdim block (row-major, ld) to planes; mode 0
+ *     A operand, mode 1 skew-B operand of a skew-Hermitian matrix whose
+ *     diagonal entry of local row j is column diag0 + j, mode 2 both (A
+ *     planes into planes, skew-B into planes2) from one read; shift:
+ *     pad(rows) ints.
+ *   zt_oz_convert_cols: kdim x ncols matrix as a general B operand
+ *     (column scales); colmax_ws: pad(ncols) 8-byte words.
+ *   zt_oz_reconstruct: residues of zt_oz_modgemm(…, pad(m), pad(n), …) to
+ *     complex128 C (m x n) into c (nullable), and/or column j into
+ *     ((double*)peers[j / mloc]) at row r0 + i of an N x mloc block (the
+ *     all-to-all fused into the reconstruction), and/or -conj(C)^T into
+ *     mirror (ld_mirror); lower != 0 (square, residues of a lower-mode
+ *     zt_oz_modgemm): only the 256-tiles on or below the diagonal, entries of
+ *     strictly-lower tiles mirrored (pass the block itself as mirror to
+ *     complete a skew-Hermitian diagonal block). */
+int zt_oz_bits(int k);
+size_t zt_oz_plane_bytes(int rows, int cols);
+int zt_oz_convert_rows(int rows, int kdim, const double* src, int64_t ld, int mode, int diag0, int kb, void* planes,
+                       int* shift, void* planes2, void* stream);
+int zt_oz_convert_cols(int kdim, int ncols, const double* src, int64_t ld, int kb, void* planes, int* shift,
+                       void* colmax_ws, void* stream);
+int zt_oz_reconstruct(int m, int n, const void* r, const int* rs, const int* cs, double* c, int64_t ldc,
+                      const unsigned long long* peers, int mloc, int r0, double* mirror, int64_t ld_mirror,
+                      int lower, void* stream);
+
 /* Config-3 ops (integrator.py:127-129): commutator C = P W - W P = a - a^H
  * with a = P W; sandwich S = W - (h/2)(a - a^H) - (h^2/4) a P
  * = (I - hP/2) W (I + hP/2).  `work` holds n*n complex (a). */
@@ -259,6 +291,11 @@ int64_t zt_launch_count(void);
  * eagerly with one 8-byte read-back per iteration (results are bitwise
  * identical).  Returns the previous mode. */
 int zt_set_graph(int on);
+
+/* The step's product path, fixed when the library loads: 2 = the INT8
+ * Ozaki-II product (default), 0 / 1 = native FP64 DMMA 3M / 4M
+ * (ZT_GEMM_ALGO=3m / 4m). */
+int zt_step_algo(void);
 
 #ifdef __cplusplus
 }

@@ -45,6 +45,12 @@ SIGNATURES = {
     "zt_oz_modgemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int, _vp]),
     "zt_oz_moduli": (_c_int, [_vp, _c_int]),
     "zt_oz_iotas": (_c_int, [_vp, _c_int]),
+    "zt_oz_bits": (_c_int, [_c_int]),
+    "zt_oz_plane_bytes": (_c_sz, [_c_int, _c_int]),
+    "zt_oz_convert_rows": (_c_int, [_c_int, _c_int, _vp, _c_i64, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp]),
+    "zt_oz_convert_cols": (_c_int, [_c_int, _c_int, _vp, _c_i64, _c_int, _vp, _vp, _vp, _vp]),
+    "zt_oz_reconstruct": (_c_int, [_c_int, _c_int, _vp, _vp, _vp, _vp, _c_i64, _vp, _c_int, _c_int, _vp, _c_i64,
+                                   _c_int, _vp]),
     "zt_oz_workspace_bytes": (_c_sz, [_c_int]),
     "zt_oz_profile_read": (_c_int, [_vp, _vp, _c_int]),
     "zt_oz_zgemm": (_c_int, [_c_int, _vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_sz, _vp]),
@@ -76,6 +82,7 @@ SIGNATURES = {
     ),
     "zt_launch_count": (_c_i64, []),
     "zt_set_graph": (_c_int, [_c_int]),
+    "zt_step_algo": (_c_int, []),
     "zt_profile_enable": (_c_int, [_c_int]),
     "zt_profile_read": (_c_int, [_vp, _vp, _c_int]),
 }

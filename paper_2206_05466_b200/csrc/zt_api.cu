@@ -682,6 +682,8 @@ int64_t zt_launch_count(void) { return g_launches.load(); }
 
 int zt_set_graph(int on) { return g_graph.exchange(on != 0) ? 1 : 0; }
 
+int zt_step_algo(void) { return g_algo; }
+
 int zt_profile_enable(int on) {
   g_prof = on != 0;
   oz_profile_enable(g_prof);

@@ -481,15 +481,15 @@ __device__ __forceinline__ double2 oz_scale2(int sh) {
 // out2; the row scale is shared since |-conj(v)| = |v|).  One block per
 // padded row; 4 consecutive k per thread (one 32-bit store per plane).
 // <= 80 registers (3 blocks of 256 per SM)
-__global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int n, const double* __restrict__ src, int64_t ld, int mp,
-                                                       int kp, int kb, int mode, int8_t* out,
+__global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const double* __restrict__ src, int64_t ld,
+                                                       int mp, int kp, int kb, int mode, int diag0, int8_t* out,
                                                        int* __restrict__ shift, int8_t* out2 = nullptr) {
-  const int i = blockIdx.x;
+  const int i = blockIdx.x;  // row of the (rows x n) block; its diagonal entry is column diag0 + i
   __shared__ double red[8];
   double amax = 0.0;
   pdl_trigger();
   pdl_wait();
-  if (i < n) {
+  if (i < rows) {
     // all of this thread's loads in flight at once (the max chain would
     // otherwise serialise them)
     int k = threadIdx.x;
@@ -520,12 +520,12 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int n, const double* __
     for (int e = 0; e < 4; ++e) {
       const int k = k0 + e;
       double2 v = make_double2(0.0, 0.0);
-      if (i < n && k < n) v = ld2(src + ((size_t)i * ld + k) * 2);
+      if (i < rows && k < n) v = ld2(src + ((size_t)i * ld + k) * 2);
       xv[e] = rint(v.x * sc.x * sc.y);
       xv[4 + e] = rint(v.y * sc.x * sc.y);
     }
-    const bool diag = (unsigned)(i - k0) < 4u;
-    const int sh8 = 8 * (i - k0);
+    const bool diag = (unsigned)(diag0 + i - k0) < 4u;
+    const int sh8 = 8 * (diag0 + i - k0);
     // running word pointers into the planes of modulus t
     uint32_t* pa = reinterpret_cast<uint32_t*>(out + (size_t)i * kp + k0);
     uint32_t* pb = reinterpret_cast<uint32_t*>((mode == 1 ? out : out2) + (size_t)i * kp + k0);
@@ -569,13 +569,13 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int n, const double* __
 
 // B operand of a general matrix X (B[j][k] = X[k][j]): column maxima first
 // (NaN-propagating: the max of the bit patterns of |x|)
-__global__ void __launch_bounds__(256) k_oz_colmax(int n, const double* __restrict__ x, int64_t ld,
+__global__ void __launch_bounds__(256) k_oz_colmax(int kdim, int n, const double* __restrict__ x, int64_t ld,
                                                    unsigned long long* colmax) {
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int r0 = blockIdx.y * 64 + (threadIdx.x >> 5) * 8;
   if (j >= n) return;
   double m = 0.0;
-  for (int r = r0; r < min(r0 + 8, n); ++r) {
+  for (int r = r0; r < min(r0 + 8, kdim); ++r) {
     const double2 v = ld2(x + ((size_t)r * ld + j) * 2);
     m = nanmax(m, nanmax(fabs(v.x), fabs(v.y)));
   }
@@ -584,15 +584,16 @@ __global__ void __launch_bounds__(256) k_oz_colmax(int n, const double* __restri
 
 // then 32 (k) x 32 (j) tiles through shared memory; thread t produces output
 // row j = j0 + t / 8, k = k0 + 4 (t % 8) .. +3 (one 32-bit store per plane)
-__global__ void __launch_bounds__(256, 3) k_oz_conv_cols(int n, const double* __restrict__ x, int64_t ld, int np,
-                                                       int kp, int kb, const unsigned long long* __restrict__ colmax,
-                                                       int8_t* out, int* __restrict__ shift) {
+__global__ void __launch_bounds__(256, 3) k_oz_conv_cols(int kdim, int n, const double* __restrict__ x, int64_t ld,
+                                                       int np, int kp, int kb,
+                                                       const unsigned long long* __restrict__ colmax, int8_t* out,
+                                                       int* __restrict__ shift) {
   __shared__ double2 tl[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r, j = j0 + tx;
-    tl[r][tx] = (k < n && j < n) ? ld2(x + ((size_t)k * ld + j) * 2) : make_double2(0.0, 0.0);
+    tl[r][tx] = (k < kdim && j < n) ? ld2(x + ((size_t)k * ld + j) * 2) : make_double2(0.0, 0.0);
   }
   __syncthreads();
   const int jj = threadIdx.x >> 3, kk = (threadIdx.x & 7) * 4;
@@ -666,15 +667,10 @@ __device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bi
 // reconstruction: 2 output columns per thread at <= 64 registers (4 blocks
 // of 256 per SM): the FP64 chains need the extra warps to hide the loads
 constexpr int OZ_RECON_COLS = 2;
-__global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t* __restrict__ r, int mp, int np,
-                                                   const int* __restrict__ rs, const int* __restrict__ cs, double* c,
-                                                   int64_t ldc, int lower) {
-  const int i = blockIdx.y;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
-  pdl_trigger();
-  pdl_wait();
-  if (i >= m || j0 >= n) return;
-  if (lower && (j0 >> 7) > (i >> 7)) return;
+// the centred integers Re, Im of product entries (i, j0 .. j0 + C - 1)
+// before scaling
+__device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp, int np, int i, int j0, double* vr,
+                                           double* vi) {
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
   constexpr int C = OZ_RECON_COLS;
   using word_t = unsigned short;
@@ -701,7 +697,6 @@ __global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t*
       for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, e < C ? c_crt.wr[t][k] : c_crt.wi[t][k], s[e][k]);
     }
   }
-  double vr[C], vi[C];
 #pragma unroll
   for (int e = 0; e < 2 * C; ++e) {
     const double q = rint(((s[e][2] + s[e][1]) + s[e][0]) * c_crt.m_inv);
@@ -714,22 +709,68 @@ __global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t*
     else
       vi[e - C] = x;
   }
+}
+__device__ __forceinline__ double2 scaled(double vr, double vi, int ri, int cj) {
+  if (ri == OZ_BAD || cj == OZ_BAD)
+    return make_double2(__longlong_as_double(0x7ff8000000000000LL), __longlong_as_double(0x7ff8000000000000LL));
+  const int sh = -(ri + cj);
+  return make_double2(ldexp(vr, sh), ldexp(vi, sh));
+}
+
+__global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t* __restrict__ r, int mp, int np,
+                                                   const int* __restrict__ rs, const int* __restrict__ cs, double* c,
+                                                   int64_t ldc, int lower) {
+  const int i = blockIdx.y;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
+  pdl_trigger();
+  pdl_wait();
+  if (i >= m || j0 >= n) return;
+  if (lower && (j0 >> 7) > (i >> 7)) return;
+  double vr[OZ_RECON_COLS], vi[OZ_RECON_COLS];
+  crt_values(r, mp, np, i, j0, vr, vi);
   const int ri = rs[i];
 #pragma unroll
-  for (int e = 0; e < C; ++e) {
+  for (int e = 0; e < OZ_RECON_COLS; ++e) {
     const int j = j0 + e;
-    if (j < n && !(lower && (j >> 7) > (i >> 7))) {
-      const int cj = cs[j];
-      double2 o;
-      if (ri == OZ_BAD || cj == OZ_BAD) {
-        o = make_double2(__longlong_as_double(0x7ff8000000000000LL), __longlong_as_double(0x7ff8000000000000LL));
-      } else {
-        const int sh = -(ri + cj);
-        o = make_double2(ldexp(vr[e], sh), ldexp(vi[e], sh));
-      }
-      st2(c + ((size_t)i * ldc + j) * 2, o);
-    }
+    if (j < n && !(lower && (j >> 7) > (i >> 7))) st2(c + ((size_t)i * ldc + j) * 2, scaled(vr[e], vi[e], ri, cs[j]));
   }
+}
+
+// Reconstruction for the row-block sharded step: C (m x n) into `c` (may be
+// null), and/or column j into rank h = j / mloc's N x mloc buffer a[:, R_h]
+// at row r0 + i (peer pointers: the all-to-all of the a tiles fused into the
+// epilogue), and/or -conj(C)^T into `mirror` (the partner's rows of the
+// skew-Hermitian b, ld_mirror).
+__global__ void __launch_bounds__(256, 4) k_oz_recon_ex(int m, int n, const int8_t* __restrict__ r, int mp, int np,
+                                                      const int* __restrict__ rs, const int* __restrict__ cs,
+                                                      double* c, int64_t ldc, const unsigned long long* peers,
+                                                      int mloc, int r0, double* mirror, int64_t ldm, int lower) {
+  const int i = blockIdx.y;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
+  pdl_trigger();
+  pdl_wait();
+  if (i >= m || j0 >= n) return;
+  // lower (square, from a lower-mode residue GEMM): only 256-tiles on or
+  // below the diagonal were computed; entries of strictly-lower tiles are
+  // also mirrored, diagonal tiles are complete on both sides
+  if (lower && (j0 >> 8) > (i >> 8)) return;
+  double vr[OZ_RECON_COLS], vi[OZ_RECON_COLS];
+  crt_values(r, mp, np, i, j0, vr, vi);
+  const int ri = rs[i];
+#pragma unroll
+  for (int e = 0; e < OZ_RECON_COLS; ++e) {
+    const int j = j0 + e;
+    if (j >= n) continue;
+    const double2 o = scaled(vr[e], vi[e], ri, cs[j]);
+    if (c) st2(c + ((size_t)i * ldc + j) * 2, o);
+    if (peers) {
+      const int h = j / mloc;
+      double* dst = reinterpret_cast<double*>(peers[h]);
+      st2(dst + ((size_t)(r0 + i) * mloc + (j - h * mloc)) * 2, o);
+    }
+    if (mirror && !(lower && (j >> 8) == (i >> 8))) st2(mirror + ((size_t)j * ldm + i) * 2, make_double2(-o.x, o.y));
+  }
+  if (peers || mirror) __threadfence_system();
 }
 
 static cudaError_t launch_recon(int m, int n, const int8_t* r, int mp, int np, const int* rs, const int* cs, double* c,
@@ -935,19 +976,19 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   int* rsh = reinterpret_cast<int*>(rres + (size_t)OZ_NMOD * 2 * p * p);
   int* csh = rsh + p;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(csh + p);
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, a, lda, p, p, kb, 0, ares, rsh,
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, n, a, lda, p, p, kb, 0, 0, ares, rsh,
                            (int8_t*)nullptr));
   ZT_LAUNCHED();
   if (bmode == 1) {
-    ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, b, ldb, p, p, kb, 1, bres, csh,
+    ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, n, b, ldb, p, p, kb, 1, 0, bres, csh,
                              (int8_t*)nullptr));
     ZT_LAUNCHED();
   } else {
     ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * p, st));
     if (p != n) ZT_CUDA_CHECK(cudaMemsetAsync(bres, 0, (size_t)OZ_NMOD * 2 * p * p, st));
-    k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, b, ldb, cmax);
+    k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, n, b, ldb, cmax);
     ZT_LAUNCHED();
-    k_oz_conv_cols<<<dim3(p / 32, p / 32), 256, 0, st>>>(n, b, ldb, p, p, kb, cmax, bres, csh);
+    k_oz_conv_cols<<<dim3(p / 32, p / 32), 256, 0, st>>>(n, n, b, ldb, p, p, kb, cmax, bres, csh);
     ZT_LAUNCHED();
   }
   rc = oz_modgemm(OZ_NMOD, p, p, p, ares, bres, rres, lower, st);
@@ -980,9 +1021,9 @@ int oz_convert_x(int n, const double* x, void* ws, cudaStream_t st) {
   int* sx = reinterpret_cast<int*>(bx + 6 * pl) + pd;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(sx + 3 * pd);
   ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pd, st));
-  k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, x, n, cmax);
+  k_oz_colmax<<<dim3((n + 31) / 32, (n + 63) / 64), 256, 0, st>>>(n, n, x, n, cmax);
   ZT_LAUNCHED();
-  k_oz_conv_cols<<<dim3(pd / 32, pd / 32), 256, 0, st>>>(n, x, n, pd, pd, kb, cmax, bx, sx);
+  k_oz_conv_cols<<<dim3(pd / 32, pd / 32), 256, 0, st>>>(n, n, x, n, pd, pd, kb, cmax, bx, sx);
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return ZT_OK;
@@ -1012,8 +1053,8 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   int* sx = sp + pd;                                // X columns
   int* sa = sx + pd;                                // a rows
   // P: A layout and skew-B layout in one pass
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, p, (int64_t)n, pd, pd, kb,
-                           gemm1_only ? 0 : 2, ares, sp, gemm1_only ? (int8_t*)nullptr : bp));
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, p, (int64_t)n, pd, pd, kb,
+                           gemm1_only ? 0 : 2, 0, ares, sp, gemm1_only ? (int8_t*)nullptr : bp));
   ZT_LAUNCHED();
   if (x_join) {
     ZT_CUDA_CHECK(cudaStreamWaitEvent(st, x_join, 0));
@@ -1026,8 +1067,8 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sx, a, n, 0, st));
   ZT_LAUNCHED();
   if (gemm1_only) return final_commutator(n, a, wn, hh, out, st);
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, (const double*)a, (int64_t)n, pd, pd, kb,
-                           0, ares, sa, (int8_t*)nullptr));
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, (const double*)a, (int64_t)n, pd, pd,
+                           kb, 0, 0, ares, sa, (int8_t*)nullptr));
   ZT_LAUNCHED();
   rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bp, rres, 1, st);
   if (rc) return rc;
@@ -1089,4 +1130,71 @@ extern "C" int zt_oz_zgemm(int n, const double* a, int64_t lda, const double* b,
                            int64_t ldc, int lower, void* ws, size_t ws_bytes, void* stream) {
   if (!a || !b || !c || !ws) return zt::fail(ZT_EINVAL, "zt_oz_zgemm: bad argument");
   return zt::oz_zgemm(n, a, lda, b, ldb, bmode, c, ldc, lower, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// ---- building blocks of the row-block sharded step (sharded.py) -------------
+extern "C" int zt_oz_bits(int k) { return zt::oz_bits(k); }
+
+extern "C" size_t zt_oz_plane_bytes(int rows, int cols) {
+  return (size_t)zt::OZ_NMOD * 2 * zt::oz_pad(rows) * zt::oz_pad(cols);
+}
+
+// rows x kdim block of a complex128 matrix (row-major, ld) to residue planes
+// [NMOD][2][pad(rows)][pad(kdim)]; mode 0: A planes (phi+, phi-) of the rows;
+// mode 1: skew-B planes of the rows of a skew-Hermitian S (B[j][k] = S[k][j]
+// = -conj(S[j][k]), the diagonal entry -- column diag0 + j -- as is).  kb:
+// zt_oz_bits(K).  shift: pad(rows) ints (row scales).  mode 2: both from one
+// read, A planes into `planes`, skew-B planes into `planes2`.
+extern "C" int zt_oz_convert_rows(int rows, int kdim, const double* src, int64_t ld, int mode, int diag0, int kb,
+                                  void* planes, int* shift, void* planes2, void* stream) {
+  using namespace zt;
+  if (rows < 1 || kdim < 1 || !src || !planes || !shift || mode < 0 || mode > 2 || (mode == 2 && !planes2))
+    return fail(ZT_EINVAL, "zt_oz_convert_rows: bad argument");
+  int rc = crt_init();
+  if (rc) return rc;
+  const int mp = (int)oz_pad(rows), kp = (int)oz_pad(kdim);
+  cudaStream_t st = (cudaStream_t)stream;
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(mp), dim3(256), 0, st, rows, kdim, src, ld, mp, kp, kb, mode, diag0,
+                           static_cast<int8_t*>(planes), shift, static_cast<int8_t*>(planes2)));
+  ZT_LAUNCHED();
+  return ZT_OK;
+}
+
+// kdim x ncols general matrix X as the B operand (B[j][k] = X[k][j], column
+// scales): planes [NMOD][2][pad(ncols)][pad(kdim)]; colmax_ws: pad(ncols)
+// 8-byte words of scratch.
+extern "C" int zt_oz_convert_cols(int kdim, int ncols, const double* src, int64_t ld, int kb, void* planes,
+                                  int* shift, void* colmax_ws, void* stream) {
+  using namespace zt;
+  if (kdim < 1 || ncols < 1 || !src || !planes || !shift || !colmax_ws)
+    return fail(ZT_EINVAL, "zt_oz_convert_cols: bad argument");
+  int rc = crt_init();
+  if (rc) return rc;
+  const int np = (int)oz_pad(ncols), kp = (int)oz_pad(kdim);
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* cmax = static_cast<unsigned long long*>(colmax_ws);
+  ZT_CUDA_CHECK(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * np, st));
+  k_oz_colmax<<<dim3((ncols + 31) / 32, (kdim + 63) / 64), 256, 0, st>>>(kdim, ncols, src, ld, cmax);
+  ZT_LAUNCHED();
+  k_oz_conv_cols<<<dim3(np / 32, kp / 32), 256, 0, st>>>(kdim, ncols, src, ld, np, kp, kb, cmax,
+                                                         static_cast<int8_t*>(planes), shift);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+// C = A B^T residues -> complex128 (see k_oz_recon_ex): r from zt_oz_modgemm
+// with mp = pad(m), np = pad(n); rs / cs the A / B shifts.
+extern "C" int zt_oz_reconstruct(int m, int n, const void* r, const int* rs, const int* cs, double* c, int64_t ldc,
+                                 const unsigned long long* peers, int mloc, int r0, double* mirror, int64_t ld_mirror,
+                                 int lower, void* stream) {
+  using namespace zt;
+  if (m < 1 || n < 1 || !r || !rs || !cs || (!c && !peers && !mirror) || (peers && mloc < 1) || (lower && m != n))
+    return fail(ZT_EINVAL, "zt_oz_reconstruct: bad argument");
+  const dim3 grid((n + 256 * OZ_RECON_COLS - 1) / (256 * OZ_RECON_COLS), m);
+  ZT_CUDA_CHECK(launch_pdl(k_oz_recon_ex, grid, dim3(256), 0, (cudaStream_t)stream, m, n,
+                           static_cast<const int8_t*>(r), (int)oz_pad(m), (int)oz_pad(n), rs, cs, c, ldc, peers, mloc,
+                           r0, mirror, ld_mirror, lower));
+  ZT_LAUNCHED();
+  return ZT_OK;
 }

@@ -45,6 +45,9 @@ class DeviceBackend:
         self._ws = workspace
         self._stream = _stream_ptr
         self._flag = torch.zeros(1, dtype=torch.int64, device=device)
+        # the products follow the library's step path: INT8 Ozaki-II (default)
+        # or native FP64 DMMA (ZT_GEMM_ALGO=3m / 4m)
+        self.oz = _lib.lib.zt_step_algo() == 2
 
     def solve(self, x_full: torch.Tensor) -> torch.Tensor:
         from .laplacian import _solve_device
@@ -56,8 +59,38 @@ class DeviceBackend:
 
         validate_vorticity(x_full)
 
+    def _oz_product(self, a_rows: torch.Tensor, b: torch.Tensor, bmode: int) -> torch.Tensor:
+        """a_rows (m x n) times B on the INT8 product: bmode 0 B = b (n x n,
+        column scales), bmode 1 B = the skew-Hermitian b read by rows."""
+        lib, dev = self._lib, self.device
+        m, n = a_rows.shape
+        pad = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        s = self._stream(dev)
+        kb = lib.lib.zt_oz_bits(n)
+        ap = torch.empty(lib.lib.zt_oz_plane_bytes(m, n), dtype=torch.uint8, device=dev)
+        sa = torch.empty(pad(m), dtype=torch.int32, device=dev)
+        bp = torch.empty(lib.lib.zt_oz_plane_bytes(n, n), dtype=torch.uint8, device=dev)
+        sb = torch.empty(pad(n), dtype=torch.int32, device=dev)
+        r = torch.empty(lib.lib.zt_oz_plane_bytes(m, n), dtype=torch.uint8, device=dev)
+        out = torch.empty((m, n), dtype=torch.complex128, device=dev)
+        lib.check(lib.lib.zt_oz_convert_rows(m, n, a_rows.data_ptr(), n, 0, 0, kb, ap.data_ptr(), sa.data_ptr(),
+                                             None, s))
+        if bmode == 0:
+            cmax = torch.empty(pad(n), dtype=torch.int64, device=dev)
+            lib.check(lib.lib.zt_oz_convert_cols(n, n, b.data_ptr(), n, kb, bp.data_ptr(), sb.data_ptr(),
+                                                 cmax.data_ptr(), s))
+        else:
+            lib.check(lib.lib.zt_oz_convert_rows(n, n, b.data_ptr(), n, 1, 0, kb, bp.data_ptr(), sb.data_ptr(),
+                                                 None, s))
+        lib.check(lib.lib.zt_oz_modgemm(17, pad(m), pad(n), pad(n), ap.data_ptr(), bp.data_ptr(), r.data_ptr(), 0, s))
+        lib.check(lib.lib.zt_oz_reconstruct(m, n, r.data_ptr(), sa.data_ptr(), sb.data_ptr(), out.data_ptr(), n,
+                                            None, 1, 0, None, n, 0, s))
+        return out
+
     def gemm_rows(self, p_rows: torch.Tensor, x_full: torch.Tensor) -> torch.Tensor:
         m, n = p_rows.shape
+        if self.oz:
+            return self._oz_product(p_rows, x_full, 0)
         out = torch.empty((m, n), dtype=torch.complex128, device=self.device)
         self._lib.check(self._lib.lib.zt_zgemm_rect(m, n, n, p_rows.data_ptr(), n, x_full.data_ptr(), n,
                                                     out.data_ptr(), n, 0, self._stream(self.device)))
@@ -65,6 +98,15 @@ class DeviceBackend:
 
     def update_rows(self, a_rows, p, ah_rows, base, xprev, hh, qq):
         m, n = a_rows.shape
+        if self.oz:
+            # b_R = a_R P (P skew-Hermitian: skew-B rows, full rows of b); the
+            # elementwise update of this comparison path in torch
+            b = self._oz_product(a_rows, p, 1)
+            out = base + hh * (a_rows - ah_rows) + qq * b
+            if xprev is None:
+                return out, 0.0
+            res = float((out - xprev).abs().max().item())
+            return out, (math.inf if res != res else res)
         out = torch.empty_like(a_rows)
         self._flag.zero_()
         self._lib.check(self._lib.lib.zt_zgemm_update_rows(
@@ -171,14 +213,15 @@ class ShardedStepper:
 # Peer-memory variant: the two data-path collectives are fused into the GEMM
 # epilogues as NVLink stores into the other ranks' buffers.
 #
-#   all-gather of the iterate  -> the update epilogue writes every new row of
-#                                 X_R into each rank's N x N iterate buffer
-#                                 (zt_zgemm_update_rows_peer), overlapped with
-#                                 the GEMM-2 tiles that produce them;
-#   all-to-all for (a^H)_R     -> the GEMM-1 epilogue writes column block h of
-#                                 a_R into rank h's N x (N/G) buffer a[:, R_h]
-#                                 (zt_zgemm_rect_scatter), which the update
-#                                 epilogue reads transposed.
+#   all-gather of the iterate  -> the elementwise update writes every new row
+#                                 of X_R into each rank's N x N iterate buffer
+#                                 (zt_update_rows_ew);
+#   all-to-all for (a^H)_R     -> the GEMM-1 epilogue / reconstruction writes
+#                                 column block h of a_R into rank h's
+#                                 N x (N/G) buffer a[:, R_h]
+#                                 (zt_oz_reconstruct with peer pointers on the
+#                                 INT8 product, zt_zgemm_rect_scatter on DMMA),
+#                                 which the update reads transposed.
 #
 # GEMM-2 is balanced over the skew symmetry of b = a P = P X P: of every
 # pair of off-diagonal blocks b[R_g, R_h], b[R_h, R_g] = -b[R_g, R_h]^H only
@@ -298,24 +341,146 @@ class PeerRank:
             self.brows.data_ptr() if with_b else None,
             base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
             self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
-        bits = int(self._flag.item())
-        return out, torch.tensor([bits], dtype=torch.int64).view(torch.float64).item()
+        # the residual stays on the device as the bit pattern of a
+        # non-negative double (NaN above every number): max over ranks is an
+        # integer max, and the host reads it once per update after the reduction
+        return out, self._flag
 
-    def phase2(self, base_rows, xprev_rows, hh: float, qq: float):
-        """Unbalanced alternative: full rows of b per rank, fused update epilogue."""
+
+class OzPeerRank(PeerRank):
+    """PeerRank with both products on the INT8 tensor cores (the step's
+    default product, csrc/zt_oz.cu): the same algorithm, with
+
+      GEMM-1  a_R = P_R X: P rows as A planes, the gathered iterate X as
+              column-scaled B planes (converted on a side stream while the
+              stream solve runs), one residue GEMM, and a reconstruction that
+              scatters column block h of a_R into rank h's a[:, R_h]
+              (zt_oz_reconstruct with peer pointers: the all-to-all fused
+              into the reconstruction);
+      GEMM-2  b blocks = a_R[rows] P[:, C]: a rows as A planes, rows C of the
+              skew-Hermitian P as skew-B planes (no transpose), and a
+              reconstruction that also stores -conj(block)^T into the
+              partner's b rows (the skew mirror); the diagonal block runs on
+              its lower tiles and mirrors into itself.  P rows R_g are
+              converted once for both roles (A planes of GEMM-1, skew-B planes
+              of the diagonal block).
+
+    Row and column scales are those of the single-GPU step (P rows, X
+    columns, a rows), so a_R is bitwise the single-GPU a's rows."""
+
+    NMOD = 17
+
+    def _buf(self, key, nbytes, dtype=torch.uint8):
+        store = self.__dict__.setdefault("_bufs", {})
+        t = store.get(key)
+        esz = torch.tensor([], dtype=dtype).element_size()
+        if t is None or t.numel() * esz < nbytes:
+            t = torch.empty(max(1, -(-nbytes // esz)), dtype=dtype, device=self.be.device)
+            store[key] = t
+        return t
+
+    @staticmethod
+    def _pad(x):
+        return (x + 255) // 256 * 256
+
+    def _planes(self, key, rows):
         lib = self.be._lib
-        out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
-        self._flag.zero_()
-        lib.check(lib.lib.zt_zgemm_update_rows_peer(
-            self.m, self.n, self.a_rows.data_ptr(), self.p.data_ptr(), self.acol.data_ptr(), self.m,
-            base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
-            self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
-        bits = int(self._flag.item())
-        return out, torch.tensor([bits], dtype=torch.int64).view(torch.float64).item()
+        return (self._buf(("pl",) + key, lib.lib.zt_oz_plane_bytes(rows, self.n)),
+                self._buf(("sh",) + key, 4 * self._pad(rows), torch.int32))
+
+    def _convert_rows(self, key, rows, src, mode, diag0, stream, key2=None):
+        lib = self.be._lib
+        planes, shift = self._planes(key, rows)
+        planes2 = self._planes(key2, rows)[0] if mode == 2 else None
+        lib.check(lib.lib.zt_oz_convert_rows(rows, self.n, src, self.n, mode, diag0, self.kb, planes.data_ptr(),
+                                             shift.data_ptr(), planes2.data_ptr() if planes2 is not None else None,
+                                             stream))
+        return planes, shift, planes2
+
+    def _product(self, key, a_planes, a_shift, m, b_planes, b_shift, ncols, stream, c=None, peers=None,
+                 mloc=1, r0=0, mirror=None, lower=0):
+        lib = self.be._lib
+        r = self._buf(("r",) + key, lib.lib.zt_oz_plane_bytes(m, ncols))
+        lib.check(lib.lib.zt_oz_modgemm(self.NMOD, self._pad(m), self._pad(ncols), self._pad(self.n),
+                                        a_planes.data_ptr(), b_planes.data_ptr(), r.data_ptr(), lower, stream))
+        lib.check(lib.lib.zt_oz_reconstruct(m, ncols, r.data_ptr(), a_shift.data_ptr(), b_shift.data_ptr(), c,
+                                            self.n, peers, mloc, r0, mirror, self.n, lower, stream))
+
+    def phase1(self, validate: bool) -> None:
+        lib, n, m = self.be._lib, self.n, self.m
+        if validate:
+            self.be.validate(self.xfull)
+        self.kb = lib.lib.zt_oz_bits(n)
+        main = torch.cuda.current_stream(self.be.device)
+        s = main.cuda_stream
+        # X's column conversion does not depend on the solve: side stream
+        side = self._side_streams(1)[0]
+        fork = torch.cuda.Event()
+        fork.record(main)
+        side.wait_event(fork)
+        bx = self._buf("bx", lib.lib.zt_oz_plane_bytes(n, n))
+        sx = self._buf("sx", 4 * self._pad(n), torch.int32)
+        cmax = self._buf("cmax", 8 * self._pad(n))
+        lib.check(lib.lib.zt_oz_convert_cols(n, n, self.xfull.data_ptr(), n, self.kb, bx.data_ptr(), sx.data_ptr(),
+                                             cmax.data_ptr(), side.cuda_stream))
+        join = torch.cuda.Event()
+        join.record(side)
+        self.p = self.be.solve(self.xfull)
+        # P rows R_g: A planes (GEMM-1) and skew-B planes (the diagonal GEMM-2 block) in one pass
+        self.pa, self.sp, self.pb = self._convert_rows(("p",), m, self.p[self.r0:].data_ptr(), 2, self.r0, s,
+                                                       key2=("pb",))
+        main.wait_event(join)
+        self.a_rows = torch.empty((m, n), dtype=torch.complex128, device=self.be.device)
+        self._product(("g1",), self.pa, self.sp, m, bx, sx, n, s, c=self.a_rows.data_ptr(),
+                      peers=self.aptrs.data_ptr(), mloc=m, r0=self.r0)
+
+    def phase2a(self):
+        n, esz = self.n, 16
+        blocks = self.blocks()
+        main = torch.cuda.current_stream(self.be.device)
+        s = main.cuda_stream
+        # A planes of the a rows each block multiplies (all rows, or a half)
+        arows = {}
+        for r0, nr, _, _, _ in blocks:
+            if (r0, nr) not in arows:
+                ap, sa, _ = self._convert_rows(("a", r0, nr), nr, self.a_rows.data_ptr() + r0 * n * esz, 0, 0, s)
+                arows[(r0, nr)] = (ap, sa)
+        streams = self._side_streams(len(blocks))
+        ready = torch.cuda.Event()
+        ready.record(main)
+        done = []
+        for bi, ((r0, nr, c0, nc, h), ss) in enumerate(zip(blocks, streams)):
+            ss.wait_event(ready)
+            st = ss.cuda_stream
+            ap, sa = arows[(r0, nr)]
+            c_ptr = self.brows.data_ptr() + (r0 * n + c0) * esz
+            if h is None:
+                # the diagonal block b[R_g, R_g] is skew-Hermitian: its lower
+                # 256-tiles only, mirrored into itself (the single-GPU scheme),
+                # from the skew-B planes of P rows R_g converted in phase 1
+                self._product(("g2", bi), ap, sa, nr, self.pb, self.sp, nc, st, c=c_ptr, mirror=c_ptr, lower=1)
+            else:
+                # rows c0 .. c0 + nc of the skew-Hermitian P as the B operand of P[:, C]
+                bp, sb, _ = self._convert_rows(("b", bi), nc, self.p.data_ptr() + c0 * n * esz, 1, c0, st)
+                mir = self.bptrs[h] + ((c0 - h * self.m) * n + self.r0 + r0) * esz
+                self._product(("g2", bi), ap, sa, nr, bp, sb, nc, st, c=c_ptr, mirror=mir)
+            ev = torch.cuda.Event()
+            ev.record(ss)
+            done.append(ev)
+        for ev in done:
+            main.wait_event(ev)
+
+
+def _local_max(flags) -> float:
+    """Max over this process's ranks of the device residual bit patterns; one
+    host read (NaN -> inf: never converged, integrator.py:131)."""
+    bits = torch.max(torch.stack([f.reshape(()) for f in flags])) if len(flags) > 1 else flags[0].reshape(())
+    v = torch.tensor([int(bits.item())], dtype=torch.int64).view(torch.float64).item()
+    return math.inf if v != v else v
 
 
 def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda: None,
-                       allreduce_max=lambda v: v):
+                       allreduce_max=_local_max):
     """integrator.py:96-171 over row blocks with peer-fused collectives.
     `ranks` / `w_rows`: the ranks this process drives and their rows of W_n.
     Returns (rows of W_{n+1}, iterations, residual)."""
@@ -345,8 +510,8 @@ def peer_midpoint_step(ranks, w_rows, h, tol=1e-12, max_iter=10, barrier=lambda:
         for rk, xr, wr in zip(ranks, x, w_rows):
             nx, rr = rk.phase2b(wr, xr, hh, qq)
             new.append(nx)
-            res.append(math.inf if rr != rr else rr)
-        r = allreduce_max(max(res))  # also orders the broadcast before the next solve
+            res.append(rr)
+        r = allreduce_max(res)  # also orders the broadcast before the next solve
         x = new
         if r <= tol:
             break
@@ -387,14 +552,15 @@ class PeerShardedStepper:
         self._hb = symm.rendezvous(brows, name)
         xptrs = torch.tensor(self._hx.buffer_ptrs, dtype=torch.int64, device=dev)
         aptrs = torch.tensor(self._ha.buffer_ptrs, dtype=torch.int64, device=dev)
-        self.r = PeerRank(n, self.world, self.rank, backend, xfull, acol, xptrs, aptrs, brows,
-                          list(self._hb.buffer_ptrs))
+        cls = OzPeerRank if backend.oz else PeerRank
+        self.r = cls(n, self.world, self.rank, backend, xfull, acol, xptrs, aptrs, brows, list(self._hb.buffer_ptrs))
         self.n, self.m, self.r0 = n, m, self.r.r0
 
-    def _allreduce_max(self, v: float) -> float:
-        t = torch.tensor([v], dtype=torch.float64, device=self.r.be.device)
+    def _allreduce_max(self, flags) -> float:
+        # integer MAX over the ranks' residual bit patterns, on the device
+        t = flags[0].clone()
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        return float(t.item())
+        return _local_max([t])
 
     def midpoint_step(self, w_rows, h, tol=1e-12, max_iter=10):
         out, k, r = peer_midpoint_step([self.r], [w_rows], h, tol, max_iter,

@@ -108,3 +108,17 @@ def test_sharded_requires_divisible_n():
     # single process (no process group): world = 1, any N divides
     st = ShardedStepper(10, CpuBackend())
     assert st.m == 10 and st.r0 == 0
+
+
+def test_residual_bit_pattern_max():
+    """The peer path reduces residuals as int64 bit patterns of non-negative
+    doubles (one host read per update): the max is the max double, NaN wins
+    and reads back as inf (never converged, integrator.py:131)."""
+    from paper_2206_05466_b200.sharded import _local_max
+
+    def bits(v):
+        return torch.tensor([v], dtype=torch.float64).view(torch.int64)
+
+    assert _local_max([bits(1e-13), bits(3e-12), bits(0.0)]) == 3e-12
+    assert _local_max([bits(2.5e-14)]) == 2.5e-14
+    assert _local_max([bits(1e-13), bits(float("nan"))]) == float("inf")

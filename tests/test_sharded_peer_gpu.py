@@ -1,5 +1,6 @@
 """Peer-fused sharded step (sharded.py: collectives as epilogue stores into
-the other ranks' buffers).  G virtual ranks on one GPU run the algorithm
+the other ranks' buffers) on the library's step product (the INT8 Ozaki-II
+GEMM by default; a subprocess runs the DMMA variant).  G virtual ranks on one GPU run the algorithm
 phase by phase (every kernel's inputs are complete before it starts; no rank
 waits on another), and must reproduce the single-GPU step; the symmetric-
 memory path runs on a one-rank NCCL group."""
@@ -15,9 +16,10 @@ pytestmark = pytest.mark.gpu
 
 
 def _virtual_ranks(n, world, dev):
-    from paper_2206_05466_b200.sharded import DeviceBackend, PeerRank
+    from paper_2206_05466_b200.sharded import DeviceBackend, OzPeerRank, PeerRank
 
     be = DeviceBackend(n, dev)
+    cls = OzPeerRank if be.oz else PeerRank
     m = n // world
     xf = [torch.zeros((n, n), dtype=torch.complex128, device=dev) for _ in range(world)]
     ac = [torch.zeros((n, m), dtype=torch.complex128, device=dev) for _ in range(world)]
@@ -25,7 +27,7 @@ def _virtual_ranks(n, world, dev):
     xp = torch.tensor([t.data_ptr() for t in xf], dtype=torch.int64, device=dev)
     ap = torch.tensor([t.data_ptr() for t in ac], dtype=torch.int64, device=dev)
     bp = [t.data_ptr() for t in br]
-    return [PeerRank(n, world, g, be, xf[g], ac[g], xp, ap, br[g], bp) for g in range(world)]
+    return [cls(n, world, g, be, xf[g], ac[g], xp, ap, br[g], bp) for g in range(world)]
 
 
 @pytest.mark.parametrize("n,world", ((256, 2), (512, 4), (384, 3), (512, 8), (640, 5), (768, 6), (300, 3), (200, 4), (210, 6)))
@@ -100,3 +102,31 @@ def test_symmetric_memory_path_one_rank():
         assert k == kr and relf(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
     finally:
         dist.destroy_process_group()
+
+
+def test_virtual_ranks_default_product_is_int8():
+    from paper_2206_05466_b200.sharded import DeviceBackend, OzPeerRank
+
+    dev = torch.device("cuda:0")
+    assert DeviceBackend(256, dev).oz
+    assert isinstance(_virtual_ranks(256, 2, dev)[0], OzPeerRank)
+
+
+def test_virtual_ranks_native_dmma_variant():
+    """ZT_GEMM_ALGO=3m in a fresh process: the DMMA sharded kernels still
+    reproduce the single-GPU step."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import torch\n"
+        "from test_sharded_peer_gpu import test_virtual_ranks_match_single_gpu as t\n"
+        "t(512, 4); t(300, 3)\n"
+        "print('ok')\n"
+    )
+    env = dict(os.environ, ZT_GEMM_ALGO="3m", PYTHONPATH=os.pathsep.join([ROOT, os.path.join(ROOT, "tests")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
