@@ -1080,7 +1080,10 @@ __global__ void __launch_bounds__(256) k_update_rows_ew(int m, int n, const doub
     st2(out + o, nw);
     for (int h = 0; h < npeer; ++h) st2(reinterpret_cast<double*>(peers[h]) + ((size_t)(r0 + i) * n + j) * 2, nw);
   }
-  if (npeer) __threadfence_system();
+  if (npeer) {  // one system-scope fence per block (cumulative over the block's stores)
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
   if (resid) {
     unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(rmax));
     if (rmax != rmax) bits = 0x7ff8000000000000ull;
@@ -1112,7 +1115,8 @@ __global__ void k_rows_broadcast(int m, int n, const double* __restrict__ rows, 
     const double2 v = ld2(rows + (i * ld + j) * 2);
     for (int h = 0; h < npeer; ++h) st2(reinterpret_cast<double*>(peers[h]) + ((r0 + i) * (size_t)n + j) * 2, v);
   }
-  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 int rows_broadcast(int m, int n, const double* rows, int64_t ld, const unsigned long long* peers, int npeer, int r0,

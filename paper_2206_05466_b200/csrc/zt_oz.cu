@@ -739,38 +739,59 @@ __global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t*
 // Reconstruction for the row-block sharded step: C (m x n) into `c` (may be
 // null), and/or column j into rank h = j / mloc's N x mloc buffer a[:, R_h]
 // at row r0 + i (peer pointers: the all-to-all of the a tiles fused into the
-// epilogue), and/or -conj(C)^T into `mirror` (the partner's rows of the
-// skew-Hermitian b, ld_mirror).
+// reconstruction), and/or -conj(C)^T into `mirror` (the partner's rows of
+// the skew-Hermitian b, ld_mirror).  A block is 8 rows x 64 columns (a warp
+// per row, 2 columns per lane): direct stores are whole-warp 1 KB runs, and
+// the mirror goes through shared memory so each of its rows receives one
+// 128-byte run.  One system-scope fence per block orders the peer stores
+// (the rank barrier that follows publishes them).
+constexpr int RX_ROWS = 8, RX_COLS = 64;
 __global__ void __launch_bounds__(256, 4) k_oz_recon_ex(int m, int n, const int8_t* __restrict__ r, int mp, int np,
                                                       const int* __restrict__ rs, const int* __restrict__ cs,
                                                       double* c, int64_t ldc, const unsigned long long* peers,
                                                       int mloc, int r0, double* mirror, int64_t ldm, int lower) {
-  const int i = blockIdx.y;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
+  __shared__ double2 tl[RX_ROWS][RX_COLS + 1];
+  const int lane = threadIdx.x & 31, wr = threadIdx.x >> 5;
+  const int i0 = blockIdx.y * RX_ROWS, jb = blockIdx.x * RX_COLS;
+  const int i = i0 + wr, j0 = jb + lane * OZ_RECON_COLS;
   pdl_trigger();
   pdl_wait();
-  if (i >= m || j0 >= n) return;
   // lower (square, from a lower-mode residue GEMM): only 256-tiles on or
   // below the diagonal were computed; entries of strictly-lower tiles are
   // also mirrored, diagonal tiles are complete on both sides
-  if (lower && (j0 >> 8) > (i >> 8)) return;
-  double vr[OZ_RECON_COLS], vi[OZ_RECON_COLS];
-  crt_values(r, mp, np, i, j0, vr, vi);
-  const int ri = rs[i];
+  if (lower && (jb >> 8) > (i0 >> 8)) return;  // 8 | 256 and 64 | 256: whole block in one tile pair
+  const bool mirror_blk = mirror && !(lower && (jb >> 8) == (i0 >> 8));
+  if (i < m && j0 < n) {
+    double vr[OZ_RECON_COLS], vi[OZ_RECON_COLS];
+    crt_values(r, mp, np, i, j0, vr, vi);
+    const int ri = rs[i];
 #pragma unroll
-  for (int e = 0; e < OZ_RECON_COLS; ++e) {
-    const int j = j0 + e;
-    if (j >= n) continue;
-    const double2 o = scaled(vr[e], vi[e], ri, cs[j]);
-    if (c) st2(c + ((size_t)i * ldc + j) * 2, o);
-    if (peers) {
-      const int h = j / mloc;
-      double* dst = reinterpret_cast<double*>(peers[h]);
-      st2(dst + ((size_t)(r0 + i) * mloc + (j - h * mloc)) * 2, o);
+    for (int e = 0; e < OZ_RECON_COLS; ++e) {
+      const int j = j0 + e;
+      if (j >= n) continue;
+      const double2 o = scaled(vr[e], vi[e], ri, cs[j]);
+      if (c) st2(c + ((size_t)i * ldc + j) * 2, o);
+      if (peers) {
+        const int h = j / mloc;
+        double* dst = reinterpret_cast<double*>(peers[h]);
+        st2(dst + ((size_t)(r0 + i) * mloc + (j - h * mloc)) * 2, o);
+      }
+      if (mirror_blk) tl[wr][lane * OZ_RECON_COLS + e] = make_double2(-o.x, o.y);
     }
-    if (mirror && !(lower && (j >> 8) == (i >> 8))) st2(mirror + ((size_t)j * ldm + i) * 2, make_double2(-o.x, o.y));
   }
-  if (peers || mirror) __threadfence_system();
+  if (mirror_blk) {
+    __syncthreads();
+    // mirror row jj (64 of them) x RX_ROWS columns: 8 lanes per row
+    for (int t = threadIdx.x; t < RX_COLS * RX_ROWS; t += blockDim.x) {
+      const int jj = t / RX_ROWS, ii = t % RX_ROWS;
+      const int j = jb + jj, ir = i0 + ii;
+      if (j < n && ir < m) st2(mirror + ((size_t)j * ldm + ir) * 2, tl[ii][jj]);
+    }
+  }
+  if (peers || mirror) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
 }
 
 static cudaError_t launch_recon(int m, int n, const int8_t* r, int mp, int np, const int* rs, const int* cs, double* c,
@@ -1191,8 +1212,8 @@ extern "C" int zt_oz_reconstruct(int m, int n, const void* r, const int* rs, con
   using namespace zt;
   if (m < 1 || n < 1 || !r || !rs || !cs || (!c && !peers && !mirror) || (peers && mloc < 1) || (lower && m != n))
     return fail(ZT_EINVAL, "zt_oz_reconstruct: bad argument");
-  const dim3 grid((n + 256 * OZ_RECON_COLS - 1) / (256 * OZ_RECON_COLS), m);
-  ZT_CUDA_CHECK(launch_pdl(k_oz_recon_ex, grid, dim3(256), 0, (cudaStream_t)stream, m, n,
+  const dim3 grid((n + RX_COLS - 1) / RX_COLS, (m + RX_ROWS - 1) / RX_ROWS);
+  ZT_CUDA_CHECK(launch_pdl(k_oz_recon_ex, grid, dim3(32 * RX_ROWS), 0, (cudaStream_t)stream, m, n,
                            static_cast<const int8_t*>(r), (int)oz_pad(m), (int)oz_pad(n), rs, cs, c, ldc, peers, mloc,
                            r0, mirror, ld_mirror, lower));
   ZT_LAUNCHED();
