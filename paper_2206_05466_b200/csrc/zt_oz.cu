@@ -670,7 +670,7 @@ constexpr int OZ_RECON_COLS = 2;
 // the centred integers Re, Im of product entries (i, j0 .. j0 + C - 1)
 // before scaling
 __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp, int np, int i, int j0, double* vr,
-                                           double* vi) {
+                                           double* vi, const CrtConst& cc = c_crt) {
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
   constexpr int C = OZ_RECON_COLS;
   using word_t = unsigned short;
@@ -689,20 +689,20 @@ __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp,
     for (int k = 0; k < OZ_NPC; ++k) s[e][k] = 0.0;
 #pragma unroll
   for (int t = 0; t < OZ_NMOD; ++t) {
-    const double bias = c_crt.bias[t];
+    const double bias = cc.bias[t];
 #pragma unroll
     for (int e = 0; e < 2 * C; ++e) {
       const double u = byte_to_double(e < C ? wr[t] : wi[t], e % C, bias);
 #pragma unroll
-      for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, e < C ? c_crt.wr[t][k] : c_crt.wi[t][k], s[e][k]);
+      for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, e < C ? cc.wr[t][k] : cc.wi[t][k], s[e][k]);
     }
   }
 #pragma unroll
   for (int e = 0; e < 2 * C; ++e) {
-    const double q = rint(((s[e][2] + s[e][1]) + s[e][0]) * c_crt.m_inv);
-    const double d2 = fma(-q, c_crt.mp[2], s[e][2]);
-    const double d1 = fma(-q, c_crt.mp[1], s[e][1]);
-    const double d0 = fma(-q, c_crt.mp[0], s[e][0]);
+    const double q = rint(((s[e][2] + s[e][1]) + s[e][0]) * cc.m_inv);
+    const double d2 = fma(-q, cc.mp[2], s[e][2]);
+    const double d1 = fma(-q, cc.mp[1], s[e][1]);
+    const double d0 = fma(-q, cc.mp[0], s[e][0]);
     const double x = (d2 + d1) + d0;
     if (e < C)
       vr[e] = x;
@@ -1085,9 +1085,15 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   }
   rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bx, rres, 0, st);
   if (rc) return rc;
+  if (gemm1_only) {
+    ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sx, a, n, 0, st));
+    ZT_LAUNCHED();
+    return final_commutator(n, a, wn, hh, out, st);
+  }
+  // (a fused reconstruction + row conversion, one block per row of a with
+  // the row re-read from L2, measured 184 us against 48 + 83 us: removed)
   ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sx, a, n, 0, st));
   ZT_LAUNCHED();
-  if (gemm1_only) return final_commutator(n, a, wn, hh, out, st);
   ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, (const double*)a, (int64_t)n, pd, pd,
                            kb, 0, 0, ares, sa, (int8_t*)nullptr));
   ZT_LAUNCHED();
