@@ -684,7 +684,7 @@ def run_ours(args):
 
 # ncu --set full dram bytes per launch (profiles/): the residue GEMM and the
 # DMMA path's fused update
-TRAFFIC_OZ = (285.3 + 115.4) * 1e6
+TRAFFIC_OZ = (285.3 + 119.2) * 1e6
 TRAFFIC_OZ_SRC = "ncu --set full, one 17-modulus k_oz_gemm at N = 2048, profiles/r02_ncu_summary.md (not measured in this run)"
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
