@@ -170,6 +170,7 @@ __device__ __forceinline__ void commit_both(uint64_t* bar) {
 struct GemmArgs {
   int nmod, mt, nt, kt;  // pair tiles per dimension (256 rows / columns) and K blocks (64 B)
   int lower;             // square: only the 256-tiles on or below the diagonal
+  int bswap;             // B planes read swapped (phi- with U, phi+ with V): B = conj of the converted rows
   int mp, np;            // padded M, N (output leading dimension np)
   int8_t* r;             // [nmod][2][mp][np]
 };
@@ -265,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         work_of(g, w, per, j, tm, tn);
         for (int part = 0; part < 2; ++part) {
           const int ra = (j * 2 + part) * g.mp + tm * TM + rank * 128;
-          const int rb = (j * 2 + part) * g.np + tn * TN + rank * (TN / 2);
+          const int rb = (j * 2 + (part ^ g.bswap)) * g.np + tn * TN + rank * (TN / 2);
           for (int kb = 0; kb < g.kt; kb += KPS, ++it) {
             const int s = it % STAGES;
             wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -936,7 +937,7 @@ void oz_profile_enable(bool on) {
 // R residues for every modulus (see the header comment); mp, np multiples
 // of 256, kp of 128
 int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* b, int8_t* r, int lower,
-               cudaStream_t st) {
+               cudaStream_t st, int bswap = 0) {
   using namespace oz;
   // kp <= 2^14 keeps |accumulator| < 89 2^22 (modx's exact range)
   if (nmod < 1 || nmod > OZ_NMOD || mp % TM || np % TN || kp % (KPS * TK) || kp > 16384 || (lower && mp != np))
@@ -955,6 +956,7 @@ int oz_modgemm(int nmod, int mp, int np, int kp, const int8_t* a, const int8_t* 
   g.nt = np / TN;
   g.kt = kp / TK;
   g.lower = lower;
+  g.bswap = bswap;
   g.mp = mp;
   g.np = np;
   g.r = r;
@@ -1066,16 +1068,16 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   const int pd = (int)oz_pad(n);
   const int kb = oz_bits(n);
   const size_t pl = (size_t)OZ_NMOD * pd * pd;
-  int8_t* ares = static_cast<int8_t*>(ws);
+  int8_t* ares = static_cast<int8_t*>(ws);  // P rows (A operand of both products)
   int8_t* bx = ares + 2 * pl;   // X as B operand
-  int8_t* bp = bx + 2 * pl;     // P as B operand
-  int8_t* rres = bp + 2 * pl;
+  int8_t* ba = bx + 2 * pl;     // a rows (B operand of GEMM-2, planes read swapped: a^H)
+  int8_t* rres = ba + 2 * pl;
   int* sp = reinterpret_cast<int*>(rres + 2 * pl);  // P rows (= P-as-B columns)
   int* sx = sp + pd;                                // X columns
   int* sa = sx + pd;                                // a rows
-  // P: A layout and skew-B layout in one pass
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, p, (int64_t)n, pd, pd, kb,
-                           gemm1_only ? 0 : 2, 0, ares, sp, gemm1_only ? (int8_t*)nullptr : bp));
+  // P rows: the A operand of GEMM-1 and of GEMM-2
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, p, (int64_t)n, pd, pd, kb, 0, 0, ares,
+                           sp, (int8_t*)nullptr));
   ZT_LAUNCHED();
   if (x_join) {
     ZT_CUDA_CHECK(cudaStreamWaitEvent(st, x_join, 0));
@@ -1095,11 +1097,17 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sx, a, n, 0, st));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, (const double*)a, (int64_t)n, pd, pd,
-                           kb, 0, 0, ares, sa, (int8_t*)nullptr));
+                           kb, 0, 0, ba, sa, (int8_t*)nullptr));
   ZT_LAUNCHED();
-  rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, bp, rres, 1, st);
+  // b = a P = P X P computed as P a^H (a^H = (P X)^H = X P for the
+  // skew-Hermitian iterate and stream matrix): the A planes are P's rows from
+  // GEMM-1, the B operand a^H is the conjugate of a's rows, i.e. a's row
+  // planes with phi+ and phi- swapped (column scales = a's row scales), so P
+  // needs no second (skew-B) layout; lower 256-tiles only, mirrored by the
+  // update pass
+  rc = oz_modgemm(OZ_NMOD, pd, pd, pd, ares, ba, rres, 1, st, 1);
   if (rc) return rc;
-  ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sa, sp, bbuf, n, 1, st));
+  ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sa, bbuf, n, 1, st));
   ZT_LAUNCHED();
   ZT_CUDA_CHECK(cudaGetLastError());
   return update_pairs(n, a, bbuf, out, base, xprev, wn, hh, qq, resid, cons, st);
