@@ -253,19 +253,30 @@ static void prof_collect() {
 // INT8 path: X's column conversion is independent of the solve, so it runs
 // on a side stream forked from `st` (event fork / join: captured into the
 // step graph as parallel branches) while the latency-bound solve runs.
-static thread_local cudaStream_t t_side = nullptr;
-static thread_local cudaEvent_t t_fork = nullptr, t_join = nullptr;
+// Streams and events this library creates lazily, per calling thread AND per
+// device (a stream belongs to the device current when it was created)
+struct DevStreams {
+  cudaStream_t side = nullptr, cap[2] = {nullptr, nullptr}, copy = nullptr, copy2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, copy_ev = nullptr, copy_ev2 = nullptr, reset_ev = nullptr;
+};
+static thread_local DevStreams t_ds[64];
+static DevStreams& ds() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  return t_ds[dev];
+}
 static int oz_fork_x(int n, const double* x, StepWS& w, cudaStream_t st) {
-  if (!t_side) {
-    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_side, cudaStreamNonBlocking));
-    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_fork, cudaEventDisableTiming));
-    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_join, cudaEventDisableTiming));
+  DevStreams& d = ds();
+  if (!d.side) {
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming));
   }
-  ZT_CUDA_CHECK(cudaEventRecord(t_fork, st));
-  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_side, t_fork, 0));
-  const int rc = oz_convert_x(n, x, w.oz, t_side);
+  ZT_CUDA_CHECK(cudaEventRecord(d.fork, st));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(d.side, d.fork, 0));
+  const int rc = oz_convert_x(n, x, w.oz, d.side);
   if (rc) return rc;
-  ZT_CUDA_CHECK(cudaEventRecord(t_join, t_side));
+  ZT_CUDA_CHECK(cudaEventRecord(d.join, d.side));
   return ZT_OK;
 }
 
@@ -283,7 +294,7 @@ static int update(zt_operator* op, const double* x, const double* base, const do
   if (rc) return rc;
   prof_mark(1, st);
   if (g_algo == 2) {
-    rc = oz_update(n, w.p, x, w.a, w.b, base, xprev, wn, out, hh, qq, resid, cons, w.oz, st, 0, t_join);
+    rc = oz_update(n, w.p, x, w.a, w.b, base, xprev, wn, out, hh, qq, resid, cons, w.oz, st, 0, ds().join);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;
@@ -324,7 +335,7 @@ static int final_update(zt_operator* op, double* x, const double* wn, double h, 
   if (rc) return rc;
   prof_mark(1, st);
   if (g_algo == 2) {
-    rc = oz_update(n, w.p, x, w.a, nullptr, nullptr, nullptr, wn, x, h, 0.0, nullptr, nullptr, w.oz, st, 1, t_join);
+    rc = oz_update(n, w.p, x, w.a, nullptr, nullptr, nullptr, wn, x, h, 0.0, nullptr, nullptr, w.oz, st, 1, ds().join);
     prof_mark(2, st);
     prof_mark(3, st);
     return rc;
@@ -428,16 +439,17 @@ struct GraphEntry {
   int64_t kp = 0, kb = 0, ke = 0;  // kernels in prologue / per iteration / epilogue
 };
 static thread_local std::vector<GraphEntry> t_graphs;
-static thread_local cudaStream_t t_cap[2] = {nullptr, nullptr};
+
 // ZT_GRAPH=0 or zt_set_graph(0): eager step with per-iteration host sync
 static std::atomic<bool> g_graph{env_on("ZT_GRAPH", true)};
 
 static int build_step_graph(GraphEntry& e, StepWS& w) {
   zt_operator* op = e.op;
   const int n = op->n;
-  for (auto& s : t_cap)
+  DevStreams& d = ds();
+  for (auto& s : d.cap)
     if (!s) ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  cudaStream_t cs = t_cap[0], cb = t_cap[1];
+  cudaStream_t cs = d.cap[0], cb = d.cap[1];
   const double hh = 0.5 * e.h, qq = 0.25 * e.h * e.h;
   double* x = e.wnext;
   t_capturing = true;
@@ -533,8 +545,6 @@ static wait_value_fn wait_value32() {
   }
   return fn;
 }
-static thread_local cudaStream_t t_copy = nullptr, t_copy2 = nullptr;
-static thread_local cudaEvent_t t_copy_ev = nullptr, t_copy_ev2 = nullptr, t_reset_ev = nullptr;
 
 // Enqueue the row-block device-to-host copies of W_{n+1} behind the progressive
 // final update's flags: clear the flags on `st`, then (after that clear, via an
@@ -542,28 +552,30 @@ static thread_local cudaEvent_t t_copy_ev = nullptr, t_copy_ev2 = nullptr, t_res
 // Call right before the step graph launch on `st`; `join` makes `st` wait for
 // the copies (call after the launch).
 static int host_copy_prologue(int n, StepWS& w, cudaStream_t st) {
-  if (!t_copy) {
-    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_copy, cudaStreamNonBlocking));
-    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&t_copy2, cudaStreamNonBlocking));
-    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_copy_ev, cudaEventDisableTiming));
-    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_copy_ev2, cudaEventDisableTiming));
-    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&t_reset_ev, cudaEventDisableTiming));
+  DevStreams& d = ds();
+  if (!d.copy) {
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaStreamCreateWithFlags(&d.copy2, cudaStreamNonBlocking));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&d.copy_ev, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&d.copy_ev2, cudaEventDisableTiming));
+    ZT_CUDA_CHECK(cudaEventCreateWithFlags(&d.reset_ev, cudaEventDisableTiming));
   }
   const int T = (n + 63) / 64;
   unsigned* flags = w.prog + (size_t)T * (T + 1) / 2 + T;
   ZT_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(unsigned) * T, st));
-  ZT_CUDA_CHECK(cudaEventRecord(t_reset_ev, st));
-  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_copy, t_reset_ev, 0));
-  ZT_CUDA_CHECK(cudaStreamWaitEvent(t_copy2, t_reset_ev, 0));
+  ZT_CUDA_CHECK(cudaEventRecord(d.reset_ev, st));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(d.copy, d.reset_ev, 0));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(d.copy2, d.reset_ev, 0));
   return ZT_OK;
 }
 static int host_copy_enqueue(int n, StepWS& w, double* host_out, cudaStream_t st) {
+  DevStreams& d = ds();
   const int T = (n + 63) / 64;
   const unsigned* flags = w.prog + (size_t)T * (T + 1) / 2 + T;
   // two copy streams (alternating blocks) so one block's flag wait and copy
   // setup overlap the other's transfer
   for (int s = 0; s < T; ++s) {
-    cudaStream_t cs = (s & 1) ? t_copy2 : t_copy;
+    cudaStream_t cs = (s & 1) ? d.copy2 : d.copy;
     const CUresult r = wait_value32()(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(flags + s),
                                       1u, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(ZT_ECUDA, "cuStreamWaitValue32 failed");
@@ -571,10 +583,10 @@ static int host_copy_enqueue(int n, StepWS& w, double* host_out, cudaStream_t st
     ZT_CUDA_CHECK(cudaMemcpyAsync(host_out + (size_t)s * 64 * n * 2, w.b + (size_t)s * 64 * n * 2, rows * n * 16,
                                   cudaMemcpyDeviceToHost, cs));
   }
-  ZT_CUDA_CHECK(cudaEventRecord(t_copy_ev, t_copy));
-  ZT_CUDA_CHECK(cudaEventRecord(t_copy_ev2, t_copy2));
-  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, t_copy_ev, 0));
-  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, t_copy_ev2, 0));
+  ZT_CUDA_CHECK(cudaEventRecord(d.copy_ev, d.copy));
+  ZT_CUDA_CHECK(cudaEventRecord(d.copy_ev2, d.copy2));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, d.copy_ev, 0));
+  ZT_CUDA_CHECK(cudaStreamWaitEvent(st, d.copy_ev2, 0));
   return ZT_OK;
 }
 
