@@ -65,24 +65,10 @@ namespace oz {
 constexpr int TM = 256, TN = 256, TK = 64;  // pair tile; TK in bytes (64 B swizzle)
 constexpr int A_BYTES = 128 * TK;          // one CTA's 128 rows of an A plane
 constexpr int B_BYTES = (TN / 2) * TK;     // one CTA's 128 columns of a B plane
-#ifdef OZX_NOEPI
-#define OZX_EPI 0
-#else
-#define OZX_EPI 1
-#endif
-#ifndef OZX_KPS
-#define OZX_KPS 2
-#endif
-#ifndef OZX_STAGES
-#define OZX_STAGES 6
-#endif
-constexpr int KPS = OZX_KPS;               // K blocks per pipeline stage
+constexpr int KPS = 2;                     // K blocks per pipeline stage
 constexpr int STAGE_BYTES = KPS * (A_BYTES + B_BYTES);
-constexpr int STAGES = OZX_STAGES;
-#ifndef OZX_EPI_WARPS
-#define OZX_EPI_WARPS 16
-#endif
-constexpr int EPI_WARPS = OZX_EPI_WARPS;  // 4 per TMEM lane quarter, 64 columns each
+constexpr int STAGES = 6;
+constexpr int EPI_WARPS = 16;             // 4 per TMEM lane quarter, 64 columns each
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 // D s32, A/B signed int8, K-major, M = 256 (pair), N = 256
@@ -301,9 +287,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               const uint32_t a = smem_u32(smem + s * STAGE_BYTES + u * (A_BYTES + B_BYTES)), b = a + A_BYTES;
 #pragma unroll
               for (int k = 0; k < TK / 32; ++k)
-#ifdef OZX_NOMMA
-                if (g.kt < 0)
-#endif
                 mma(d, sdesc(a + k * 32), sdesc(b + k * 32), (kb | u | k) ? 1u : 0u);
             }
             commit_both(&empty[s]);
@@ -333,7 +316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       wait(&tfull[0], lt & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-      for (int c = 0; c < (OZX_EPI ? CW : 0); c += 64) {
+      for (int c = 0; c < CW; c += 64) {
         uint32_t v[64];
         OZ_LD32(v, trow + c);
         OZ_LD32((v + 32), trow + c + 32);
@@ -355,7 +338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int8_t* out_s = g.r + ((size_t)(j * 2) * g.mp + row) * g.np + tn * TN + ch;
       int8_t* out_d = out_s + (size_t)g.mp * g.np;
 #pragma unroll
-      for (int c = 0; c < (OZX_EPI ? CW : 0); c += 64) {
+      for (int c = 0; c < CW; c += 64) {
         uint32_t v[64];
         OZ_LD32(v, trow + TN + c);
         OZ_LD32((v + 32), trow + TN + c + 32);
