@@ -435,6 +435,24 @@ __device__ __forceinline__ void phi_words(float yr, float yi, int t, uint32_t& w
   wp = __float_as_uint(fmaf(-qp, p, zp + OZ_MAGIC_F));
   wm = __float_as_uint(fmaf(-qm, p, zm + OZ_MAGIC_F));
 }
+// the same for two elements at once on the packed FP32 pipe (FFMA2 / FADD2,
+// sm_100): the conversions are instruction-issue bound, and the per-modulus
+// FP32 work is most of their instructions
+__device__ __forceinline__ void phi_words2(float2 yr, float2 yi, int t, uint32_t* wp, uint32_t* wm) {
+  const float p = c_oz_pf[t], pinv = c_oz_pinvf[t], io = c_oz_iota[t];
+  const float2 np2 = make_float2(-p, -p), pinv2 = make_float2(pinv, pinv), io2 = make_float2(io, io),
+               nio2 = make_float2(-io, -io), m2 = make_float2(OZ_MAGIC_F, OZ_MAGIC_F),
+               nm2 = make_float2(-OZ_MAGIC_F, -OZ_MAGIC_F);
+  const float2 qi = __fadd2_rn(__ffma2_rn(yi, pinv2, m2), nm2);
+  const float2 ri = __ffma2_rn(qi, np2, yi);
+  const float2 zp = __ffma2_rn(io2, ri, yr), zm = __ffma2_rn(nio2, ri, yr);
+  const float2 qp = __fadd2_rn(__ffma2_rn(zp, pinv2, m2), nm2), qm = __fadd2_rn(__ffma2_rn(zm, pinv2, m2), nm2);
+  const float2 rp = __ffma2_rn(qp, np2, __fadd2_rn(zp, m2)), rm = __ffma2_rn(qm, np2, __fadd2_rn(zm, m2));
+  wp[0] = __float_as_uint(rp.x);
+  wp[1] = __float_as_uint(rp.y);
+  wm[0] = __float_as_uint(rm.x);
+  wm[1] = __float_as_uint(rm.y);
+}
 // low bytes of four words into one (byte e from word e)
 __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
@@ -513,7 +531,7 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
     // running word pointers into the planes of modulus t
     uint32_t* pa = reinterpret_cast<uint32_t*>(out + (size_t)i * kp + k0);
     uint32_t* pb = reinterpret_cast<uint32_t*>((mode == 1 ? out : out2) + (size_t)i * kp + k0);
-#pragma unroll 1
+#pragma unroll
     for (int g = 0; g < OZ_NGRP; ++g) {
       float yr[4], yi[4];
 #pragma unroll
@@ -526,7 +544,8 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
         if (t >= OZ_NMOD) break;
         uint32_t wp[4], wm[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) phi_words(yr[e], yi[e], t, wp[e], wm[e]);
+        for (int e = 0; e < 4; e += 2)
+          phi_words2(make_float2(yr[e], yr[e + 1]), make_float2(yi[e], yi[e + 1]), t, wp + e, wm + e);
         const uint32_t ap = pack4(wp[0], wp[1], wp[2], wp[3]);
         const uint32_t am = pack4(wm[0], wm[1], wm[2], wm[3]);
         if (mode != 1) {
@@ -608,7 +627,8 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_cols(int kdim, int n, const 
       if (t >= OZ_NMOD) break;
       uint32_t wp[4], wm[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) phi_words(yr[e], yi[e], t, wp[e], wm[e]);
+      for (int e = 0; e < 4; e += 2)
+        phi_words2(make_float2(yr[e], yr[e + 1]), make_float2(yi[e], yi[e + 1]), t, wp + e, wm + e);
       pb[0] = pack4(wp[0], wp[1], wp[2], wp[3]);
       pb[pw] = pack4(wm[0], wm[1], wm[2], wm[3]);
       pb += 2 * pw;
