@@ -1237,11 +1237,11 @@ int final_commutator(int n, const double* a, const double* wn, double h, double*
 }
 
 // The update as a streaming pass over 32 x 32 tile pairs (R, C), R >= C:
-// new = base + hh (a - a^H) + qq b with b read where GEMM-2 computed it (the
-// lower and diagonal BM x BN GEMM tiles of `bm`) and mirrored (b_ji = -conj(b_ij))
-// elsewhere -- the same operands and operation order as the fused epilogue
-// (epilogue_tile<EPI_UPDATE>), so the result is bitwise identical; plus the
-// NaN-propagating residual / consistency maxima.  `out` may alias `xprev`
+// new = base + hh (a - a^H) + qq b with b read on and below the diagonal
+// and mirrored (b_ji = -conj(b_ij)) above it; every mirror pair is computed
+// from negated conjugate operands in the same operation order, so the new
+// iterate is exactly skew-Hermitian off the diagonal whenever the base is;
+// plus the NaN-propagating residual / consistency maxima.  `out` may alias `xprev`
 // (in-place iteration): every element is read and written by one thread.
 template <bool XP, bool WN>
 __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __restrict__ a,
@@ -1261,12 +1261,11 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
   const int R = I * 32, C = J * 32;
   pdl_wait();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const bool same_tile = (R / BM) == (C / BM);  // b computed on both sides
   double rmax = 0.0, cmax = 0.0;
   // all loads of both phases first (the in-place `out` == `xprev` stores
   // would otherwise pin every load behind the previous row's store)
   const bool two = I != J;
-  double2 aij[4], bij[4], b0[4], xp[4], w0[4], b0m[4], xpm[4], bm2[4], w0m[4];  // unused ones fold away
+  double2 aij[4], bij[4], b0[4], xp[4], w0[4], b0m[4], xpm[4], w0m[4];  // unused ones fold away
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int r = ty + 8 * q;
@@ -1290,9 +1289,27 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
     b0m[q] = okm ? ld2(base + om) : z;
     xpm[q] = (XP && okm) ? ld2_plain(xprev + om) : z;
     w0m[q] = (WN && okm) ? ld2(wn + om) : z;
-    bm2[q] = (okm && same_tile) ? ld2(bm + om) : z;
+  }
+  if (!two) {
+    // b is used from the lower half only: the upper half of a diagonal tile
+    // takes -conj of its mirror, like every other upper entry, so the new
+    // iterate is exactly skew-Hermitian off the diagonal whenever the base
+    // is (dd, unused by diagonal tiles until the loop below, holds b)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dd[ty + 8 * q][tx] = bij[q];
   }
   __syncthreads();
+  if (!two) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = ty + 8 * q;
+      if (r < tx) {
+        const double2 t = dd[tx][r];
+        bij[q] = make_double2(-t.x, t.y);
+      }
+    }
+    __syncthreads();  // every read of dd before the loop below rewrites it
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int r = ty + 8 * q;
@@ -1322,13 +1339,8 @@ __global__ void __launch_bounds__(256, 2) k_update_pairs(int n, const double* __
       if (i < n && j < n) {
         const double2 d = dd[tx][r];
         const double2 dji = make_double2(-d.x, d.y);
-        double2 bji;
-        if (same_tile) {
-          bji = bm2[q];
-        } else {
-          const double2 t = tb[r][tx];
-          bji = make_double2(-t.x, t.y);
-        }
+        const double2 t = tb[r][tx];
+        const double2 bji = make_double2(-t.x, t.y);
         const double2 nw = cadd(cadd(b0m[q], rmul(hh, dji)), rmul(qq, bji));
         if (XP) rmax = nanmax(rmax, hypot(nw.x - xpm[q].x, nw.y - xpm[q].y));
         if (WN) {

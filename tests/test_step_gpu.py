@@ -346,3 +346,35 @@ def test_gate_rejects_before_the_fixed_point(zt):
             assert k >= 1
         finally:
             _lib.lib.zt_set_graph(prev)
+
+
+def test_exact_skew_is_preserved_and_not_required(zt):
+    """From a W_n that is exactly skew-Hermitian off the diagonal (the
+    reference's generator and every solve output are), each step's W_{n+1}
+    is exactly skew off the diagonal too (the update and final passes write
+    mirror pairs as exact negated conjugates, like the reference's own
+    a - a^H); a W_n that is skew only to round-off still matches the oracle."""
+    n = 333
+    w = zo.smooth_initial(n)
+    off = ~np.eye(n, dtype=bool)
+    assert np.array_equal(w[off], (-w.conj().T)[off])
+    op = zt.build_operator(n)
+    x = dev(w)
+    ref = w
+    for _ in range(3):
+        x, k, _, _ = zt.integrator.midpoint_step_raw(x, 0.005, 1e-12, 10, op)
+        ref, kr, _ = zo.midpoint_step(ref, 0.005)
+        assert k == kr
+        got = x.cpu().numpy()
+        assert np.array_equal(got[off], (-got.conj().T)[off])
+    assert relf(got, ref) <= 1e-12
+    # skew to round-off only: perturb a few upper entries by 1e-15 relative
+    w2 = w.copy()
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        i, j = sorted(rng.choice(n, 2, replace=False))
+        w2[i, j] += 1e-15 * abs(w2[i, j]) * (1 + 1j)
+    assert not np.array_equal(w2[off], (-w2.conj().T)[off])
+    y, k2, _, _ = zt.integrator.midpoint_step_raw(dev(w2), 0.005, 1e-12, 10, op)
+    ref2, kr2, _ = zo.midpoint_step(w2, 0.005)
+    assert k2 == kr2 and relf(y.cpu().numpy(), ref2) <= 1e-12
