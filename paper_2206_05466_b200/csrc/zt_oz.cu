@@ -808,16 +808,6 @@ static cudaError_t launch_recon(int m, int n, const int8_t* r, int mp, int np, c
 static bool g_crt_ready[OZ_MAXDEV] = {};
 static int g_oz_sms[OZ_MAXDEV] = {};
 
-static int modpow(long long b, long long e, long long m) {
-  long long r = 1 % m;
-  b %= m;
-  while (e) {
-    if (e & 1) r = r * b % m;
-    b = b * b % m;
-    e >>= 1;
-  }
-  return (int)r;
-}
 static int modinv(int a, int p) {
   for (int y = 1; y < p; ++y)
     if ((long long)a * y % p == 1) return y;
@@ -829,12 +819,6 @@ static int sqrt_minus_one(int p) {
     if ((long long)x * x % p == p - 1) return x;
   return -1;
 }
-
-// host copies of the constants (for zt_oz_moduli and the tests)
-struct OzHost {
-  int iota[OZ_NMOD];
-};
-static OzHost h_oz;
 
 static int crt_init() {
   int dev = 0;
@@ -866,7 +850,6 @@ static int crt_init() {
     const int p = h_oz_p[t];
     const int io = sqrt_minus_one(p);
     if (io < 0) return fail(ZT_EINVAL, "oz: modulus without a square root of -1");
-    h_oz.iota[t] = io;
     const u128 mt = m / (u128)p;
     const int y = modinv((int)(mt % (u128)p), p);
     const int half = (p + 1) / 2;                      // 2^-1 mod p
@@ -883,7 +866,6 @@ static int crt_init() {
     pif[t] = 1.0f / (float)p;
     iof[t] = (float)io;
   }
-  (void)modpow;
   pieces(m, h.mp);
   h.m_inv = 1.0 / ((h.mp[2] + h.mp[1]) + h.mp[0]);
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
