@@ -606,6 +606,18 @@ def run_ours(args):
                 "TF_per_product": 8.0 * N**3 / (full_ms * 1e-3) / 1e12,
                 "dmma_peak_TF": load_fp64_peak()[0],
             },
+            "operand_supply": {
+                # int8 residue planes TMA-loaded from L2 per full product: 17 moduli x 2
+                # planes x (256 A rows + 256 B rows) per 256 x 256 pair tile x K
+                "bytes_per_launch": OZ_L2_BYTES(pd, nmod),
+                "TBps": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12,
+                "ceiling_TBps": OZ_L2_CEILING_TBPS,
+                "frac": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12 / OZ_L2_CEILING_TBPS,
+                "note": "the kernel's actual bound: the L2-to-SM operand supply (the same kernel with its "
+                        "epilogue compiled out moves the 2.28 GB at 12.4 TB/s in 184 us at N = 2048; on 36 / 74 "
+                        "SMs the per-SM rate is 1.38x / 1.3x higher, so the limit is aggregate); "
+                        "profiles/r02_ncu_summary.md",
+            },
             "accuracy": "relF vs extended precision <= 4e-16 at N = 5-256 (native FP64 DMMA 5.5e-16-1.1e-15); "
                         "per-row/column bound tests/test_oz_gpu.py",
         }
@@ -686,6 +698,13 @@ def run_ours(args):
 # DMMA path's fused update
 TRAFFIC_OZ = (285.3 + 119.2) * 1e6
 TRAFFIC_OZ_SRC = "ncu --set full, one 17-modulus k_oz_gemm at N = 2048, profiles/r02_ncu_summary.md (not measured in this run)"
+def OZ_L2_BYTES(pd, nmod):
+    return float(nmod * 2 * (pd // 256) ** 2 * pd * 512)
+
+
+# measured: the residue GEMM with its epilogue compiled out (TMA + MMA only),
+# N = 2048, 2.28 GB in 184 us (profiles/r02_ncu_summary.md)
+OZ_L2_CEILING_TBPS = 12.4
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
