@@ -156,3 +156,14 @@ def test_final_update_identity(n, h):
     sandwich = wt + 0.5 * h * (a - a.conj().T) - 0.25 * h * h * (a @ p)
     comm = w + h * (a - a.conj().T)
     assert relf(comm, sandwich) <= 1e-15
+
+
+def test_bench_arms_print_the_same_config():
+    """bench.py: both arms' `config` is the workload description only
+    (identical dicts, so a driver comparing them sees the same workload)."""
+    import bench
+
+    a = bench.bench_config([2, 2, 2])
+    b = bench.bench_config([2])
+    assert a == b
+    assert set(a) == {"workload", "N", "h", "tol", "max_iter", "init", "iterations_per_step"}
