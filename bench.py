@@ -47,7 +47,7 @@ H = 0.005
 TOL = 1e-12
 MAX_ITER = 10
 METRIC = "isospectral time-steps/sec at N=2048 complex128"
-WORKLOAD = "cfg4: full isospectral midpoint step on 1 GPU (N=2048, h=0.005, tol=1e-12)"
+WORKLOAD = "cfg4: full isospectral midpoint step (N=2048, h=0.005, tol=1e-12)"
 REASONS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
     0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -377,9 +377,11 @@ def run_sharded(args):
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"row-block sharded midpoint step, N={n}, h={h}", "N": n, "h": h,
-                   "iterations_per_step": sorted(set(iters)), "parallelism": f"rowblock{world}",
-                   "transport": transport,
+        "config": bench_config(iters) if n == N else {
+            "workload": f"cfg5: midpoint step N={n}, h={h}", "N": n, "h": h, "tol": TOL, "max_iter": MAX_ITER,
+            "init": f"W0 = lap^-1(random_admissible({n}, default_rng(0), 1/{n})) / ||.||_F",
+            "iterations_per_step": sorted(set(iters))},
+        "implementation": {"parallelism": f"rowblock{world}", "transport": transport,
                    "collectives": ("all-gather of X and all-to-all of a fused into the GEMM epilogues as NVLink "
                                    "peer stores (torch symmetric memory), rank barrier + NCCL all_reduce(max "
                                    "residual) per update") if transport == "p2p" else
