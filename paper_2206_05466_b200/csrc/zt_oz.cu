@@ -134,6 +134,12 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(IDESC), "r"(acc));
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.s32 %0, 1;\n}" : "+r"(pred) : "r"(0xffffffffu));
+  return pred != 0;
+}
 // arrive on the barrier at this offset in both CTAs once the issued MMAs finish
 __device__ __forceinline__ void commit_both(uint64_t* bar) {
   asm volatile(
@@ -241,21 +247,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   pdl_trigger();
   pdl_wait();  // operands from the conversions; R still read by the previous reconstruction
 
+  // producer and MMA issuer: the whole warp runs the loop (warp-uniform
+  // values stay in uniform registers, no per-instruction uniformity loops)
+  // and one elected lane issues — the issuer shares its SM sub-partition with
+  // four epilogue warps, so its instruction count per stage matters
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
-      const uint32_t fb0 = mapa(smem_u32(&full[0]), 0);
-      unsigned it = 0;
-      for (int w = cl; w < total; w += ncl) {
-        int j, tm, tn;
-        work_of(g, w, per, j, tm, tn);
-        for (int part = 0; part < 2; ++part) {
-          const int ra = (j * 2 + part) * g.mp + tm * TM + rank * 128;
-          const int rb = (j * 2 + (part ^ g.bswap)) * g.np + tn * TN + rank * (TN / 2);
-          for (int kb = 0; kb < g.kt; kb += KPS, ++it) {
-            const int s = it % STAGES;
-            wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+    }
+    const uint32_t fb0 = mapa(smem_u32(&full[0]), 0);
+    unsigned it = 0;
+    for (int w = cl; w < total; w += ncl) {
+      int j, tm, tn;
+      work_of(g, w, per, j, tm, tn);
+      for (int part = 0; part < 2; ++part) {
+        const int ra = (j * 2 + part) * g.mp + tm * TM + rank * 128;
+        const int rb = (j * 2 + (part ^ g.bswap)) * g.np + tn * TN + rank * (TN / 2);
+        for (int kb = 0; kb < g.kt; kb += KPS, ++it) {
+          const int s = it % STAGES;
+          wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          if (elect_one()) {
             unsigned char* st = smem + s * STAGE_BYTES;
             if (rank == 0) mbar_arrive_tx(&full[s], 2 * STAGE_BYTES);
 #pragma unroll
@@ -265,13 +277,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               tma2d_pair(su + A_BYTES, &mb, (kb + u) * TK, rb, fb0 + s * 8);
             }
           }
+          __syncwarp();
         }
       }
-      // drain: every issued stage consumed before this CTA may exit
-      for (int i = 0; i < STAGES; ++i, ++it) wait(&empty[it % STAGES], ((it / STAGES) & 1) ^ 1);
     }
+    // drain: every issued stage consumed before this CTA may exit
+    for (int i = 0; i < STAGES; ++i, ++it) wait(&empty[it % STAGES], ((it / STAGES) & 1) ^ 1);
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
+      const uint64_t dsm = sdesc(smem_u32(smem));
       unsigned it = 0, lt = 0;
       for (int w = cl; w < total; w += ncl, ++lt) {
         for (int part = 0; part < 2; ++part) {
@@ -282,16 +296,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const int s = it % STAGES;
             wait(&full[s], (it / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
+            if (elect_one()) {
 #pragma unroll
-            for (int u = 0; u < KPS; ++u) {
-              const uint32_t a = smem_u32(smem + s * STAGE_BYTES + u * (A_BYTES + B_BYTES)), b = a + A_BYTES;
+              for (int u = 0; u < KPS; ++u) {
+                // descriptor address field = shared-memory byte address >> 4
+                const uint64_t a = dsm + (uint64_t)((s * STAGE_BYTES + u * (A_BYTES + B_BYTES)) >> 4);
+                const uint64_t b = a + (A_BYTES >> 4);
 #pragma unroll
-              for (int k = 0; k < TK / 32; ++k)
-                mma(d, sdesc(a + k * 32), sdesc(b + k * 32), (kb | u | k) ? 1u : 0u);
+                for (int k = 0; k < TK / 32; ++k) mma(d, a + 2 * k, b + 2 * k, (kb | u | k) ? 1u : 0u);
+              }
+              commit_both(&empty[s]);
             }
-            commit_both(&empty[s]);
+            __syncwarp();
           }
-          commit_both(&tfull[part]);
+          if (elect_one()) commit_both(&tfull[part]);
+          __syncwarp();
         }
       }
     }

@@ -58,7 +58,10 @@ def test_moduli_split_gaussian_integers(lib):
 
 @pytest.mark.parametrize("nmod,mp,np_,kp,lower", [(1, 256, 256, 128, 0), (3, 256, 512, 384, 0), (17, 256, 256, 256, 0),
                                                   (2, 512, 512, 256, 1), (4, 768, 768, 128, 1),
-                                                  (5, 1024, 1024, 256, 1), (3, 768, 512, 640, 0)])
+                                                  (5, 1024, 1024, 256, 1), (3, 768, 512, 640, 0),
+                                                  # odd tile counts, more / fewer tiles than CTA pairs
+                                                  (17, 1024, 1280, 256, 0), (17, 1280, 1280, 128, 1),
+                                                  (1, 2048, 2048, 128, 0)])
 def test_residue_gemm_exact(lib, nmod, mp, np_, kp, lower):
     """R_j = ((U + V) + k_j, (U - V) + k_j) mod p_j with U = A+ B+^T, V = A- B-^T,
     exactly, on the CTA-pair (cta_group::2) tcgen05 kind::i8 kernel; the
