@@ -1,8 +1,10 @@
 // FP64-accurate complex GEMM on the INT8 tensor cores (Ozaki scheme II with
 // a Gaussian-integer split):
 //
-// * operands are scaled to integers (row / column power-of-two scales, up to
-//   53 significant bits) and reduced modulo NMOD = 17 pairwise-coprime odd
+// * operands are scaled to integers (row / column power-of-two scales; the
+//   line maximum is put at KB = 55 bits for K <= 4096, 54 up to K = 2^14, so
+//   entries down to a quarter / half of their line's maximum keep all 53 of
+//   their significant bits) and reduced modulo NMOD = 17 pairwise-coprime odd
 //   moduli p <= 241 whose prime factors are all = 1 mod 4;
 // * for such p, -1 has a square root iota mod p, so Z[i] / (p) splits into two
 //   copies of Z / p: phi+(x + iy) = x + iota y and phi-(x + iy) = x - iota y
@@ -17,9 +19,9 @@
 //   reassembling the exact integer product, which is scaled back.
 //
 // Moduli: 241 233 229 221(=13*17) 205(=5*41) 197 193 181 173 157 149 137 113
-// 109 101 97 89, product M ~ 2^124.16: 53-bit operands up to K = 2^14 (the
+// 109 101 97 89, product M ~ 2^124.16: KB-bit operands up to K = 2^14 (the
 // residue GEMM's exact-division range) with the complex sum bound
-// 2 K 2^106 < M / 2.
+// 2 K 2^(2 KB) < M / 2 (oz_bits).
 //
 // Layouts (int8 centred residues, zero padded to 256 in every dimension):
 //   A residues [NMOD][2][Mp][Kp]  planes phi+ (A), phi- (A)   (K-major rows)
@@ -192,9 +194,10 @@ __device__ __forceinline__ void work_of(const GemmArgs& g, int w, int per, int& 
 // s = l - 1 (m p - 2^(31+l) < p <= 2^l): no correction step, FMA / ALU pipes
 // only (a min-based correction lands on the slow XU pipe, which bound the
 // epilogue at 106% XU in ncu).
-__device__ __forceinline__ uint32_t modx(int v, uint32_t p, uint32_t m, uint32_t s, uint32_t off) {
-  const uint32_t u = (uint32_t)v + (p << 22) + off;
-  return u - (__umulhi(u, m) >> s) * p;
+// add = p 2^22 + off, np = -p (mod 2^32): u - q p as one IMAD with no negation
+__device__ __forceinline__ uint32_t modx(int v, uint32_t add, uint32_t m, uint32_t s, uint32_t np) {
+  const uint32_t u = (uint32_t)v + add;
+  return u + (__umulhi(u, m) >> s) * np;
 }
 __device__ __forceinline__ void st256(int8_t* p, const uint32_t* w) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
@@ -203,10 +206,10 @@ __device__ __forceinline__ void st256(int8_t* p, const uint32_t* w) {
 }
 // two 16-bit lanes holding values in [0, 2p - 2]: subtract p from each lane
 // that is >= p (no carries cross lanes: every lane stays in [0, 2^16))
-__device__ __forceinline__ uint32_t lanes_mod(uint32_t x2, uint32_t p, uint32_t c1) {
+__device__ __forceinline__ uint32_t lanes_mod(uint32_t x2, uint32_t np, uint32_t c1) {
   const uint32_t t = x2 + c1;                       // lane + 0x8000 - p: bit 15 set iff lane >= p
   const uint32_t msk = (t >> 15) & 0x00010001u;
-  return x2 - msk * p;
+  return x2 + msk * np;                             // msk * (2^32 - p) = -msk * p (mod 2^32)
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -325,6 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       work_of(g, w, per, j, tm, tn);
       const uint32_t p = (uint32_t)c_oz_p[j], pm = c_oz_m[j], ps = c_oz_s[j];
       const uint32_t k = p >> 1, c1 = (0x8000u - p) * 0x10001u, cim = (p - 1) * 0x10001u;
+      const uint32_t np = 0u - p, a0 = p << 22, ak = (p << 22) + k;
       const int row = tm * TM + rank * 128 + q * 32 + lane;
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ch;
       // U mod p (offset 0) kept in registers, 4 bytes per word; V is taken
@@ -342,8 +346,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const uint32_t lo = modx((int)v[4 * e], p, pm, ps, 0) | (modx((int)v[4 * e + 1], p, pm, ps, 0) << 16);
-          const uint32_t hi = modx((int)v[4 * e + 2], p, pm, ps, 0) | (modx((int)v[4 * e + 3], p, pm, ps, 0) << 16);
+          const uint32_t lo = modx((int)v[4 * e], a0, pm, ps, np) | (modx((int)v[4 * e + 1], a0, pm, ps, np) << 16);
+          const uint32_t hi =
+              modx((int)v[4 * e + 2], a0, pm, ps, np) | (modx((int)v[4 * e + 3], a0, pm, ps, np) << 16);
           ur[c / 4 + e] = __byte_perm(lo, hi, 0x6420);
         }
       }
@@ -367,10 +372,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int e = 0; e < 16; ++e) {
           const uint32_t uw = ur[c / 4 + e];
           const uint32_t u01 = __byte_perm(uw, 0u, 0x4140), u23 = __byte_perm(uw, 0u, 0x4342);
-          const uint32_t v01 = modx((int)v[4 * e], p, pm, ps, k) | (modx((int)v[4 * e + 1], p, pm, ps, k) << 16);
-          const uint32_t v23 = modx((int)v[4 * e + 2], p, pm, ps, k) | (modx((int)v[4 * e + 3], p, pm, ps, k) << 16);
-          const uint32_t s01 = lanes_mod(u01 + v01, p, c1), s23 = lanes_mod(u23 + v23, p, c1);
-          const uint32_t d01 = lanes_mod(u01 - v01 + cim, p, c1), d23 = lanes_mod(u23 - v23 + cim, p, c1);
+          const uint32_t v01 = modx((int)v[4 * e], ak, pm, ps, np) | (modx((int)v[4 * e + 1], ak, pm, ps, np) << 16);
+          const uint32_t v23 =
+              modx((int)v[4 * e + 2], ak, pm, ps, np) | (modx((int)v[4 * e + 3], ak, pm, ps, np) << 16);
+          const uint32_t s01 = lanes_mod(u01 + v01, np, c1), s23 = lanes_mod(u23 + v23, np, c1);
+          const uint32_t d01 = lanes_mod(u01 - v01 + cim, np, c1), d23 = lanes_mod(u23 - v23 + cim, np, c1);
           ws[e] = __byte_perm(s01, s23, 0x6420);
           wd[e] = __byte_perm(d01, d23, 0x6420);
         }
@@ -422,10 +428,11 @@ static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols, in
 // ---------------------------------------------------------------------------
 // Operand conversion: scale each row (A operand) / each column (B operand) of
 // a complex128 matrix by a power of two so its largest |re|, |im| lies in
-// [2^(KB-1), 2^KB), round to integers (exact in binary64 for KB <= 53), and
+// [2^(KB-1), 2^KB), round to integers (exact in binary64: the scaling is a
+// power of two and values >= 2^53 are integers already), and
 // write phi+- = (re +- iota im) mod p, centred, as int8 planes.
 //
-// Residues of an integer-valued x (|x| < 2^53) in two levels: y = x mod Q_g
+// Residues of an integer-valued x (|x| < 2^56) in two levels: y = x mod Q_g
 // for the groups Q_g = p_2g p_2g+1 < 2^16 (the last group is p_16 alone) in
 // FP64 (q = rint(x / Q) from the rounded reciprocal is floor or ceil, and
 // y = x - q Q is exact by FMA; |y| < 2^17), then in FP32 (exact integer
@@ -909,12 +916,14 @@ static int crt_init() {
   return ZT_OK;
 }
 
-// integer bits per operand entry so that |sum| < M / 2 over K terms (complex form)
+// integer bits per operand entry so that |sum| < M / 2 over K terms (complex
+// form): 55 for K <= 4096, 54 up to 2^14.  Capped at 56 so x / Q stays below
+// 2^51 for the group reduction's rint (smallest group Q = 89).
 static int oz_bits(int k) {
   double lg = 0.0;
   for (int t = 0; t < OZ_NMOD; ++t) lg += std::log2((double)h_oz_p[t]);
   const int kb = (int)std::floor((lg - 1.0 - std::log2(2.0 * k) - 1e-9) / 2.0);
-  return std::min(53, kb);
+  return std::min(56, kb);
 }
 
 static size_t oz_pad(int n) { return ((size_t)n + 255) / 256 * 256; }

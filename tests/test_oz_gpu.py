@@ -43,7 +43,8 @@ def _iotas(lib):
 
 def test_moduli_split_gaussian_integers(lib):
     """Every modulus is odd with a square root of -1 (prime factors = 1 mod 4),
-    pairwise coprime, product >= 2^124 (53-bit operands up to K = 2^15)."""
+    pairwise coprime, product >= 2^124; operand bits KB with 2 K 2^(2 KB) < M / 2:
+    55 up to K = 4096, 54 up to K = 2^14."""
     import math
 
     P, I = _moduli(lib), _iotas(lib)
@@ -54,6 +55,10 @@ def test_moduli_split_gaussian_integers(lib):
         for y in range(x + 1, len(P)):
             assert math.gcd(P[x], P[y]) == 1
     assert sum(math.log2(p) for p in P) >= 124.0
+    lg = sum(math.log2(p) for p in P)
+    for k, kb in ((256, 56), (2048, 55), (4096, 55), (8192, 54), (16384, 54)):
+        assert lib.zt_oz_bits(k) == kb
+        assert 1 + math.log2(k) + 2 * kb < lg - 1  # |Re C|, |Im C| <= 2 K 2^(2 KB) < M / 2
 
 
 @pytest.mark.parametrize("nmod,mp,np_,kp,lower", [(1, 256, 256, 128, 0), (3, 256, 512, 384, 0), (17, 256, 256, 256, 0),
@@ -232,13 +237,14 @@ def test_nan_and_inf_propagate(lib):
 
 def test_intra_row_dynamic_range_bound(lib):
     """Rows of A whose entries span 1e-20 .. 1 (and columns of B likewise):
-    the Ozaki-II product scales each row / column by its largest entry, so an
-    entry is kept to 2^-53 of its ROW maximum, not of itself; entries below
-    rowmax * 2^-53 are rounded away (native DGEMM keeps them).  The error is
-    therefore bounded per row / column,
-        |C~ - C|_ij <= sqrt2 2^-53 (rowmax_i(A) sum_k |B_kj| + colmax_j(B) sum_k |A_ik|) + 2u |C_ij|,
+    the Ozaki-II product scales each row / column so its largest entry has KB
+    integer bits (zt_oz_bits: 56 at K = 256), so an entry is kept to 2^-KB of
+    its ROW maximum, not of itself; entries below rowmax * 2^-KB are rounded
+    away (native DGEMM keeps them).  The error is therefore bounded per row /
+    column,
+        |C~ - C|_ij <= sqrt2 2^-KB (rowmax_i(A) sum_k |B_kj| + colmax_j(B) sum_k |A_ik|) + 2u |C_ij|,
     which this test checks entrywise against an extended-precision product,
-    together with the normwise error (no worse than native DMMA's)."""
+    together with the normwise error."""
     from paper_2206_05466_b200.integrator import zgemm
 
     n = 256
@@ -252,15 +258,14 @@ def test_intra_row_dynamic_range_bound(lib):
     c = _oz(lib, ad, bd)
     ref = (a.astype(np.clongdouble) @ b.astype(np.clongdouble)).astype(np.complex128)
     u = 2.0**-53
+    q = 2.0 ** -lib.zt_oz_bits(n)
     rowmax = np.maximum(np.abs(a.real), np.abs(a.imag)).max(axis=1)
     colmax = np.maximum(np.abs(b.real), np.abs(b.imag)).max(axis=0)
-    bound = np.sqrt(2) * u * (rowmax[:, None] * np.abs(b).sum(axis=0)[None, :]
+    bound = np.sqrt(2) * q * (rowmax[:, None] * np.abs(b).sum(axis=0)[None, :]
                               + colmax[None, :] * np.abs(a).sum(axis=1)[:, None]) * 1.01 + 2 * u * np.abs(ref)
     err = np.abs(c - ref)
     assert np.all(err <= bound), float(np.max(err / bound))
-    # normwise the row-scaled product stays at the 1e-15 level, but here it is
-    # NOT better than native DGEMM (measured 7.8e-16 vs 4.3e-16): DGEMM's error
-    # is componentwise in |A||B|, this one per row / column maximum
     native = zgemm(ad, bd).cpu().numpy()
+    print(f"intra-row range: oz relF {relf(c, ref):.2e}, native DMMA {relf(native, ref):.2e}")
     assert relf(c, ref) <= 2e-15
     assert relf(native, ref) <= 2e-15
