@@ -170,20 +170,48 @@ struct GemmArgs {
 };
 
 __host__ __device__ __forceinline__ int lower_count(int mt) { return mt * (mt + 1) / 2; }
-// work item w -> modulus j, pair tile (tm, tn)
+// work item w -> modulus j, pair tile (tm, tn).  Within a modulus the tiles
+// run in bands of GR row tiles, column tiles outer and rows inner inside a
+// band (lower mode: the same bands over the tiles with tn <= tm).  For
+// N <= 4096 a band is the whole modulus (column-major order); at N = 8192 the
+// ~74 tiles in flight share 16 row tiles of A and ~5 column tiles of B, and
+// the product runs ~3% faster than in column-major order (bands of 8: ~3%
+// slower; the kernel runs power-capped at that size, so fewer L2 misses
+// matter little).
+constexpr int GR = 16;
 __device__ __forceinline__ void work_of(const GemmArgs& g, int w, int per, int& j, int& tm, int& tn) {
   j = w / per;
   int t = w - j * per;
   if (g.lower) {
-    tm = 0;
-    while (t > tm) {
-      t -= tm + 1;
-      ++tm;
+    int r0 = 0;
+    for (;;) {
+      const int gs = min(GR, g.mt - r0);
+      const int cnt = gs * r0 + gs * (gs + 1) / 2;
+      if (t < cnt) {
+        if (t < gs * r0) {
+          tn = t / gs;
+          tm = r0 + t % gs;
+        } else {
+          t -= gs * r0;
+          int c = 0;
+          while (t >= gs - c) {
+            t -= gs - c;
+            ++c;
+          }
+          tn = r0 + c;
+          tm = tn + t;
+        }
+        return;
+      }
+      t -= cnt;
+      r0 += GR;
     }
-    tn = t;
   } else {
-    tm = t % g.mt;
-    tn = t / g.mt;
+    const int r0 = (t / (GR * g.nt)) * GR;
+    t -= r0 * g.nt;
+    const int gs = min(GR, g.mt - r0);
+    tn = t / gs;
+    tm = r0 + t % gs;
   }
 }
 
