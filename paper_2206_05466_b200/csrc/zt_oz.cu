@@ -537,6 +537,7 @@ __device__ __forceinline__ double2 oz_scale2(int sh) {
 // out2; the row scale is shared since |-conj(v)| = |v|).  One block per
 // padded row; 4 consecutive k per thread (one 32-bit store per plane).
 // <= 80 registers (3 blocks of 256 per SM)
+template <int MODE>
 __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const double* __restrict__ src, int64_t ld,
                                                        int mp, int kp, int kb, int mode, int diag0, int8_t* out,
                                                        int* __restrict__ shift, int8_t* out2 = nullptr) {
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
     const int sh8 = 8 * (diag0 + i - k0);
     // running word pointers into the planes of modulus t
     uint32_t* pa = reinterpret_cast<uint32_t*>(out + (size_t)i * kp + k0);
-    uint32_t* pb = reinterpret_cast<uint32_t*>((mode == 1 ? out : out2) + (size_t)i * kp + k0);
+    uint32_t* pb = reinterpret_cast<uint32_t*>((MODE == 1 ? out : out2) + (size_t)i * kp + k0);
 #pragma unroll
     for (int g = 0; g < OZ_NGRP; ++g) {
       float yr[4], yi[4];
@@ -602,12 +603,12 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
           phi_words2(make_float2(yr[e], yr[e + 1]), make_float2(yi[e], yi[e + 1]), t, wp + e, wm + e);
         const uint32_t ap = pack4(wp[0], wp[1], wp[2], wp[3]);
         const uint32_t am = pack4(wm[0], wm[1], wm[2], wm[3]);
-        if (mode != 1) {
+        if (MODE != 1) {
           pa[0] = ap;
           pa[pw] = am;
         }
         pa += 2 * pw;
-        if (mode != 0) {
+        if (MODE != 0) {
           // skew-B: -phi-+ off the diagonal, phi+- on it
           uint32_t bp = __vneg4(am), bm = __vneg4(ap);
           if (diag) {
@@ -617,8 +618,8 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
           }
           pb[0] = bp;
           pb[pw] = bm;
+          pb += 2 * pw;
         }
-        pb += 2 * pw;
       }
     }
   }
@@ -1040,11 +1041,11 @@ int oz_zgemm(int n, const double* a, int64_t lda, const double* b, int64_t ldb, 
   int* rsh = reinterpret_cast<int*>(rres + (size_t)OZ_NMOD * 2 * p * p);
   int* csh = rsh + p;
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(csh + p);
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, n, a, lda, p, p, kb, 0, 0, ares, rsh,
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows<0>, dim3(p), dim3(256), 0, st, n, n, a, lda, p, p, kb, 0, 0, ares, rsh,
                            (int8_t*)nullptr));
   ZT_LAUNCHED();
   if (bmode == 1) {
-    ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(p), dim3(256), 0, st, n, n, b, ldb, p, p, kb, 1, 0, bres, csh,
+    ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows<1>, dim3(p), dim3(256), 0, st, n, n, b, ldb, p, p, kb, 1, 0, bres, csh,
                              (int8_t*)nullptr));
     ZT_LAUNCHED();
   } else {
@@ -1117,7 +1118,7 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   int* sx = sp + pd;                                // X columns
   int* sa = sx + pd;                                // a rows
   // P rows: the A operand of GEMM-1 and of GEMM-2
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, p, (int64_t)n, pd, pd, kb, 0, 0, ares,
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows<0>, dim3(pd), dim3(256), 0, st, n, n, p, (int64_t)n, pd, pd, kb, 0, 0, ares,
                            sp, (int8_t*)nullptr));
   ZT_LAUNCHED();
   if (x_join) {
@@ -1137,7 +1138,7 @@ int oz_update(int n, const double* p, const double* x, double* a, double* bbuf, 
   // the row re-read from L2, measured 184 us against 48 + 83 us: removed)
   ZT_CUDA_CHECK(launch_recon(n, n, rres, pd, pd, sp, sx, a, n, 0, st));
   ZT_LAUNCHED();
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(pd), dim3(256), 0, st, n, n, (const double*)a, (int64_t)n, pd, pd,
+  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows<0>, dim3(pd), dim3(256), 0, st, n, n, (const double*)a, (int64_t)n, pd, pd,
                            kb, 0, 0, ba, sa, (int8_t*)nullptr));
   ZT_LAUNCHED();
   // b = a P = P X P computed as P a^H (a^H = (P X)^H = X P for the
@@ -1230,7 +1231,8 @@ extern "C" int zt_oz_convert_rows(int rows, int kdim, const double* src, int64_t
   if (rc) return rc;
   const int mp = (int)oz_pad(rows), kp = (int)oz_pad(kdim);
   cudaStream_t st = (cudaStream_t)stream;
-  ZT_CUDA_CHECK(launch_pdl(k_oz_conv_rows, dim3(mp), dim3(256), 0, st, rows, kdim, src, ld, mp, kp, kb, mode, diag0,
+  auto kern = mode == 0 ? k_oz_conv_rows<0> : (mode == 1 ? k_oz_conv_rows<1> : k_oz_conv_rows<2>);
+  ZT_CUDA_CHECK(launch_pdl(kern, dim3(mp), dim3(256), 0, st, rows, kdim, src, ld, mp, kp, kb, mode, diag0,
                            static_cast<int8_t*>(planes), shift, static_cast<int8_t*>(planes2)));
   ZT_LAUNCHED();
   return ZT_OK;
