@@ -699,14 +699,17 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_cols(int kdim, int n, const 
 //   Re C = sum_t s_t Wr_t mod M,  Wr_t = (2^-1 y_t mod p_t) M_t
 //   Im C = sum_t d_t Wi_t mod M,  Wi_t = ((2 iota_t)^-1 y_t mod p_t) M_t
 // (any representative of the residue works: a multiple of p_t times M_t is a
-// multiple of M).  W_t (< M < 2^124.2) and M are split into three signed
-// pieces on the grids 2^0, 2^42, 2^84, the two lower ones balanced in
-// [-2^41, 2^41) and the top one < 2^40.2, so with sum_t |c_t| <= 1404 < 2^11
-// every partial sum S_k and every q M_k (q = rint(S / M), |q| <= 1404) is
-// below 2^52, D_k = S_k - q M_k is exact, and x = D_2 + D_1 + D_0 is the
-// centred representative (|x| < M / 2 by the choice of KB).
+// multiple of M).  W_t (< M < 2^124.2) and M are split into signed pieces
+// on the grids 2^0, 2^42, 2^84, the two lower ones balanced in [-2^41, 2^41)
+// and the top one < 2^40.2, so with sum_t |c_t| <= 1404 < 2^11 every partial
+// sum S_k and every q M_k (q = rint(S / M), |q| <= 1404) is below 2^52 and
+// D_k = S_k - q M_k is exact.  Only the pieces on 2^84 and 2^42 are used:
+// dropping the 2^0 pieces of W_t and M changes x = D_2 + D_1 by at most
+// 2 * 1404 * 2^41 < 2^52.5, i.e. 2^-69 of the |x| <= 2 K 2^(2 KB) bound
+// (K = 2048, KB = 55) and ~2^-13 of the operands' own rounding error
+// (K 2^(KB-1)), and q is unchanged (|x| < M / 2 with a 12% margin).
 // ---------------------------------------------------------------------------
-constexpr int OZ_NPC = 3;
+constexpr int OZ_NPC = 2;  // pieces used: [0] on 2^42, [1] on 2^84
 struct CrtConst {
   double wr[OZ_NMOD][OZ_NPC];  // pieces of Wr_t
   double wi[OZ_NMOD][OZ_NPC];  // pieces of Wi_t
@@ -758,11 +761,10 @@ __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp,
   }
 #pragma unroll
   for (int e = 0; e < 2 * C; ++e) {
-    const double q = rint(((s[e][2] + s[e][1]) + s[e][0]) * cc.m_inv);
-    const double d2 = fma(-q, cc.mp[2], s[e][2]);
-    const double d1 = fma(-q, cc.mp[1], s[e][1]);
-    const double d0 = fma(-q, cc.mp[0], s[e][0]);
-    const double x = (d2 + d1) + d0;
+    const double q = rint((s[e][1] + s[e][0]) * cc.m_inv);
+    const double d2 = fma(-q, cc.mp[1], s[e][1]);
+    const double d1 = fma(-q, cc.mp[0], s[e][0]);
+    const double x = d2 + d1;
     if (e < C)
       vr[e] = x;
     else
@@ -885,17 +887,18 @@ static int crt_init() {
   CrtConst h;
   u128 m = 1;
   for (int t = 0; t < OZ_NMOD; ++t) m *= (u128)h_oz_p[t];
-  // balanced pieces: v = sum_k piece_k 2^(42 k), |piece_0|, |piece_1| <= 2^41
+  // balanced pieces: v = sum_k piece_k 2^(42 k), |piece_0|, |piece_1| <= 2^41;
+  // pieces 1 and 2 are kept (out[0], out[1]), piece 0 is dropped
   auto pieces = [](u128 v, double* out) {
     i128 rest = (i128)v;
-    for (int k = 0; k < OZ_NPC; ++k) {
+    for (int k = 0; k < 3; ++k) {
       i128 pk = rest;
-      if (k < OZ_NPC - 1) {
+      if (k < 2) {
         pk = rest & (((i128)1 << 42) - 1);
         if (pk >= ((i128)1 << 41)) pk -= (i128)1 << 42;
         rest = (rest - pk) >> 42;
       }
-      out[k] = std::ldexp((double)(long long)pk, 42 * k);  // <= 42 bits: exact
+      if (k > 0) out[k - 1] = std::ldexp((double)(long long)pk, 42 * k);  // <= 42 bits: exact
     }
   };
   int pm[OZ_NMOD];
@@ -922,7 +925,7 @@ static int crt_init() {
     iof[t] = (float)io;
   }
   pieces(m, h.mp);
-  h.m_inv = 1.0 / ((h.mp[2] + h.mp[1]) + h.mp[0]);
+  h.m_inv = 1.0 / (double)m;
   ZT_CUDA_CHECK(cudaMemcpyToSymbol(c_crt, &h, sizeof h));
   double qd[OZ_NGRP], qi[OZ_NGRP];
   for (int g = 0; g < OZ_NGRP; ++g) {
