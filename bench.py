@@ -615,10 +615,9 @@ def run_ours(args):
                 "TBps": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12,
                 "ceiling_TBps": OZ_L2_CEILING_TBPS,
                 "frac": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12 / OZ_L2_CEILING_TBPS,
-                "note": "the kernel's actual bound: the L2-to-SM operand supply (the same kernel with its "
-                        "epilogue compiled out moves the 2.28 GB at 12.4 TB/s in 184 us at N = 2048; on 36 / 74 "
-                        "SMs the per-SM rate is 1.38x / 1.3x higher, so the limit is aggregate); "
-                        "profiles/r02_ncu_summary.md",
+                "note": "the kernel's operand-supply floor: the same kernel with its MMAs and epilogue "
+                        "compiled out (TMA loads only) moves the 2.28 GB at 13.3 TB/s in 171.7 us at N = 2048 "
+                        "(MMAs alone 142.5 us, both 182 us); profiles/r02_ncu_summary.md",
             },
             "accuracy": "relF vs extended precision <= 4e-16 at N = 5-256 (native FP64 DMMA 5.5e-16-1.1e-15); "
                         "per-row/column bound tests/test_oz_gpu.py",
@@ -701,15 +700,15 @@ def run_ours(args):
 
 # ncu --set full dram bytes per launch (profiles/): the residue GEMM and the
 # DMMA path's fused update
-TRAFFIC_OZ = (285.3 + 119.2) * 1e6
+TRAFFIC_OZ = (285.3 + 118.0) * 1e6
 TRAFFIC_OZ_SRC = "ncu --set full, one 17-modulus k_oz_gemm at N = 2048, profiles/r02_ncu_summary.md (not measured in this run)"
 def OZ_L2_BYTES(pd, nmod):
     return float(nmod * 2 * (pd // 256) ** 2 * pd * 512)
 
 
-# measured: the residue GEMM with its epilogue compiled out (TMA + MMA only),
-# N = 2048, 2.28 GB in 184 us (profiles/r02_ncu_summary.md)
-OZ_L2_CEILING_TBPS = 12.4
+# measured: the residue GEMM with MMAs and epilogue compiled out (TMA loads
+# only), N = 2048, 2.28 GB in 171.7 us (profiles/r02_ncu_summary.md)
+OZ_L2_CEILING_TBPS = 13.3
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
