@@ -135,6 +135,29 @@ def test_complex_product_accuracy(lib, n):
     np.testing.assert_array_equal(cl[blk], c1[blk])
 
 
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_complex_product_accuracy_full_size(lib, n):
+    """The step's sizes: a P X-shaped product (P the solve of a random
+    skew-Hermitian field, X skew-Hermitian) at N = 2048 / 4096, checked on 16
+    rows against an extended-precision (x87 80-bit) product of those rows:
+    relF <= 4e-16 and no worse than the native FP64 DMMA product's rows."""
+    from paper_2206_05466_b200.integrator import zgemm
+
+    rng = np.random.default_rng(n + 1)
+    x = zo.random_admissible(n, rng, 1.0 / n)
+    p = zo.random_admissible(n, rng, 1.0 / n)
+    dev = torch.device("cuda:0")
+    ad, bd = torch.from_numpy(p).to(dev), torch.from_numpy(x).to(dev)
+    c = _oz(lib, ad, bd)
+    native = zgemm(ad, bd).cpu().numpy()
+    rows = np.sort(rng.choice(n, 16, replace=False))
+    ref = (p[rows].astype(np.clongdouble) @ x.astype(np.clongdouble)).astype(np.complex128)
+    e_oz, e_dmma = relf(c[rows], ref), relf(native[rows], ref)
+    print(f"N={n}: oz relF {e_oz:.2e}, native DMMA {e_dmma:.2e} (16 rows)")
+    assert e_oz <= 4e-16
+    assert e_oz <= e_dmma * 1.05
+
+
 def test_zero_and_scaled_inputs(lib):
     """Zero rows/columns (shift 0) stay exact zeros; the power-of-two scaling
     makes the product equivariant to 2^k rescaling of either operand."""
