@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(SOLVE_WARPS * 32, FINAL ? SOLVE_MINB_FIN : SOL
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* sm = reinterpret_cast<double2*>(smem_raw) + warp * SR * DPW;
+  pdl_wait();  // W from the previous kernel (update pass) / the carries
   const double* w = A.w + (size_t)b * A.sw * 2;
   double* p = A.p + (size_t)b * A.sp * 2;
   if ((int)blockIdx.x < gblocks) {
@@ -678,6 +679,7 @@ __global__ void __launch_bounds__(MAXT) k_solve_carry(int n, int C, const double
                                                       double2* m0mg) {
   __shared__ AffW agg[32][32];
   __shared__ double2 red[32];
+  pdl_wait();  // the pass-1 aggregates
   const int SEG = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, wseg = threadIdx.x >> 5;
   const int m = blockIdx.x * 32 + lane;
@@ -1102,24 +1104,22 @@ static int stream_solve_one(zt_operator* op, const double* w, int64_t ldw, int64
   const int td = (A.ntiles + SOLVE_WARPS - 1) / SOLVE_WARPS;
   // one launch per tile pass: boundary tiles first (dispatched first, their
   // latency hides under the interior tiles), then the interior tiles
+  // programmatic dependent launches: each pass's blocks are scheduled under
+  // its predecessor's tail and wait (griddepcontrol.wait) before reading
   auto pass = [&](bool fin) -> int {
     const dim3 grid(tg + td, batch);
-    if (fin)
-      k_solve_merged<true><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
-    else
-      k_solve_merged<false><<<grid, SOLVE_WARPS * 32, smem, st>>>(A, op->gen_tiles, op->ngen, tg);
+    ZT_CUDA_CHECK(launch_pdl(fin ? k_solve_merged<true> : k_solve_merged<false>, grid, dim3(SOLVE_WARPS * 32),
+                             smem, st, A, (const int2*)op->gen_tiles, op->ngen, tg));
     ZT_LAUNCHED();
     return ZT_OK;
   };
   int rc = pass(false);
   if (rc) return rc;
   const int seg = std::max(8, (C + CE - 1) / CE);  // chunk segments per carry block
-  if (seg <= 16)
-    k_solve_carry<512><<<dim3((n + 31) / 32, batch), 32 * seg, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x,
-                                                                       A.yend, A.xst, A.m0acc, A.m0mg);
-  else  // N > 8192: 32 segments, register-limited
-    k_solve_carry<1024><<<dim3((n + 31) / 32, batch), 32 * seg, 0, st>>>(n, C, op->G, op->H, op->K, op->m0x,
-                                                                        A.yend, A.xst, A.m0acc, A.m0mg);
+  ZT_CUDA_CHECK(launch_pdl(seg <= 16 ? k_solve_carry<512> : k_solve_carry<1024>,  // N > 8192: 32 segments
+                           dim3((n + 31) / 32, batch), dim3(32 * seg), 0, st, n, C, (const double*)op->G,
+                           (const double*)op->H, (const double*)op->K, (const double*)op->m0x, A.yend, A.xst,
+                           (const double2*)A.m0acc, A.m0mg));
   ZT_LAUNCHED();
   rc = pass(true);
   if (rc) return rc;
