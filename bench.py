@@ -306,7 +306,7 @@ def run_sharded(args):
         try:
             from paper_2206_05466_b200.sharded import PeerShardedStepper
 
-            st = PeerShardedStepper(n, be)
+            st = PeerShardedStepper(n, be, graph=args.graph)
         except Exception as exc:  # no symmetric memory / peer access on this box
             print(f"[bench] p2p transport unavailable ({exc!r}); using NCCL collectives", file=sys.stderr)
             transport = "nccl"
@@ -381,7 +381,7 @@ def run_sharded(args):
             "workload": f"cfg5: midpoint step N={n}, h={h}", "N": n, "h": h, "tol": TOL, "max_iter": MAX_ITER,
             "init": f"W0 = lap^-1(random_admissible({n}, default_rng(0), 1/{n})) / ||.||_F",
             "iterations_per_step": sorted(set(iters))},
-        "implementation": {"parallelism": f"rowblock{world}", "transport": transport,
+        "implementation": {"parallelism": f"rowblock{world}", "transport": transport, "graph": bool(getattr(st, "graph", False)),
                    "collectives": ("all-gather of X and all-to-all of a fused into the GEMM epilogues as NVLink "
                                    "peer stores (torch symmetric memory), rank barrier + NCCL all_reduce(max "
                                    "residual) per update") if transport == "p2p" else
@@ -726,6 +726,9 @@ def main():
     ap.add_argument("--transport", choices=("p2p", "nccl"), default="p2p",
                     help="sharded step: collectives fused into the GEMM epilogues as peer-memory stores "
                          "(p2p, torch symmetric memory) or NCCL all-gather / all-to-all (nccl)")
+    ap.add_argument("--graph", action="store_true",
+                    help="sharded p2p step as one device-driven CUDA graph per step (fixed point as a "
+                         "conditional WHILE node, residual all-reduce by peer stores)")
     ap.add_argument("--replicas", action="store_true",
                     help="with WORLD_SIZE > 1: independent replicas per rank instead of sharding")
     ap.add_argument("--n", type=int, default=N, help="matrix size for --sharded (cfg 5: 4096, 8192)")

@@ -246,6 +246,41 @@ int zt_update_rows_ew(int m, int n, const double* a_rows, const double* acol, in
                       const double* base, const double* xprev, double* out, int64_t ld, double hh, double qq,
                       unsigned long long* resid, const unsigned long long* peers, int npeer, int r0, void* stream);
 
+/* Device-driven fixed point for callers that enqueue their own update (the
+ * sharded step, sharded.py): a CUDA graph captured from `stream` whose
+ * fixed-point loop is a conditional WHILE node (the single-GPU step's
+ * scheme, integrator.py:125-138), so a step is one graph launch with no host
+ * round trip per update.
+ *   zt_loop_graph_begin      begin capturing `stream` (the prologue); the
+ *                            loop condition starts at 1
+ *   zt_loop_graph_gate       the input gate (laplacian.py:107-116) on the
+ *                            two residuals at val[0..1] (zt_residuals
+ *                            output): a rejected W_n runs no update
+ *   zt_loop_graph_body_begin append the WHILE node and capture `body` into
+ *                            its body graph (the update goes here)
+ *   zt_loop_graph_decide     in the body: r = max of `nslots` residual bit
+ *                            patterns (one per rank, NaN above every
+ *                            number), mail[2] += 1, mail[3] = r; continue
+ *                            while !(r <= tol) and mail[2] < max_iter
+ *   zt_loop_graph_body_end   end the body capture
+ *   zt_loop_graph_end        end the capture and instantiate
+ *   zt_loop_graph_launch / zt_loop_graph_destroy
+ *   zt_peer_put_u64          *src into dst_ptrs[h][index] for every rank h
+ *                            (dst_ptrs: device array of peer pointers),
+ *                            then a system-scope fence */
+typedef struct zt_loop_graph* zt_loop_graph_t;
+int zt_loop_graph_begin(void* stream, zt_loop_graph_t* out);
+int zt_loop_graph_gate(zt_loop_graph_t g, const double* val, void* stream);
+int zt_loop_graph_body_begin(zt_loop_graph_t g, void* stream, void* body);
+int zt_loop_graph_decide(zt_loop_graph_t g, const unsigned long long* slots, int nslots, unsigned long long* mail,
+                         double tol, int max_iter, void* body);
+int zt_loop_graph_body_end(zt_loop_graph_t g, void* body);
+int zt_loop_graph_end(zt_loop_graph_t g, void* stream);
+int zt_loop_graph_launch(zt_loop_graph_t g, void* stream);
+int zt_loop_graph_destroy(zt_loop_graph_t g);
+int zt_peer_put_u64(const unsigned long long* src, const unsigned long long* dst_ptrs, int index, int npeer,
+                    void* stream);
+
 /* Quantized spherical-harmonic basis (basis.py).
  * Vectors for orders m0 <= m < m1 are stored like the reference's
  * QuantizedBasis.vectors[m]: row-major (N - m) x n_l(m) doubles,

@@ -82,6 +82,15 @@ SIGNATURES = {
     ),
     "zt_launch_count": (_c_i64, []),
     "zt_set_graph": (_c_int, [_c_int]),
+    "zt_loop_graph_begin": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "zt_loop_graph_gate": (_c_int, [_vp, _vp, _vp]),
+    "zt_loop_graph_body_begin": (_c_int, [_vp, _vp, _vp]),
+    "zt_loop_graph_decide": (_c_int, [_vp, _vp, _c_int, _vp, _c_dbl, _c_int, _vp]),
+    "zt_loop_graph_body_end": (_c_int, [_vp, _vp]),
+    "zt_loop_graph_end": (_c_int, [_vp, _vp]),
+    "zt_loop_graph_launch": (_c_int, [_vp, _vp]),
+    "zt_loop_graph_destroy": (_c_int, [_vp]),
+    "zt_peer_put_u64": (_c_int, [_vp, _vp, _c_int, _c_int, _vp]),
     "zt_step_algo": (_c_int, []),
     "zt_profile_enable": (_c_int, [_c_int]),
     "zt_profile_read": (_c_int, [_vp, _vp, _c_int]),

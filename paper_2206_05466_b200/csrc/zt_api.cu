@@ -695,6 +695,126 @@ int64_t zt_launch_count(void) { return g_launches.load(); }
 
 int zt_set_graph(int on) { return g_graph.exchange(on != 0) ? 1 : 0; }
 
+// ---- device-driven fixed point for caller-enqueued updates (sharded step) ---
+}  // extern "C"
+struct zt_loop_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+};
+namespace zt {
+__global__ void k_loop_decide(const unsigned long long* slots, int nslots, unsigned long long* mail, double tol,
+                              int max_iter, cudaGraphConditionalHandle h) {
+  unsigned long long bits = 0;
+  for (int g = 0; g < nslots; ++g) bits = max(bits, ((const volatile unsigned long long*)slots)[g]);
+  double r;
+  memcpy(&r, &bits, sizeof r);
+  const unsigned long long k = ++mail[2];
+  mail[3] = bits;
+  cudaGraphSetConditional(h, (!(r <= tol) && (long long)k < (long long)max_iter) ? 1u : 0u);
+}
+__global__ void k_peer_put_u64(const unsigned long long* src, const unsigned long long* dst, int index, int npeer) {
+  const int h = threadIdx.x;
+  if (h < npeer) reinterpret_cast<volatile unsigned long long*>(dst[h])[index] = *src;
+  __threadfence_system();
+}
+}  // namespace zt
+extern "C" {
+
+int zt_loop_graph_begin(void* stream, zt_loop_graph_t* out) {
+  if (!out) return fail(ZT_EINVAL, "zt_loop_graph_begin: null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  zt_loop_graph* g = new zt_loop_graph;
+  cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  cudaStreamCaptureStatus stt;
+  cudaGraph_t cg = nullptr;
+  if (!e) e = cudaStreamGetCaptureInfo(st, &stt, nullptr, &cg, nullptr, nullptr);
+  if (!e) e = cudaGraphConditionalHandleCreate(&g->cond, cg, 1, cudaGraphCondAssignDefault);
+  if (e) {
+    delete g;
+    return cuda_fail(e, "zt_loop_graph_begin");
+  }
+  *out = g;
+  return ZT_OK;
+}
+
+int zt_loop_graph_gate(zt_loop_graph_t g, const double* val, void* stream) {
+  if (!g || !val) return fail(ZT_EINVAL, "zt_loop_graph_gate: bad argument");
+  k_gate<<<1, 1, 0, (cudaStream_t)stream>>>(val, g->cond);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+int zt_loop_graph_body_begin(zt_loop_graph_t g, void* stream, void* body) {
+  if (!g) return fail(ZT_EINVAL, "zt_loop_graph_body_begin: null graph");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaStreamCaptureStatus stt;
+  cudaGraph_t cg;
+  const cudaGraphNode_t* deps;
+  size_t nd;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &stt, nullptr, &cg, &deps, &nd);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = g->cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (!e) e = cudaGraphAddNode(&node, cg, deps, nd, &cp);
+  if (!e) e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
+  if (!e)
+    e = cudaStreamBeginCaptureToGraph((cudaStream_t)body, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+  if (e) return cuda_fail(e, "zt_loop_graph_body_begin");
+  return ZT_OK;
+}
+
+int zt_loop_graph_decide(zt_loop_graph_t g, const unsigned long long* slots, int nslots, unsigned long long* mail,
+                         double tol, int max_iter, void* body) {
+  if (!g || !slots || !mail || nslots < 1) return fail(ZT_EINVAL, "zt_loop_graph_decide: bad argument");
+  k_loop_decide<<<1, 1, 0, (cudaStream_t)body>>>(slots, nslots, mail, tol, max_iter, g->cond);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
+int zt_loop_graph_body_end(zt_loop_graph_t g, void* body) {
+  if (!g) return fail(ZT_EINVAL, "zt_loop_graph_body_end: null graph");
+  cudaGraph_t bg;
+  ZT_CUDA_CHECK(cudaStreamEndCapture((cudaStream_t)body, &bg));
+  return ZT_OK;
+}
+
+int zt_loop_graph_end(zt_loop_graph_t g, void* stream) {
+  if (!g) return fail(ZT_EINVAL, "zt_loop_graph_end: null graph");
+  ZT_CUDA_CHECK(cudaStreamEndCapture((cudaStream_t)stream, &g->graph));
+  ZT_CUDA_CHECK(cudaGraphInstantiate(&g->exec, g->graph, 0));
+  return ZT_OK;
+}
+
+int zt_loop_graph_launch(zt_loop_graph_t g, void* stream) {
+  if (!g || !g->exec) return fail(ZT_EINVAL, "zt_loop_graph_launch: graph not built");
+  ZT_CUDA_CHECK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+  return ZT_OK;
+}
+
+int zt_loop_graph_destroy(zt_loop_graph_t g) {
+  if (!g) return ZT_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return ZT_OK;
+}
+
+int zt_peer_put_u64(const unsigned long long* src, const unsigned long long* dst_ptrs, int index, int npeer,
+                    void* stream) {
+  if (!src || !dst_ptrs || npeer < 1 || npeer > 1024 || index < 0) return fail(ZT_EINVAL, "zt_peer_put_u64: bad argument");
+  k_peer_put_u64<<<1, npeer, 0, (cudaStream_t)stream>>>(src, dst_ptrs, index, npeer);
+  ZT_LAUNCHED();
+  ZT_CUDA_CHECK(cudaGetLastError());
+  return ZT_OK;
+}
+
 int zt_step_algo(void) { return g_algo; }
 
 int zt_profile_enable(int on) {

@@ -76,30 +76,80 @@ def test_virtual_ranks_errors_and_nonconvergence():
     assert e.value.iterations == 1 and e.value.residual > 1e-14
 
 
-def test_symmetric_memory_path_one_rank():
+def _one_rank_group(dev):
     import os
     import socket
 
     import torch.distributed as dist
 
-    from paper_2206_05466_b200.integrator import midpoint_step_raw
-    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper
-
-    dev = torch.device("cuda:0")
     if not dist.is_initialized():
         s = socket.socket()
         s.bind(("127.0.0.1", 0))
         os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
         s.close()
         dist.init_process_group("nccl", device_id=dev)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_symmetric_memory_path_one_rank(graph):
+    """One-rank NCCL group with torch symmetric memory: the eager peer path
+    and the device-driven graph path (fixed point as a conditional WHILE
+    node, residual exchanged by peer stores, input gate in the graph) over
+    two consecutive steps (the second replays the captured graph)."""
+    import torch.distributed as dist
+
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper
+
+    dev = torch.device("cuda:0")
+    _one_rank_group(dev)
     try:
         n = 256
         be = DeviceBackend(n, dev)
-        st = PeerShardedStepper(n, be)
+        st = PeerShardedStepper(n, be, graph=graph)
+        assert st.graph == graph
         w = torch.from_numpy(zo.smooth_initial(n)).to(dev)
-        out, k, _ = st.midpoint_step(w.clone(), 0.005)
-        ref, kr, _, _ = midpoint_step_raw(w, 0.005, 1e-12, 10, be.op)
-        assert k == kr and relf(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+        ref = w
+        cur = w.clone()
+        for _ in range(2):
+            cur, k, _ = st.midpoint_step(cur, 0.005)
+            ref, kr, _, _ = midpoint_step_raw(ref, 0.005, 1e-12, 10, be.op)
+            assert k == kr and relf(cur.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+    finally:
+        dist.destroy_process_group()
+
+
+def test_graph_path_matches_eager_and_raises():
+    """The graph path is bitwise the eager peer path; a non-skew input raises
+    StructureError from the in-graph gate and a capped fixed point raises
+    FixedPointError with the iteration count, as the reference does."""
+    import torch.distributed as dist
+
+    from paper_2206_05466_b200.integrator import FixedPointError
+    from paper_2206_05466_b200.laplacian import StructureError
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper
+
+    dev = torch.device("cuda:0")
+    _one_rank_group(dev)
+    try:
+        n = 256
+        be = DeviceBackend(n, dev)
+        ge, gg = PeerShardedStepper(n, be, graph=False), PeerShardedStepper(n, be, graph=True)
+        w = torch.from_numpy(zo.random_admissible(n, np.random.default_rng(3), 1.0 / n)).to(dev)
+        oe, ke, re = ge.midpoint_step(w.clone(), 0.01)
+        og, kg, rg = gg.midpoint_step(w.clone(), 0.01)
+        assert ke == kg and re == rg and torch.equal(oe, og)
+        bad = w.clone()
+        bad[0, 1] += 1.0
+        with pytest.raises(StructureError, match="skew-Hermitian"):
+            gg.midpoint_step(bad, 0.01)
+        big = torch.from_numpy(zo.random_admissible(n, np.random.default_rng(1), 1.0)).to(dev)
+        with pytest.raises(FixedPointError) as e:
+            gg.midpoint_step(big, 0.5, max_iter=1)
+        assert e.value.iterations == 1 and e.value.residual > 1e-14
+        # the graph path still steps correctly after the errors
+        og2, kg2, _ = gg.midpoint_step(w.clone(), 0.01)
+        assert kg2 == ke and torch.equal(og2, oe)
     finally:
         dist.destroy_process_group()
 

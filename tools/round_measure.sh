@@ -13,3 +13,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_oz
   -o $O/final_oz_gemm python tools/oz_prof.py 2048 > /dev/null 2>&1
 timeout 300 python tools/oz_zgemm_check.py > $O/final_oz_accuracy.txt 2>&1
 timeout 900 python tools/cfg4_full.py > $O/final_cfg4_full.json 2>&1
+timeout 600 python tools/bench_ops.py > $O/final_bench_ops.jsonl 2> $O/final_bench_ops.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_solve_merged -c 2 \
+  -o $O/final_solve python tools/solve_once.py 4096 1 > /dev/null 2>&1
