@@ -1078,7 +1078,11 @@ __global__ void __launch_bounds__(256) k_update_rows_ew(int m, int n, const doub
       rmax = nanmax(rmax, hypot(nw.x - xp.x, nw.y - xp.y));
     }
     st2(out + o, nw);
-    for (int h = 0; h < npeer; ++h) st2(reinterpret_cast<double*>(peers[h]) + ((size_t)(r0 + i) * n + j) * 2, nw);
+    for (int h = 0; h < npeer; ++h) {
+      // (out may be this rank's own rows of the gathered iterate: no second store)
+      double* dst = reinterpret_cast<double*>(peers[h]) + ((size_t)(r0 + i) * n + j) * 2;
+      if (dst != out + o) st2(dst, nw);
+    }
   }
   if (npeer) {  // one system-scope fence per block (cumulative over the block's stores)
     __syncthreads();

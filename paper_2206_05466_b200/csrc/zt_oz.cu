@@ -831,11 +831,12 @@ __global__ void __launch_bounds__(256, 4) k_oz_recon_ex(int m, int n, const int8
       const int j = j0 + e;
       if (j >= n) continue;
       const double2 o = scaled(vr[e], vi[e], ri, cs[j]);
-      if (c) st2(c + ((size_t)i * ldc + j) * 2, o);
+      double* cc = c ? c + ((size_t)i * ldc + j) * 2 : nullptr;
+      if (c) st2(cc, o);
       if (peers) {
         const int h = j / mloc;
-        double* dst = reinterpret_cast<double*>(peers[h]);
-        st2(dst + ((size_t)(r0 + i) * mloc + (j - h * mloc)) * 2, o);
+        double* dst = reinterpret_cast<double*>(peers[h]) + ((size_t)(r0 + i) * mloc + (j - h * mloc)) * 2;
+        if (dst != cc) st2(dst, o);  // one rank: the scatter target may be c itself
       }
       if (mirror_blk) tl[wr][lane * OZ_RECON_COLS + e] = make_double2(-o.x, o.y);
     }

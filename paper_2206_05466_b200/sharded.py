@@ -331,16 +331,23 @@ class PeerRank:
         return pool[:k]
 
     def phase2b(self, base_rows, xprev_rows, hh: float, qq: float, with_b: bool = True):
-        """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, broadcast to every rank
-        (with_b=False: no b term, the final update W_n + h (a - a^H))."""
+        """X_R' = base + hh (a_R - (a^H)_R) + qq b_R, written in place over
+        this rank's rows of its gathered iterate (the residual is taken
+        against the old rows by the same thread) and broadcast to every other
+        rank.  with_b=False: the final update W_n + h (a - a^H) into a new
+        tensor, no broadcast (the next step seeds the iterate afresh)."""
         lib = self.be._lib
-        out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
+        if with_b:
+            out, peers, npeer = self.xfull[self.r0:self.r0 + self.m], self.xptrs.data_ptr(), self.world
+        else:
+            out = torch.empty((self.m, self.n), dtype=torch.complex128, device=self.be.device)
+            peers, npeer = None, 0
         self._flag.zero_()
         lib.check(lib.lib.zt_update_rows_ew(
             self.m, self.n, self.a_rows.data_ptr(), self.acol.data_ptr(), self.m,
             self.brows.data_ptr() if with_b else None,
             base_rows.data_ptr(), xprev_rows.data_ptr() if xprev_rows is not None else None, out.data_ptr(),
-            self.n, hh, qq, self._flag.data_ptr(), self.xptrs.data_ptr(), self.world, self.r0, self._s()))
+            self.n, hh, qq, self._flag.data_ptr(), peers, npeer, self.r0, self._s()))
         # the residual stays on the device as the bit pattern of a
         # non-negative double (NaN above every number): max over ranks is an
         # integer max, and the host reads it once per update after the reduction
@@ -435,7 +442,10 @@ class OzPeerRank(PeerRank):
         self.pa, self.sp, self.pb = self._convert_rows(("p",), m, self.p[self.r0:].data_ptr(), 2, self.r0, s,
                                                        key2=("pb",))
         main.wait_event(join)
-        if getattr(self, "persistent", False):
+        if self.world == 1:
+            # one rank: a[:, R] is all of a, laid out as a_R -- one buffer
+            self.a_rows = self.acol
+        elif getattr(self, "persistent", False):
             self.a_rows = self._buf("arows", 16 * m * n, torch.complex128).view(m, n)
         else:
             self.a_rows = torch.empty((m, n), dtype=torch.complex128, device=self.be.device)
