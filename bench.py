@@ -619,7 +619,7 @@ def run_ours(args):
                         "compiled out (TMA loads only) moves the 2.28 GB at 13.3 TB/s in 171.7 us at N = 2048 "
                         "(MMAs alone 142.5 us, both 182 us); profiles/r02_ncu_summary.md",
             },
-            "accuracy": "relF vs extended precision <= 4e-16 at N = 5-256 (native FP64 DMMA 5.5e-16-1.1e-15); "
+            "accuracy": "relF vs extended precision 3.7e-17-3.9e-16 at N = 130-512 and 7.4e-17 at N = 2048 / 4096 (native FP64 DMMA 5.5e-16-1.1e-15 / 2-3e-15); "
                         "per-row/column bound tests/test_oz_gpu.py",
         }
         roofline.update(common)
@@ -655,7 +655,7 @@ def run_ours(args):
     impl = {
         "parallelism": "replicas" if world > 1 else "single",
         "gemm": ("FP64-accurate complex products on the INT8 tensor cores: Ozaki scheme II with a Gaussian-integer "
-                 "split (operands scaled to 53-bit integers, 17 odd coprime moduli <= 241 with sqrt(-1), two real "
+                 "split (operands scaled to 55-bit integers (54 for K > 4096), 17 odd coprime moduli <= 241 with sqrt(-1), two real "
                  "tcgen05 kind::i8 residue GEMMs per modulus, exact CRT reconstruction); ZT_GEMM_ALGO=3m selects "
                  "the native FP64 DMMA path") if oz else
                 "3M DMMA (sm_100a mma.sync m8n8k4 f64), TMA 128B-swizzled stages, persistent fused update",
