@@ -64,12 +64,29 @@ namespace oz {
 // epilogue keeps U's residues in registers (32 words per thread) and, when V
 // lands, stores (U + V) and (U - V) mod p.
 // ---------------------------------------------------------------------------
+#ifndef OZ_SW128
+#define OZ_SW128 1
+#endif
+#ifndef OZ_KPS
+#define OZ_KPS 1
+#endif
+#ifndef OZ_STAGES
+#define OZ_STAGES 6
+#endif
+#if OZ_SW128
+// 128 B K blocks under the 128 B swizzle: one TMA box of 128 rows x 128 B per
+// operand per stage (64 B blocks / 64 B swizzle: 213 -> 199.5 us per full
+// product at N = 2048, 1545 -> 1441 us at N = 4096)
+constexpr int TM = 256, TN = 256, TK = 128;  // pair tile; TK in bytes
+constexpr int KPS = OZ_KPS;                  // K blocks per pipeline stage
+#else
 constexpr int TM = 256, TN = 256, TK = 64;  // pair tile; TK in bytes (64 B swizzle)
+constexpr int KPS = 2;                     // K blocks per pipeline stage
+#endif
 constexpr int A_BYTES = 128 * TK;          // one CTA's 128 rows of an A plane
 constexpr int B_BYTES = (TN / 2) * TK;     // one CTA's 128 columns of a B plane
-constexpr int KPS = 2;                     // K blocks per pipeline stage
 constexpr int STAGE_BYTES = KPS * (A_BYTES + B_BYTES);
-constexpr int STAGES = 6;
+constexpr int STAGES = OZ_STAGES;
 constexpr int EPI_WARPS = 16;             // 4 per TMEM lane quarter, 64 columns each
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
@@ -77,10 +94,11 @@ constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
                            ((uint32_t)(TM >> 4) << 24);
 
-// UMMA smem descriptor: K-major, 64 B swizzle, 8-row groups 512 B apart
+// UMMA smem descriptor: K-major, TK-byte swizzle (64 B: layout 4; 128 B:
+// layout 2), 8-row groups 8 TK bytes apart
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)((8 * TK) >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)(TK == 128 ? 2 : 4) << 61);
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
@@ -445,7 +463,8 @@ static int map_i8(CUtensorMap* m, const void* base, long long rows, int cols, in
   cuuint32_t box[2] = {TK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, TK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(ZT_ECUDA, "oz: tensor map encode failed");
   return ZT_OK;
