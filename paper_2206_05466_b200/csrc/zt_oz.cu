@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cmath>
 #include <type_traits>
+#include <type_traits>
 #include <vector>
 
 #include "zt_common.cuh"
@@ -750,11 +751,12 @@ __device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bi
 constexpr int OZ_RECON_COLS = 2;
 // the centred integers Re, Im of product entries (i, j0 .. j0 + C - 1)
 // before scaling
+template <int C = OZ_RECON_COLS>
 __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp, int np, int i, int j0, double* vr,
                                            double* vi, const CrtConst& cc = c_crt) {
   const size_t ps = (size_t)2 * mp * np;  // stride between moduli
-  constexpr int C = OZ_RECON_COLS;
-  using word_t = unsigned short;
+  static_assert(C == 2 || C == 4, "2 or 4 columns per thread");
+  using word_t = typename std::conditional<C == 2, unsigned short, unsigned int>::type;
   const int8_t* rre = r + (size_t)i * np + j0;
   const int8_t* rim = rre + (size_t)mp * np;
   word_t wr[OZ_NMOD], wi[OZ_NMOD];
@@ -797,20 +799,31 @@ __device__ __forceinline__ double2 scaled(double vr, double vi, int ri, int cj) 
   return make_double2(ldexp(vr, sh), ldexp(vi, sh));
 }
 
-__global__ void __launch_bounds__(256, 4) k_oz_recon(int m, int n, const int8_t* __restrict__ r, int mp, int np,
-                                                   const int* __restrict__ rs, const int* __restrict__ cs, double* c,
-                                                   int64_t ldc, int lower) {
+#ifndef OZ_RC
+#define OZ_RC 4
+#endif
+#ifndef OZ_RC_MINB
+#define OZ_RC_MINB 3
+#endif
+// 4 output columns per thread (one 32-bit residue load per plane, the CRT
+// constants and address increments shared by 4 values) at <= 80 registers:
+// 60.9 -> 57.7 us at N = 2048 against 2 columns at <= 64 registers
+constexpr int RC = OZ_RC;
+__global__ void __launch_bounds__(256, OZ_RC_MINB) k_oz_recon(int m, int n, const int8_t* __restrict__ r, int mp,
+                                                            int np, const int* __restrict__ rs,
+                                                            const int* __restrict__ cs, double* c, int64_t ldc,
+                                                            int lower) {
   const int i = blockIdx.y;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * OZ_RECON_COLS;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * RC;
   pdl_trigger();
   pdl_wait();
   if (i >= m || j0 >= n) return;
   if (lower && (j0 >> 7) > (i >> 7)) return;
-  double vr[OZ_RECON_COLS], vi[OZ_RECON_COLS];
-  crt_values(r, mp, np, i, j0, vr, vi);
+  double vr[RC], vi[RC];
+  crt_values<RC>(r, mp, np, i, j0, vr, vi);
   const int ri = rs[i];
 #pragma unroll
-  for (int e = 0; e < OZ_RECON_COLS; ++e) {
+  for (int e = 0; e < RC; ++e) {
     const int j = j0 + e;
     if (j < n && !(lower && (j >> 7) > (i >> 7))) st2(c + ((size_t)i * ldc + j) * 2, scaled(vr[e], vi[e], ri, cs[j]));
   }
@@ -877,7 +890,7 @@ __global__ void __launch_bounds__(256, 4) k_oz_recon_ex(int m, int n, const int8
 
 static cudaError_t launch_recon(int m, int n, const int8_t* r, int mp, int np, const int* rs, const int* cs, double* c,
                                 int64_t ldc, int lower, cudaStream_t st) {
-  const dim3 grid((n + 256 * OZ_RECON_COLS - 1) / (256 * OZ_RECON_COLS), m);
+  const dim3 grid((n + 256 * RC - 1) / (256 * RC), m);
   return launch_pdl(k_oz_recon, grid, dim3(256), 0, st, m, n, r, mp, np, rs, cs, c, ldc, lower);
 }
 
