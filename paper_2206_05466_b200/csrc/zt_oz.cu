@@ -562,8 +562,15 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
                                                        int mp, int kp, int kb, int mode, int diag0, int8_t* out,
                                                        int* __restrict__ shift, int8_t* out2 = nullptr) {
   const int i = blockIdx.x;  // row of the (rows x n) block; its diagonal entry is column diag0 + i
-  __shared__ double red[8];
-  double amax = 0.0;
+  __shared__ unsigned red[8];
+  __shared__ double redd[8];
+  // The shift needs only ilogb of the row maximum (or that it is not
+  // finite): the maximum of the high words of |x| (sign cleared) has the
+  // exponent and leading mantissa bits of the maximum, and >= 0x7ff00000
+  // exactly when an Inf or NaN is present -- one integer max per value
+  // instead of the NaN-propagating double max.  A row whose largest high
+  // word is 0 (all |x| < 2^-1042) takes the exact double maximum.
+  unsigned hmax = 0;
   pdl_trigger();
   pdl_wait();
   if (i < rows) {
@@ -575,18 +582,36 @@ __global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const 
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = ld2(src + ((size_t)i * ld + k + u * 256) * 2);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) amax = nanmax(amax, nanmax(fabs(v[u].x), fabs(v[u].y)));
+      for (int u = 0; u < 8; ++u)
+        hmax = max(hmax, max((unsigned)__double2hiint(v[u].x) & 0x7fffffffu,
+                             (unsigned)__double2hiint(v[u].y) & 0x7fffffffu));
     }
     for (; k < n; k += 256) {
       const double2 v = ld2(src + ((size_t)i * ld + k) * 2);
-      amax = nanmax(amax, nanmax(fabs(v.x), fabs(v.y)));
+      hmax = max(hmax, max((unsigned)__double2hiint(v.x) & 0x7fffffffu, (unsigned)__double2hiint(v.y) & 0x7fffffffu));
     }
   }
-  for (int o = 16; o; o >>= 1) amax = nanmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+  for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hmax;
   __syncthreads();
-  amax = red[0];
-  for (int q = 1; q < 8; ++q) amax = nanmax(amax, red[q]);
+  hmax = red[0];
+  for (int q = 1; q < 8; ++q) hmax = max(hmax, red[q]);
+  double amax = __hiloint2double((int)hmax, 0);
+  if (hmax == 0) {  // block-uniform: tiny or zero row, exact maximum
+    amax = 0.0;
+    if (i < rows)
+      for (int k = threadIdx.x; k < n; k += 256) {
+        const double2 v = ld2(src + ((size_t)i * ld + k) * 2);
+        amax = nanmax(amax, nanmax(fabs(v.x), fabs(v.y)));
+      }
+    for (int o = 16; o; o >>= 1) amax = nanmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0) redd[threadIdx.x >> 5] = amax;
+    __syncthreads();
+    amax = redd[0];
+    for (int q = 1; q < 8; ++q) amax = nanmax(amax, redd[q]);
+  } else if (hmax >= 0x7ff00000u) {
+    amax = __longlong_as_double(0x7ff8000000000000LL);  // an Inf or NaN in the row
+  }
   const int sh = oz_shift(amax, kb);
   const double2 sc = oz_scale2(sh);
   if (threadIdx.x == 0 && shift) shift[i] = sh;
