@@ -613,11 +613,12 @@ def run_ours(args):
                 # planes x (256 A rows + 256 B rows) per 256 x 256 pair tile x K
                 "bytes_per_launch": OZ_L2_BYTES(pd, nmod),
                 "TBps": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12,
-                "ceiling_TBps": OZ_L2_CEILING_TBPS,
-                "frac": OZ_L2_BYTES(pd, nmod) / (full_ms * 1e-3) / 1e12 / OZ_L2_CEILING_TBPS,
-                "note": "the kernel's operand-supply floor: the same kernel with its MMAs and epilogue "
-                        "compiled out (TMA loads only) moves the 2.28 GB at 13.3 TB/s in 171.7 us at N = 2048 "
-                        "(MMAs alone 142.5 us, both 182 us); profiles/r02_ncu_summary.md",
+                "floors_us_n2048": OZ_FLOORS_US,
+                "frac_of_mainloop_floor": (OZ_FLOORS_US["tma_and_mma"] * 1e-3 / full_ms) if pd == 2048 else None,
+                "note": "floors of the same kernel in timing-only builds at N = 2048: TMA loads alone (2.28 GB at "
+                        "21.9 TB/s), MMAs alone, both (the tensor cores' shared-memory operand path, ncu "
+                        "sm__mem_tensor_cycles_active 93%); the rest of the launch is the epilogue's V-part "
+                        "work and residue stores; profiles/r02_ncu_summary.md",
             },
             "accuracy": "relF vs extended precision 3.7e-17-3.9e-16 at N = 130-512 and 7.4e-17 at N = 2048 / 4096 (native FP64 DMMA 5.5e-16-1.1e-15 / 2-3e-15); "
                         "per-row/column bound tests/test_oz_gpu.py",
@@ -700,15 +701,15 @@ def run_ours(args):
 
 # ncu --set full dram bytes per launch (profiles/): the residue GEMM and the
 # DMMA path's fused update
-TRAFFIC_OZ = (285.3 + 118.0) * 1e6
+TRAFFIC_OZ = (285.3 + 117.4) * 1e6
 TRAFFIC_OZ_SRC = "ncu --set full, one 17-modulus k_oz_gemm at N = 2048, profiles/r02_ncu_summary.md (not measured in this run)"
 def OZ_L2_BYTES(pd, nmod):
     return float(nmod * 2 * (pd // 256) ** 2 * pd * 512)
 
 
-# measured: the residue GEMM with MMAs and epilogue compiled out (TMA loads
-# only), N = 2048, 2.28 GB in 171.7 us (profiles/r02_ncu_summary.md)
-OZ_L2_CEILING_TBPS = 13.3
+# measured floors of the residue GEMM (128 B K blocks) at N = 2048, timing-only
+# builds (profiles/r02_ncu_summary.md)
+OZ_FLOORS_US = {"tma_only": 104.0, "mma_only": 142.3, "tma_and_mma": 176.0, "no_residue_stores": 186.0}
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
 
 
