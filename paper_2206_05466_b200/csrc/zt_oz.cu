@@ -763,14 +763,33 @@ struct CrtConst {
   double mp[OZ_NPC];           // pieces of M
   double m_inv;                // 1 / M
   double bias[OZ_NMOD];        // 2^52 + 2^31 + k_t
+  uint32_t hi80;               // 0x80000000, read at run time (see byte_to_double)
 };
 __constant__ CrtConst c_crt;
 
 // unsigned byte r -> centred residue r - k_t as a double without an
 // int -> fp64 conversion: 2^52 + 2^31 + r as the bit pattern, minus the bias
-__device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bias) {
-  // one byte permute: byte e of word, then 0x00, 0x00, 0x80
-  return __hiloint2double(0x43300000, (int)__byte_perm(word, 0x80000000u, 0x7540u | e)) - bias;
+// `hi80` holds 0x80000000 read from constant memory (opaque to the
+// compiler), so the permute takes its selector as an immediate: with both
+// constants foldable ptxas kept 0x80000000 as the immediate and moved the
+// selector from a uniform register before every permute
+template <int E>
+__device__ __forceinline__ uint32_t prmt_byte(uint32_t word, uint32_t hi80) {
+  uint32_t lo;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(word), "r"(hi80), "n"(0x7540 | E));
+  return lo;
+}
+__device__ __forceinline__ double byte_to_double(uint32_t word, int e, double bias, uint32_t hi80) {
+  // one byte permute: byte e of word, then 0x00, 0x00, 0x80 (e is a
+  // compile-time constant after unrolling: the switch folds away)
+  uint32_t lo;
+  switch (e) {
+    case 0: lo = prmt_byte<0>(word, hi80); break;
+    case 1: lo = prmt_byte<1>(word, hi80); break;
+    case 2: lo = prmt_byte<2>(word, hi80); break;
+    default: lo = prmt_byte<3>(word, hi80); break;
+  }
+  return __hiloint2double(0x43300000, (int)lo) - bias;
 }
 
 // reconstruction: 2 output columns per thread at <= 64 registers (4 blocks
@@ -792,6 +811,7 @@ __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp,
     wr[t] = __ldg(reinterpret_cast<const word_t*>(rre + (size_t)t * ps));
     wi[t] = __ldg(reinterpret_cast<const word_t*>(rim + (size_t)t * ps));
   }
+  const uint32_t hi80 = cc.hi80;
   double s[2 * C][OZ_NPC];
 #pragma unroll
   for (int e = 0; e < 2 * C; ++e)
@@ -802,7 +822,7 @@ __device__ __forceinline__ void crt_values(const int8_t* __restrict__ r, int mp,
     const double bias = cc.bias[t];
 #pragma unroll
     for (int e = 0; e < 2 * C; ++e) {
-      const double u = byte_to_double(e < C ? wr[t] : wi[t], e % C, bias);
+      const double u = byte_to_double(e < C ? wr[t] : wi[t], e % C, bias, hi80);
 #pragma unroll
       for (int k = 0; k < OZ_NPC; ++k) s[e][k] = fma(u, e < C ? cc.wr[t][k] : cc.wi[t][k], s[e][k]);
     }
@@ -975,6 +995,7 @@ static int crt_init() {
     pieces(mt * (u128)(((long long)half * y) % p), h.wr[t]);
     pieces(mt * (u128)(((long long)g2 * y) % p), h.wi[t]);
     h.bias[t] = 4503601774854144.0 + (double)(p / 2);
+    h.hi80 = 0x80000000u;
     pm[t] = p;
     int l = 0;
     while ((1 << l) < p) ++l;
