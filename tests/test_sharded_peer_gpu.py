@@ -120,6 +120,31 @@ def test_symmetric_memory_path_one_rank(graph):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("n", (200, 300))
+def test_graph_path_ragged_sizes(n):
+    """The device-driven graph step at sizes that are not multiples of the
+    256-row residue tiles or of the 64-row solve chunks, replayed over three
+    steps against the single-GPU step."""
+    import torch.distributed as dist
+
+    from paper_2206_05466_b200.integrator import midpoint_step_raw
+    from paper_2206_05466_b200.sharded import DeviceBackend, PeerShardedStepper
+
+    dev = torch.device("cuda:0")
+    _one_rank_group(dev)
+    try:
+        be = DeviceBackend(n, dev)
+        st = PeerShardedStepper(n, be, graph=True)
+        w = torch.from_numpy(zo.random_admissible(n, np.random.default_rng(n), 1.0 / n)).to(dev)
+        ref, cur = w, w.clone()
+        for _ in range(3):
+            cur, k, _ = st.midpoint_step(cur, 0.01)
+            ref, kr, _, _ = midpoint_step_raw(ref, 0.01, 1e-12, 10, be.op)
+            assert k == kr and relf(cur.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+    finally:
+        dist.destroy_process_group()
+
+
 def test_graph_path_matches_eager_and_raises():
     """The graph path is bitwise the eager peer path; a non-skew input raises
     StructureError from the in-graph gate and a capped fixed point raises
