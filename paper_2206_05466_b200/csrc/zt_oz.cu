@@ -556,9 +556,9 @@ __device__ __forceinline__ double2 oz_scale2(int sh) {
 // mode 2: both at once from one read (A planes into out, skew-B planes into
 // out2; the row scale is shared since |-conj(v)| = |v|).  One block per
 // padded row; 4 consecutive k per thread (one 32-bit store per plane).
-// <= 80 registers (3 blocks of 256 per SM)
+// <= 64 registers (4 blocks of 256 per SM; 58.5 -> 57.6 us against 80 registers at 3)
 template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_oz_conv_rows(int rows, int n, const double* __restrict__ src, int64_t ld,
+__global__ void __launch_bounds__(256, 4) k_oz_conv_rows(int rows, int n, const double* __restrict__ src, int64_t ld,
                                                        int mp, int kp, int kb, int mode, int diag0, int8_t* out,
                                                        int* __restrict__ shift, int8_t* out2 = nullptr) {
   const int i = blockIdx.x;  // row of the (rows x n) block; its diagonal entry is column diag0 + i
@@ -850,11 +850,12 @@ __device__ __forceinline__ double2 scaled(double vr, double vi, int ri, int cj) 
 #define OZ_RC 4
 #endif
 #ifndef OZ_RC_MINB
-#define OZ_RC_MINB 3
+#define OZ_RC_MINB 4
 #endif
 // 4 output columns per thread (one 32-bit residue load per plane, the CRT
-// constants and address increments shared by 4 values) at <= 80 registers:
-// 60.9 -> 57.7 us at N = 2048 against 2 columns at <= 64 registers
+// constants and address increments shared by 4 values) at <= 64 registers
+// (4 blocks of 256 per SM): 62.2 -> 53.3 us at N = 2048 with the
+// immediate-selector permutes, against 2 columns per thread
 constexpr int RC = OZ_RC;
 __global__ void __launch_bounds__(256, OZ_RC_MINB) k_oz_recon(int m, int n, const int8_t* __restrict__ r, int mp,
                                                             int np, const int* __restrict__ rs,
