@@ -677,12 +677,25 @@ __global__ void __launch_bounds__(256) k_oz_colmax(int kdim, int n, const double
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int r0 = blockIdx.y * 64 + (threadIdx.x >> 5) * 8;
   if (j >= n) return;
-  double m = 0.0;
-  for (int r = r0; r < min(r0 + 8, kdim); ++r) {
-    const double2 v = ld2(x + ((size_t)r * ld + j) * 2);
-    m = nanmax(m, nanmax(fabs(v.x), fabs(v.y)));
+  // all 8 loads in flight, then the maximum of the high words of |x| (as in
+  // k_oz_conv_rows: the shift needs only ilogb of the maximum or that a value
+  // is not finite); a thread whose high words are all 0 (|x| < 2^-1042)
+  // contributes its exact bit pattern
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = (r0 + q < kdim) ? ld2(x + ((size_t)(r0 + q) * ld + j) * 2) : make_double2(0.0, 0.0);
+  unsigned hm = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    hm = max(hm, max((unsigned)__double2hiint(v[q].x) & 0x7fffffffu, (unsigned)__double2hiint(v[q].y) & 0x7fffffffu));
+  unsigned long long bits = (unsigned long long)hm << 32;
+  if (hm == 0) {
+    double m = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m = nanmax(m, nanmax(fabs(v[q].x), fabs(v[q].y)));
+    bits = (unsigned long long)__double_as_longlong(m);
   }
-  atomicMax(colmax + j, (unsigned long long)__double_as_longlong(m));
+  atomicMax(colmax + j, bits);
 }
 
 // then 32 (k) x 32 (j) tiles through shared memory; thread t produces output
