@@ -41,6 +41,11 @@ constexpr int LPD = 64 / SUB;   // lanes per diagonal
 constexpr int DPW = 32 / LPD;  // diagonals per warp tile
 constexpr int SR = SUB * LPD;  // rows per chunk (carry granularity)
 constexpr int SOLVE_WARPS = 4;
+// pass 3's interior tiles regenerate the block entries from integer
+// recurrences (as pass 1 does) instead of loading them per row
+#ifndef SOLVE_P3REC
+#define SOLVE_P3REC 1
+#endif
 
 // L2 residency between the passes: pass 1 reads W with evict_last so pass 3's
 // re-read hits L2 when the batch runs one matrix (or diagonal group) at a time;
@@ -295,6 +300,35 @@ __device__ __forceinline__ void tile_body(const SolveArgs& A, const double* __re
 #pragma unroll
       for (int r = 0; r < SUB; ++r)
         if (r <= re) sm[(s * SUB + r) * DPW + dl] = make_double2(A.L0[ib + r], A.dinv0[ib + r]);
+    } else if (FAST && SOLVE_P3REC) {
+      // interior tiles: pass 1's register form of the chain (agg_body) --
+      // e^2 = B(i) B(k) from exact integer recurrences and e = -sqrt(e^2),
+      // no per-row table loads (pass 3 was L1-bound on 4 loads per row)
+      const int k = ib - m;
+      double qm1 = 1.0, q0 = __ldg(A.d0s + (size_t)(ib / SUB) * n + m);
+      double dg = block_diag(n, m, k);
+      double inc = 2.0 * (double)(n - 2 - 2 * k - m);
+      double bi = (ib + 1.0) * (double)(n - 1 - ib), dbi = (double)(n - 3 - 2 * ib);
+      double bk = (k + 1.0) * (double)(n - 1 - k), dbk = (double)(n - 3 - 2 * k);
+#pragma unroll
+      for (int r = 0; r < SUB; ++r) {
+        const double di = qm1 * fast_rcp(q0);
+        double L = 0.0;
+        if (!(lastrow && r == SUB - 1)) {
+          const double e2 = bi * bk;
+          L = -fast_sqrt(e2) * di;
+          dg += inc;
+          inc -= 4.0;
+          const double q1 = fma(dg, q0, -e2 * qm1);
+          qm1 = q0;
+          q0 = q1;
+          bi += dbi;
+          dbi -= 2.0;
+          bk += dbk;
+          dbk -= 2.0;
+        }
+        sm[(s * SUB + r) * DPW + dl] = make_double2(L, di);
+      }
     } else {
       // Leading-minor form of the pivot recurrence: with q_{-1} = 1 and
       // q_0 = d(k0) (exact dpttrf pivot), q_j = diag q_{j-1} - e^2 q_{j-2}
