@@ -302,7 +302,12 @@ def run_sharded(args):
     h = H if n == N else 0.0025
     be = DeviceBackend(n, dev)
     transport = args.transport
-    if transport == "p2p":
+    if args.layout == "2d":
+        from paper_2206_05466_b200.sharded import BlockShardedStepper
+
+        transport = "nccl"
+        st = BlockShardedStepper(n, be)
+    elif transport == "p2p":
         try:
             from paper_2206_05466_b200.sharded import PeerShardedStepper
 
@@ -310,12 +315,12 @@ def run_sharded(args):
         except Exception as exc:  # no symmetric memory / peer access on this box
             print(f"[bench] p2p transport unavailable ({exc!r}); using NCCL collectives", file=sys.stderr)
             transport = "nccl"
-    if transport == "nccl":
+    if transport == "nccl" and args.layout != "2d":
         st = ShardedStepper(n, be, force_collectives=True)
     r = torch.from_numpy(cfg4_initial_numpy(n)).to(dev)
     w0 = zt.solve_stream(r, be.op)
     w0 = w0 / torch.linalg.norm(w0)
-    rows = w0[st.r0:st.r0 + st.m].contiguous()
+    rows = st.block(w0) if args.layout == "2d" else w0[st.r0:st.r0 + st.m].contiguous()
     for _ in range(args.warmup):
         rows, k, _ = st.midpoint_step(rows, h, TOL, MAX_ITER)
     torch.cuda.synchronize()
@@ -381,10 +386,13 @@ def run_sharded(args):
             "workload": f"cfg5: midpoint step N={n}, h={h}", "N": n, "h": h, "tol": TOL, "max_iter": MAX_ITER,
             "init": f"W0 = lap^-1(random_admissible({n}, default_rng(0), 1/{n})) / ||.||_F",
             "iterations_per_step": sorted(set(iters))},
-        "implementation": {"parallelism": f"rowblock{world}", "transport": transport, "graph": bool(getattr(st, "graph", False)),
+        "implementation": {"parallelism": (f"block{st.pr}x{st.pc}" if args.layout == "2d" else f"rowblock{world}"),
+                           "transport": transport, "graph": bool(getattr(st, "graph", False)),
                    "collectives": ("all-gather of X and all-to-all of a fused into the GEMM epilogues as NVLink "
                                    "peer stores (torch symmetric memory), rank barrier + NCCL all_reduce(max "
                                    "residual) per update") if transport == "p2p" else
+                                  "NCCL block all_gather(X) + all_gather(a) + all_reduce(max residual) per update "
+                                  "(2-D blocks, BlockShardedStepper)" if args.layout == "2d" else
                                   "NCCL all_gather(X) + all_to_all(a tiles) + all_reduce(max residual) per update",
                    "l2": "no flush: per-step working set > 126 MB L2"},
         "roofline": {"bound": "tensor", "kernel": "whole sharded step (all ranks)", "achieved": achieved,
@@ -732,6 +740,9 @@ def main():
                          "conditional WHILE node, residual all-reduce by peer stores)")
     ap.add_argument("--replicas", action="store_true",
                     help="with WORLD_SIZE > 1: independent replicas per rank instead of sharding")
+    ap.add_argument("--layout", choices=("rows", "2d"), default="rows",
+                    help="sharded step layout: row blocks (default) or 2-D blocks over a near-square process grid "
+                         "(NCCL block all-gathers)")
     ap.add_argument("--n", type=int, default=N, help="matrix size for --sharded (cfg 5: 4096, 8192)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -739,7 +750,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
-    elif args.sharded or (world > 1 and not args.replicas):
+    elif args.sharded or args.layout == "2d" or (world > 1 and not args.replicas):
         run_sharded(args)
     else:
         run_ours(args)

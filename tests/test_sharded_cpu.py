@@ -30,6 +30,9 @@ class CpuBackend:
     def gemm_rows(self, p_rows, x_full):
         return p_rows @ x_full
 
+    def gemm_block(self, a_rows, b_full, c0, mc):
+        return a_rows @ b_full[:, c0:c0 + mc]
+
     def update_rows(self, a_rows, p, ah_rows, base, xprev, hh, qq):
         out = base + hh * (a_rows - ah_rows) + qq * (a_rows @ p)
         res = float((out - xprev).abs().max()) if xprev is not None else 0.0
@@ -44,16 +47,20 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, h, steps, max_iter, q):
+def _worker(rank, world, port, n, h, steps, max_iter, q, grid=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2206_05466_b200.sharded import ShardedStepper  # noqa: WPS433
+        from paper_2206_05466_b200.sharded import BlockShardedStepper, ShardedStepper  # noqa: WPS433
 
-        st = ShardedStepper(n, CpuBackend())
         w = torch.from_numpy(zo.smooth_initial(n))
-        rows = w[st.r0:st.r0 + st.m].clone()
+        if grid is None:
+            st = ShardedStepper(n, CpuBackend())
+            rows = w[st.r0:st.r0 + st.m].clone()
+        else:
+            st = BlockShardedStepper(n, CpuBackend(), grid=grid if grid != "auto" else None)
+            rows = st.block(w)
         iters = []
         for _ in range(steps):
             rows, k, _ = st.midpoint_step(rows, h, max_iter=max_iter)
@@ -68,11 +75,11 @@ def _worker(rank, world, port, n, h, steps, max_iter, q):
         dist.destroy_process_group()
 
 
-def _run(world, n, h, steps, max_iter=10):
+def _run(world, n, h, steps, max_iter=10, grid=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, h, steps, max_iter, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, h, steps, max_iter, q, grid)) for r in range(world)]
     for p in procs:
         p.start()
     out = q.get(timeout=240)
@@ -92,6 +99,38 @@ def test_sharded_step_matches_oracle(world, n):
         ref_iters.append(k)
     assert iters == ref_iters
     assert np.linalg.norm(full - w) / np.linalg.norm(w) <= 1e-13
+
+
+@pytest.mark.parametrize("world,n,grid", [(2, 16, (1, 2)), (2, 16, (2, 1)), (4, 16, "auto"), (4, 24, (1, 4))])
+def test_block_sharded_step_matches_oracle(world, n, grid):
+    """2-D block layout (BlockShardedStepper): block all-gathers of X and a,
+    block products, the (a^H) block from the gathered a; identical iteration
+    counts and W after 3 steps against the oracle."""
+    status, full, iters = _run(world, n, h=0.01, steps=3, grid=grid)
+    assert status == "ok", (status, full)
+    w = zo.smooth_initial(n)
+    ref_iters = []
+    for _ in range(3):
+        w, k, _ = zo.midpoint_step(w, 0.01)
+        ref_iters.append(k)
+    assert iters == ref_iters
+    err = np.linalg.norm(full - w) / np.linalg.norm(w)
+    assert err <= 1e-13, (err, np.abs(full - w).max(axis=1))
+
+
+def test_block_sharded_non_convergence_raises():
+    status, name, iters = _run(4, 16, h=0.5, steps=1, max_iter=1, grid="auto")
+    assert status == "err" and name == "FixedPointError" and iters == 1
+
+
+def test_block_grid_and_shapes():
+    from paper_2206_05466_b200.sharded import BlockShardedStepper, block_grid
+
+    assert [block_grid(g) for g in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
+    st = BlockShardedStepper(12, CpuBackend())  # no process group: one 1 x 1 block
+    assert (st.mr, st.mc, st.r0, st.c0) == (12, 12, 0, 0)
+    with pytest.raises(ValueError, match="process grid"):
+        BlockShardedStepper(12, CpuBackend(), grid=(1, 2))
 
 
 def test_sharded_non_convergence_raises():
