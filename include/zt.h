@@ -160,12 +160,13 @@ int zt_oz_modgemm(int nmod, int mp, int np, int kp, const void* a, const void* b
 int zt_oz_moduli(int* out, int cap);
 int zt_oz_iotas(int* out, int cap);
 /* C = A B (complex128, n x n, row-major with leading dimensions) through the
- * residue GEMM: rows of A and columns of B scaled to integers of up to 53
- * bits, 17 moduli <= 241, CRT reconstruction from 42-bit FP64 pieces; a
+ * residue GEMM: rows of A and columns of B scaled to integers of
+ * zt_oz_bits(n) bits (55 up to n = 4096, 54 above), 17 moduli <= 241, exact
+ * CRT reconstruction in FP64 pieces; a
  * row of A or column of B holding a NaN or an infinity gives a NaN row /
  * column of C.  bmode 1: B is
  * skew-Hermitian with B[k][j] == -conj(B[j][k]) exactly off the diagonal
- * (converted row-wise, no transpose).  lower: only the 128-tiles of C on or
+ * (converted row-wise, no transpose).  lower: only the 256-tiles of C on or
  * below the diagonal.  workspace: zt_oz_workspace_bytes(n). */
 size_t zt_oz_workspace_bytes(int n);
 /* CUDA-event totals of the residue-GEMM launches recorded while profiling
