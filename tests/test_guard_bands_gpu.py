@@ -27,10 +27,10 @@ SIZES = [2, 3, 13, 97, 130, 257, 300, 513]
 class Guarded:
     """`nbytes` of device memory with pattern-filled bands on both sides."""
 
-    def __init__(self, nbytes, dev):
+    def __init__(self, nbytes, dev, fill=PAT):
         self.nbytes = int(nbytes)
         self.pad = (-self.nbytes) % 16
-        self.raw = torch.full((2 * GUARD + self.nbytes + self.pad,), PAT, dtype=torch.uint8, device=dev)
+        self.raw = torch.full((2 * GUARD + self.nbytes + self.pad,), fill, dtype=torch.uint8, device=dev)
 
     @property
     def ptr(self):
@@ -274,3 +274,59 @@ def test_oz_building_blocks_exact_buffers(lib, m, n, nc):
         assert bool((t.body().view(r0 + m, mloc * 16)[:r0] == PAT).all()), "rows above r0 overwritten"
         if w < mloc:
             assert bool((t.body().view(r0 + m, mloc, 16)[:, w:] == PAT).all()), "columns past the block overwritten"
+
+
+def _nan_padded(x, ld, dev):
+    """x (rows x cols complex128) inside rows of length ld; every pad element
+    and both guard bands are all-ones bytes (NaN as a double): a read outside
+    the matrix that reaches a result turns it into NaN."""
+    rows, cols = x.shape
+    g = Guarded(16 * rows * ld, dev, fill=0xFF)
+    g.body(torch.complex128).view(rows, ld)[:, :cols] = x
+    return g
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_inputs_read_inside_their_bounds(zt, lib, n):
+    """Inputs with padded leading dimensions whose pads and surroundings are
+    NaN: the results equal the contiguous-input results bit for bit (the
+    solve and the stencil also ignore a NaN strict upper triangle,
+    laplacian.py:370-431 reads the lower triangle only)."""
+    dev = torch.device("cuda:0")
+    s = _stream(dev)
+    op = zt.build_operator(n, dev)
+    w = torch.from_numpy(_w(n, 5)[0]).to(dev)
+    wl = w.clone()
+    wl[torch.triu(torch.ones(n, n, dtype=torch.bool, device=dev), 1)] = complex(float("nan"), float("nan"))
+    ld = n + 3
+    gw = _nan_padded(wl, ld, dev)
+    p = torch.empty_like(w)
+    wsb = lib.zt_solve_workspace_bytes(n, 1)
+    ws = Guarded(wsb, dev)
+    assert lib.zt_stream_solve_ws(op.handle, gw.ptr, ld, 0, p.data_ptr(), n, 0, 1, ws.ptr, wsb, s) == 0
+    assert torch.equal(p, zt.solve_stream(w, op, check=False))
+    for sign in (-1, 1):
+        y = torch.empty_like(w)
+        assert lib.zt_apply_laplacian(op.handle, gw.ptr, ld, 0, y.data_ptr(), n, 0, sign, 1, s) == 0
+        assert torch.equal(y, zt.apply_laplacian(w, sign, op))
+    # residuals of a padded matrix
+    gfull = _nan_padded(w, ld, dev)
+    out, out2 = torch.empty(3, dtype=torch.float64, device=dev), torch.empty(3, dtype=torch.float64, device=dev)
+    assert lib.zt_residuals(n, gfull.ptr, ld, out.data_ptr(), s) == 0
+    assert lib.zt_residuals(n, w.data_ptr(), n, out2.data_ptr(), s) == 0
+    assert torch.equal(out, out2)
+    # products with padded operands
+    rng = np.random.default_rng(6)
+    a = torch.from_numpy(rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).to(dev)
+    b = torch.from_numpy(rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).to(dev)
+    ga, gb = _nan_padded(a, n + 1, dev), _nan_padded(b, n + 5, dev)
+    wsz = lib.zt_oz_workspace_bytes(n)
+    wk = torch.empty(wsz, dtype=torch.uint8, device=dev)
+    c1, c2 = torch.empty_like(a), torch.empty_like(a)
+    assert lib.zt_oz_zgemm(n, ga.ptr, n + 1, gb.ptr, n + 5, 0, c1.data_ptr(), n, 0, wk.data_ptr(), wsz, s) == 0
+    assert lib.zt_oz_zgemm(n, a.data_ptr(), n, b.data_ptr(), n, 0, c2.data_ptr(), n, 0, wk.data_ptr(), wsz, s) == 0
+    assert torch.equal(c1, c2)
+    for algo in (0, 1):
+        assert lib.zt_zgemm(n, ga.ptr, n + 1, gb.ptr, n + 5, c1.data_ptr(), n, algo, s) == 0
+        assert lib.zt_zgemm(n, a.data_ptr(), n, b.data_ptr(), n, c2.data_ptr(), n, algo, s) == 0
+        assert torch.equal(c1, c2)
