@@ -66,3 +66,28 @@ def test_no_cpu_fallback_in_product_path():
             # (basis.py's `wigner_basis_oracle` is the reference's own API name)
             for bad in ("import oracle", "from oracle", "zeitlin_oracle", "scipy", "import numba"):
                 assert bad not in src, (f, bad)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libzt.so the package does not import (and says
+    how to build it); on a box without a GPU the public ops raise instead of
+    computing on the host."""
+    import sys
+
+    env = dict(os.environ, ZT_LIB_PATH=str(tmp_path / "absent" / "libzt.so"), PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", "import paper_2206_05466_b200"], capture_output=True, text=True,
+                       env=env)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "no CPU fallback" in r.stderr
+    import torch
+
+    if not torch.cuda.is_available():
+        import numpy as np
+
+        import paper_2206_05466_b200 as zt
+
+        w = np.zeros((4, 4), dtype=np.complex128)
+        with pytest.raises(Exception):
+            zt.solve_stream(w)
+        with pytest.raises(Exception):
+            zt.midpoint_step_info(zt.StepperState(w=w, h=0.01))
