@@ -182,7 +182,7 @@ def run_reference(args):
         },
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -462,7 +462,7 @@ def run_sharded(args):
         "clocks": clk.summary(),
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -759,7 +759,7 @@ def run_ours(args):
                       + f"; BLAS: {'; '.join(blas)}",
         }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -776,6 +776,30 @@ def OZ_L2_BYTES(pd, nmod):
 # builds (profiles/r02_ncu_summary.md)
 OZ_FLOORS_US = {"tma_only": 104.0, "mma_only": 142.3, "tma_and_mma": 176.0, "no_residue_stores": 186.0}
 TRAFFIC_FUSED = (1076.058 + 133.951 + 235.954 + 41.891 + 167.733 + 58.371) * 1e6
+
+
+_REAL_STDOUT = None
+
+
+def claim_stdout():
+    """stdout carries exactly ONE JSON line: everything else written to fd 1
+    (NCCL's `NCCL version ...` banner when the box sets NCCL_DEBUG, library
+    notices) is sent to stderr for the whole run."""
+    global _REAL_STDOUT
+    if _REAL_STDOUT is None:
+        sys.stdout.flush()
+        _REAL_STDOUT = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    sys.stdout.flush()
+    if _REAL_STDOUT is None:
+        sys.stdout.buffer.write(data)
+        sys.stdout.flush()
+    else:
+        os.write(_REAL_STDOUT, data)
 
 
 def main():
@@ -802,6 +826,7 @@ def main():
                          "(NCCL block all-gathers)")
     ap.add_argument("--n", type=int, default=N, help="matrix size for --sharded (cfg 5: 4096, 8192)")
     args = ap.parse_args()
+    claim_stdout()
     if args.warmup < 3:
         args.warmup = 3
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -167,3 +167,28 @@ def test_bench_arms_print_the_same_config():
     b = bench.bench_config([2])
     assert a == b
     assert set(a) == {"workload", "N", "h", "tol", "max_iter", "init", "iterations_per_step"}
+
+
+def test_bench_stdout_is_one_json_line(tmp_path):
+    """bench.py's stdout carries exactly one JSON line even when a library
+    writes to fd 1 during the run (NCCL prints its version banner there when
+    the box sets NCCL_DEBUG): claim_stdout() points fd 1 at stderr and emit()
+    writes the line to the original stdout."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import os, sys; sys.argv = ['bench.py']; sys.path.insert(0, %r)\n"
+        "import bench\n"
+        "bench.claim_stdout()\n"
+        "os.write(1, b'NCCL version 0.0.0+test\\n')\n"
+        "print('a library notice')\n"
+        "bench.emit({'metric': 'm', 'value': 1.5})\n" % ROOT
+    )
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1 and __import__("json").loads(lines[0]) == {"metric": "m", "value": 1.5}
+    assert "NCCL version 0.0.0+test" in r.stderr and "a library notice" in r.stderr
